@@ -1,0 +1,172 @@
+/*
+ * enmf_gpu.h — C-ABI of the B200-native extrapolated-NMF hot path.
+ *
+ * This is the drop-in boundary for the per-outer-iteration path of the
+ * reference library `enmf` (header-only C++20, /root/reference/proj/include/enmf).
+ * The reference has no FFI layer: its boundary is the template API
+ *
+ *   RunRecord enmf::run(const MatrixX& x, const DenseMatrix& w0, const DenseMatrix& h0,
+ *                       const SolverConfig& cfg, TimingMode timing)       engine.hpp:447-449
+ *   IterationRecord enmf::step(...)                                      engine.hpp:309-311
+ *
+ * Every entry point below replaces one of those (or one of the public kernels
+ * the reference's own tests call: gram / cross_wx / cross_xht / hals_solve /
+ * active_set_solve / fast_error / update_beta).  Plain pointers and sizes only;
+ * all matrices are row-major FP64 exactly as `enmf::DenseMatrix` stores them
+ * (matrix.hpp:65-66: element (i,j) at v[i*cols+j]); CSR uses 64-bit offsets and
+ * column indices like `enmf::SparseMatrix` (matrix.hpp:255-257).
+ *
+ * Errors: the reference throws C++ exceptions; here every call returns one of
+ * the ENMF_* codes below and the message is available from enmf_gpu_last_error()
+ * (thread-local).  include/enmf_gpu.hpp maps the codes back onto the reference's
+ * exception types.
+ *
+ * Thread safety: one enmf_gpu_ctx per calling thread.  Distinct contexts may be
+ * used concurrently (the reference's run_suite runs independent run() calls on a
+ * thread pool, bench.hpp:273-292).
+ */
+#ifndef ENMF_GPU_H_
+#define ENMF_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes (reference exception → code). */
+enum {
+  ENMF_OK = 0,
+  ENMF_INVALID_ARGUMENT = 1,   /* std::invalid_argument          engine.hpp:175-199,450-459 */
+  ENMF_NON_FINITE = 2,         /* enmf::NonFiniteIterate          engine.hpp:51-54 */
+  ENMF_NO_CONVERGENCE = 3,     /* enmf::NoConvergence             nnls.hpp:65-68, engine.hpp:290-292 */
+  ENMF_DEGENERATE_COLUMN = 4,  /* enmf::DegenerateColumn          nnls.hpp:54-63 */
+  ENMF_CUDA_ERROR = 5,         /* device / driver failure (no reference analogue) */
+  ENMF_CACHE_STALE = 6         /* enmf::CacheStale                engine.hpp:41-44 */
+};
+
+/* enmf::InnerSolver (engine.hpp:56) */
+enum { ENMF_INNER_EXACT = 0, ENMF_INNER_HALS = 1 };
+/* enmf::TimingMode (engine.hpp:58) */
+enum { ENMF_TIMING_WALL = 0, ENMF_TIMING_NONE = 1 };
+/* Arithmetic of the device path. FP64 is the parity path. */
+enum { ENMF_PRECISION_FP64 = 0 };
+
+/* 1:1 with enmf::SolverConfig (engine.hpp:149-173).  `inner_max_sweeps` = 0
+ * means "std::nullopt" (derive from the setup/sweep cost ratio). */
+typedef struct enmf_gpu_config {
+  int32_t inner_h;               /* ENMF_INNER_* */
+  int32_t inner_w;               /* ENMF_INNER_* */
+  int32_t hp;                    /* 1 | 2 | 3 */
+  int32_t extrapolation_enabled; /* bool */
+  double beta0;
+  double gamma;
+  double gamma_bar;
+  double eta;
+  uint64_t max_outer_iterations;
+  double max_seconds;            /* +inf = no budget */
+  int32_t literal_hp1_order;     /* bool */
+  int32_t timing;                /* ENMF_TIMING_* */
+  double inner_sweep_ratio;
+  double inner_stall_fraction;
+  uint64_t inner_max_sweeps;     /* 0 = derive */
+  uint64_t reinit_seed;
+  int32_t precision;             /* ENMF_PRECISION_* */
+  int32_t reserved;
+} enmf_gpu_config;
+
+/* enmf::IterationRecord (engine.hpp:216-223) plus per-iteration
+ * instrumentation the reference does not record (used by parity tests). */
+typedef struct enmf_gpu_iter {
+  uint64_t iteration;
+  double elapsed_seconds;
+  double error;
+  double relative_error;
+  double beta;
+  int32_t restarted;
+  int32_t inner_h_count;   /* HALS sweeps (or BPP rounds) of the H update */
+  int32_t inner_w_count;   /* HALS sweeps (or BPP rounds) of the W update */
+  int32_t reinit_events;   /* bit0: W_y columns redrawn, bit1: target rows redrawn */
+} enmf_gpu_iter;
+
+/* enmf::BetaSchedule (engine.hpp:63-70) */
+typedef struct enmf_gpu_beta_schedule {
+  double beta, beta_bar, beta_prev, gamma, gamma_bar, eta;
+} enmf_gpu_beta_schedule;
+
+typedef struct enmf_gpu_ctx enmf_gpu_ctx;
+
+/* Fills `cfg` with the defaults of enmf::SolverConfig (engine.hpp:149-173). */
+void enmf_gpu_config_default(enmf_gpu_config* cfg);
+/* Named presets of enmf::detail::algorithm_config (bench.hpp:108-135):
+ * "anls", "e-anls-hp1", "e-anls-hp3", "ahals", "e-ahals-hp1", "e-ahals-hp3". */
+int enmf_gpu_config_preset(enmf_gpu_config* cfg, const char* name);
+/* SolverConfig::validate (engine.hpp:175-199). */
+int enmf_gpu_config_validate(const enmf_gpu_config* cfg);
+/* update_beta (engine.hpp:88-99) — host scalar logic, identical on device. */
+enmf_gpu_beta_schedule enmf_gpu_update_beta(enmf_gpu_beta_schedule s, int error_decreased);
+
+/* Context: owns the CUDA stream, device buffers and captured graphs.
+ * device < 0 selects the current device. */
+int enmf_gpu_create(enmf_gpu_ctx** out, int device);
+void enmf_gpu_destroy(enmf_gpu_ctx* ctx);
+const char* enmf_gpu_last_error(void);
+/* Number of device kernels this context has launched since creation. */
+uint64_t enmf_gpu_kernel_launches(const enmf_gpu_ctx* ctx);
+
+/* ---- drop-in for enmf::run<DenseMatrix> (engine.hpp:447-521) ----------------
+ * x: m×n, w0: m×r, h0: r×n (host, row-major).  iters receives entries 0..K
+ * (entry 0 = initial pair), at most iters_cap of them; *n_iters gets the count.
+ * w_out (m×r) / h_out (r×n) receive RunRecord::factors; *norm_x = ‖X‖_F. */
+int enmf_gpu_run_dense(enmf_gpu_ctx* ctx, const double* x, size_t m, size_t n,
+                       const double* w0, const double* h0, size_t r,
+                       const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
+                       size_t* n_iters, double* w_out, double* h_out, double* norm_x);
+
+/* ---- drop-in for enmf::run<SparseMatrix> (engine.hpp:447-521 with the CSR
+ * kernels linalg.hpp:86-104,127-146,167-171).  offsets: m+1, col_idx/vals: nnz. */
+int enmf_gpu_run_csr(enmf_gpu_ctx* ctx, const uint64_t* offsets, const uint64_t* col_idx,
+                     const double* vals, size_t m, size_t n, size_t nnz,
+                     const double* w0, const double* h0, size_t r,
+                     const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
+                     size_t* n_iters, double* w_out, double* h_out, double* norm_x);
+
+/* ---- resident-data API (bench / repeated solves on one X) -------------------
+ * Upload X once (from host or from a device pointer), then solve from device
+ * or host factors.  *_device pointers are CUDA device pointers. */
+int enmf_gpu_load_dense(enmf_gpu_ctx* ctx, const double* x, size_t m, size_t n, int x_on_device);
+int enmf_gpu_solve(enmf_gpu_ctx* ctx, const double* w0, const double* h0, size_t r,
+                   int factors_on_device, const enmf_gpu_config* cfg, enmf_gpu_iter* iters,
+                   size_t iters_cap, size_t* n_iters, double* w_out, double* h_out,
+                   double* norm_x);
+
+/* ---- public kernels the reference's tests call (host pointers) -------------- */
+/* gram (linalg.hpp:49-64): a m×r → g r×r, bitwise symmetric. */
+int enmf_gpu_gram(enmf_gpu_ctx* ctx, const double* a, size_t m, size_t r, double* g);
+/* cross_wx (linalg.hpp:67-83): w m×r, x m×n → out r×n. */
+int enmf_gpu_cross_wx(enmf_gpu_ctx* ctx, const double* w, const double* x, size_t m, size_t n,
+                      size_t r, double* out);
+/* cross_xht (linalg.hpp:107-124): x m×n, h r×n → out m×r. */
+int enmf_gpu_cross_xht(enmf_gpu_ctx* ctx, const double* x, const double* h, size_t m, size_t n,
+                       size_t r, double* out);
+/* frob_norm_sq (linalg.hpp:160-171), compensated. */
+int enmf_gpu_frob_norm_sq(enmf_gpu_ctx* ctx, const double* x, size_t count, double* out);
+/* fast_error (engine.hpp:121-136): w m×r, xht m×r, hht r×r. */
+int enmf_gpu_fast_error(enmf_gpu_ctx* ctx, double norm_x_sq, const double* w, const double* xht,
+                        const double* hht, size_t m, size_t r, double* err);
+/* hals_solve (nnls.hpp:154-176) with InnerLoopPolicy{max_sweeps, stall_fraction}:
+ * gram r×r, cross r×n, h0 r×n → h r×n; *sweeps = sweeps performed. */
+int enmf_gpu_hals_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cross,
+                        const double* h0, size_t r, size_t n, uint64_t max_sweeps,
+                        double stall_fraction, double* h, int32_t* sweeps);
+/* active_set_solve (nnls.hpp:259-406): gram r×r, cross r×n, h0 r×n → h r×n;
+ * *rounds = max exchange rounds over the columns. */
+int enmf_gpu_active_set_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cross,
+                              const double* h0, size_t r, size_t n, double* h, int32_t* rounds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ENMF_GPU_H_ */

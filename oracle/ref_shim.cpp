@@ -1,0 +1,180 @@
+// ref_shim.cpp — C-ABI wrapper around the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile against
+// /root/reference/proj/include (read in place, never copied) into
+// oracle/_ref/libenmf_ref.so.  It exposes the reference's own enmf::run,
+// hals_solve, active_set_solve, gram, cross_* and fast_error through the same
+// signatures as oracle/enmf_oracle.h (ref_* instead of orc_*), so tests can
+// pin the C restatement bit-for-bit against the reference, and bench.py
+// --impl reference can time the reference's CPU path.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <enmf/data.hpp>
+#include <enmf/engine.hpp>
+#include <enmf/linalg.hpp>
+#include <enmf/matrix.hpp>
+#include <enmf/nnls.hpp>
+#include <enmf/rng.hpp>
+
+#include "../include/enmf_gpu.h"
+
+namespace {
+thread_local std::string g_err;
+
+enmf::DenseMatrix dm(const double* p, std::size_t rows, std::size_t cols) {
+  return enmf::DenseMatrix(rows, cols, std::vector<double>(p, p + rows * cols));
+}
+void out(const enmf::DenseMatrix& a, double* p) {
+  if (p) std::memcpy(p, a.data(), sizeof(double) * a.size());
+}
+enmf::SolverConfig to_cfg(const enmf_gpu_config* c) {
+  enmf::SolverConfig s;
+  s.inner_h = c->inner_h == ENMF_INNER_EXACT ? enmf::InnerSolver::exact : enmf::InnerSolver::hals;
+  s.inner_w = c->inner_w == ENMF_INNER_EXACT ? enmf::InnerSolver::exact : enmf::InnerSolver::hals;
+  s.hp = c->hp;
+  s.beta0 = c->beta0;
+  s.gamma = c->gamma;
+  s.gamma_bar = c->gamma_bar;
+  s.eta = c->eta;
+  s.max_outer_iterations = c->max_outer_iterations;
+  s.max_seconds = c->max_seconds;
+  s.extrapolation_enabled = c->extrapolation_enabled != 0;
+  s.literal_hp1_order = c->literal_hp1_order != 0;
+  s.inner_sweep_ratio = c->inner_sweep_ratio;
+  s.inner_stall_fraction = c->inner_stall_fraction;
+  if (c->inner_max_sweeps) s.inner_max_sweeps = c->inner_max_sweeps;
+  s.reinit_seed = c->reinit_seed;
+  return s;
+}
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return ENMF_OK;
+  } catch (const enmf::NonFiniteIterate& e) { g_err = e.what(); return ENMF_NON_FINITE;
+  } catch (const enmf::NoConvergence& e) { g_err = e.what(); return ENMF_NO_CONVERGENCE;
+  } catch (const enmf::DegenerateColumn& e) { g_err = e.what(); return ENMF_DEGENERATE_COLUMN;
+  } catch (const enmf::CacheStale& e) { g_err = e.what(); return ENMF_CACHE_STALE;
+  } catch (const std::invalid_argument& e) { g_err = e.what(); return ENMF_INVALID_ARGUMENT;
+  } catch (const std::exception& e) { g_err = e.what(); return ENMF_INVALID_ARGUMENT; }
+}
+void fill_record(const enmf::RunRecord& rec, enmf_gpu_iter* iters, std::size_t cap,
+                 std::size_t* n_iters) {
+  for (std::size_t k = 0; k < rec.iterations.size() && k < cap; ++k) {
+    const auto& it = rec.iterations[k];
+    std::memset(&iters[k], 0, sizeof iters[k]);
+    iters[k].iteration = it.iteration;
+    iters[k].elapsed_seconds = it.elapsed_seconds;
+    iters[k].error = it.error;
+    iters[k].relative_error = it.relative_error;
+    iters[k].beta = it.beta;
+    iters[k].restarted = it.restarted ? 1 : 0;
+  }
+  if (n_iters) *n_iters = rec.iterations.size();
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_run_dense(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                  const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
+                  size_t* n_iters, double* w_out, double* h_out, double* norm_x) {
+  return guard([&] {
+    const auto X = dm(x, m, n);
+    const auto rec = enmf::run(X, dm(w0, m, r), dm(h0, r, n), to_cfg(cfg),
+                               cfg->timing == ENMF_TIMING_NONE ? enmf::TimingMode::none
+                                                               : enmf::TimingMode::wall);
+    fill_record(rec, iters, iters_cap, n_iters);
+    out(rec.factors.w, w_out);
+    out(rec.factors.h, h_out);
+    if (norm_x) *norm_x = rec.norm_x;
+  });
+}
+
+int ref_run_csr(const uint64_t* off, const uint64_t* cidx, const double* vals, size_t m, size_t n,
+                size_t nnz, const double* w0, const double* h0, size_t r,
+                const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
+                size_t* n_iters, double* w_out, double* h_out, double* norm_x) {
+  return guard([&] {
+    enmf::SparseMatrix X(m, n, std::vector<std::size_t>(off, off + m + 1),
+                         std::vector<std::size_t>(cidx, cidx + nnz),
+                         std::vector<double>(vals, vals + nnz));
+    const auto rec = enmf::run(X, dm(w0, m, r), dm(h0, r, n), to_cfg(cfg),
+                               cfg->timing == ENMF_TIMING_NONE ? enmf::TimingMode::none
+                                                               : enmf::TimingMode::wall);
+    fill_record(rec, iters, iters_cap, n_iters);
+    out(rec.factors.w, w_out);
+    out(rec.factors.h, h_out);
+    if (norm_x) *norm_x = rec.norm_x;
+  });
+}
+
+int ref_gram(const double* a, size_t m, size_t r, double* g) {
+  return guard([&] { out(enmf::gram(dm(a, m, r)), g); });
+}
+int ref_cross_wx(const double* w, const double* x, size_t m, size_t n, size_t r, double* o) {
+  return guard([&] { out(enmf::cross_wx(dm(w, m, r), dm(x, m, n)), o); });
+}
+int ref_cross_xht(const double* x, const double* h, size_t m, size_t n, size_t r, double* o) {
+  return guard([&] { out(enmf::cross_xht(dm(x, m, n), dm(h, r, n)), o); });
+}
+int ref_frob_norm_sq(const double* x, size_t m, size_t n, double* o) {
+  return guard([&] { *o = enmf::frob_norm_sq(dm(x, m, n)); });
+}
+int ref_fast_error(double nx2, const double* w, const double* xht, const double* hht, size_t m,
+                   size_t r, double* e) {
+  return guard([&] { *e = enmf::fast_error(nx2, dm(w, m, r), dm(xht, m, r), dm(hht, r, r)); });
+}
+int ref_hals_solve(const double* gram, const double* cross, const double* h0, size_t r, size_t n,
+                   uint64_t max_sweeps, double stall, double* h) {
+  return guard([&] {
+    enmf::NnlsProblem p;
+    p.gram = dm(gram, r, r);
+    p.cross = dm(cross, r, n);
+    enmf::InnerLoopPolicy pol;
+    pol.max_sweeps = max_sweeps;
+    pol.stall_fraction = stall;
+    out(enmf::hals_solve(p, dm(h0, r, n), pol), h);
+  });
+}
+int ref_active_set_solve(const double* gram, const double* cross, const double* h0, size_t r,
+                         size_t n, double* h) {
+  return guard([&] {
+    enmf::NnlsProblem p;
+    p.gram = dm(gram, r, r);
+    p.cross = dm(cross, r, n);
+    out(enmf::active_set_solve(p, dm(h0, r, n)), h);
+  });
+}
+void ref_update_beta(const enmf_gpu_beta_schedule* in, int dec, enmf_gpu_beta_schedule* o) {
+  enmf::BetaSchedule s;
+  s.beta = in->beta; s.beta_bar = in->beta_bar; s.beta_prev = in->beta_prev;
+  s.gamma = in->gamma; s.gamma_bar = in->gamma_bar; s.eta = in->eta;
+  const auto t = enmf::update_beta(s, dec != 0);
+  o->beta = t.beta; o->beta_bar = t.beta_bar; o->beta_prev = t.beta_prev;
+  o->gamma = t.gamma; o->gamma_bar = t.gamma_bar; o->eta = t.eta;
+}
+void ref_gen_lowrank(size_t m, size_t n, size_t r, uint64_t seed, double* x) {
+  out(enmf::gen_lowrank(m, n, r, seed), x);
+}
+void ref_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* w, double* h) {
+  auto p = enmf::random_init(m, n, r, seed);
+  out(p.first, w);
+  out(p.second, h);
+}
+uint64_t ref_mix_seed(uint64_t b, uint64_t x, uint64_t y) { return enmf::mix_seed(b, x, y); }
+int ref_config_preset(const char* name, enmf_gpu_config* c) {
+  // bench.hpp's algorithm_config needs <json.hpp>; the presets are restated in
+  // the product (enmf_gpu_config_preset) and pinned by tests against bench.hpp:108-135.
+  (void)name; (void)c;
+  return ENMF_INVALID_ARGUMENT;
+}
+
+}  // extern "C"
