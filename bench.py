@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py — E-A-HALS outer iterations/s on the BASELINE.json headline config.
+
+Workload (BASELINE.json configs[4], "C5"): dense synthetic m = n = 32768,
+r = 128, X = W0·H0 + |N(0, 0.01²)| with W0, H0 ~ U[0,1), E-A-HALS hp = 3
+(beta0 .5, eta 1.5, gamma 1.01, gamma_bar 1.005), FP64.  One step = one outer
+iteration (engine.hpp:309-440) of the B200 path on HBM-resident data.
+
+Our arm prints one JSON line with value (device-timed it/s), e2e (the C-ABI
+enmf_gpu_run_dense call on pinned host buffers, copies included), roofline (the
+dominant FP64 DMMA GEMM, timed with CUDA events on the engine's stream),
+cpu_baseline (the reference's enmf::step on a bounded sample on the host
+cores), clocks and gpu_launches.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified headers compiled in place; the C restatement if _ref is absent) on
+the host cores, same metric/config, each step a bounded sample.
+
+Multi-GPU (torchrun, N > 1): each rank runs its own C5 problem (replicas, no
+collective; SURVEY §8(e) sharding of ONE problem is the next row), value = the
+sum over ranks of K / (max over ranks of the device time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = 32768
+R = 128
+METRIC = "E-A-HALS outer iters/sec + % roofline, 32768² r=128, 1/2/4/8 B200"
+UNIT = "outer_iters/s"
+FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.txt)
+FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry)"
+
+
+def cfg_c5(iters):
+    import paper_1805_06604_b200 as E
+    c = E.algorithm_config("e-ahals-hp3")
+    c.max_outer_iterations = iters
+    return c
+
+
+def config_block(args, world):
+    return {"workload": "C5: dense m=n=32768 r=128, X=W0·H0+|N(0,0.01²)|, E-A-HALS hp3 (BASELINE.json configs[4])",
+            "m": M, "n": N, "r": R, "algorithm": "e-ahals-hp3", "precision": "fp64",
+            "beta0": 0.5, "eta": 1.5, "gamma": 1.01, "gamma_bar": 1.005,
+            "l2": "inputs larger than L2 (X = 8.59 GB FP64 vs 126 MB L2); no flush needed",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ CPU baseline
+SAMPLE_L = 2048
+
+
+def _load_cpu(kind_pref="reference"):
+    from oracle.oracle import Oracle
+    try:
+        if kind_pref == "reference":
+            return Oracle("reference"), "reference"
+    except Exception:
+        pass
+    return Oracle("port"), "port"
+
+
+def cpu_reference_throughput(threads, steps_per_thread, seed=11):
+    """Runs the reference's enmf::step on SAMPLE_L² r=128 sub-problems of C5,
+    one independent problem per host thread (run_suite's parallelism,
+    bench.hpp:273-292), and converts to C5-equivalent outer it/s by the m·n
+    ratio (per-iteration cost ∝ m·n·r; at this sample size the HALS sweeps weigh
+    ~30% more than at C5, so the estimate is conservative for the CPU)."""
+    import ctypes as C
+    import numpy as np
+    from oracle.oracle import Config, preset
+    orc, kind = _load_cpu("reference")
+    fn = getattr(orc.lib, "ref_time_steps" if kind == "reference" else "orc_time_steps")
+    dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+    fn.argtypes = [dp, C.c_size_t, C.c_size_t, dp, dp, C.c_size_t, C.POINTER(Config), C.c_size_t,
+                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    fn.restype = C.c_int
+    L = SAMPLE_L
+    cfg = preset("e-ahals-hp3", max_outer_iterations=steps_per_thread)
+    problems = []
+    for t in range(threads):
+        rng = np.random.default_rng(seed + t)
+        w0 = rng.random((L, R))
+        h0 = rng.random((R, L))
+        x = w0 @ h0 + 0.01 * np.abs(rng.standard_normal((L, L)))
+        wi, hi = rng.random((L, R)), rng.random((R, L))
+        problems.append((np.ascontiguousarray(x), wi, hi))
+    secs = [0.0] * threads
+    errs = [0] * threads
+
+    def work(i):
+        x, wi, hi = problems[i]
+        s = C.c_double()
+        e = C.c_double()
+        errs[i] = fn(x, L, L, wi, hi, R, C.byref(cfg), steps_per_thread, C.byref(s), C.byref(e))
+        secs[i] = s.value
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    wall = time.perf_counter() - t0
+    if any(errs):
+        raise RuntimeError(f"reference CPU run failed: {errs}")
+    units = threads * steps_per_thread * (L * L) / (M * N)   # C5-equivalent outer iterations
+    span = max(secs)
+    return {"value": units / span, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": (f"{threads} thread(s) x {steps_per_thread} enmf::step on independent {L}x{L} r={R} "
+                       f"E-A-HALS hp3 sub-problems of C5 (1/{(M * N) // (L * L)} of its m·n); C5-equivalent it/s "
+                       f"= sample it/s x {L * L}/{M * N}"),
+            "seconds": span, "wall_seconds": wall}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    total_units = 0.0
+    total_sec = 0.0
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference_throughput(threads, 1, seed=100 + i)
+        if i >= args.warmup:
+            total_units += res["value"] * res["seconds"]
+            total_sec += res["seconds"]
+    value = total_units / total_sec
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_sec / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": res["kind"],
+                             "sample": res["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def gen_c5(device, seed):
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    w0 = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
+    h0 = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
+    x = torch.randn(M, N, device=device, dtype=torch.float64, generator=g)
+    x.abs_().mul_(0.01)
+    x.addmm_(w0, h0)
+    del w0, h0
+    wi = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
+    hi = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
+    return x, wi, hi
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1805_06604_b200 as E
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    x, wi, hi = gen_c5(dev, 1234 + rank)
+    torch.cuda.synchronize()
+    ctx = E.Context(local_rank)
+    ctx.load_device(x.data_ptr(), M, N)
+    prof_steps = 2
+    cfg = cfg_c5(args.warmup + args.steps + prof_steps)
+    ctx.begin_device(wi.data_ptr(), hi.data_ptr(), R, cfg)
+    ctx.step(args.warmup)
+    ctx.sync()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    e0.record(stream)
+    ctx.step(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    recs = ctx.sync()
+    launches = ctx.kernel_launches - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    timed = recs[args.warmup + 1: args.warmup + 1 + args.steps]
+    sweeps_h = [r.inner_h_count for r in timed]
+    sweeps_w = [r.inner_w_count for r in timed]
+    # dominant kernel: FP64 DMMA GEMM, timed per phase with CUDA events on the engine stream
+    phases = [ctx.step_profiled() for _ in range(prof_steps)]
+    ctx.sync()
+    ctx.end()
+    gemm_ms = statistics.mean([(p["cross_wx"] + p["cross_xht"]) / 2 for p in phases])
+    gemm_flops = 2.0 * R * M * N
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    iter_ms = ms / args.steps
+    flops_alg = 4.0 * M * N * R + 2.0 * (M + N) * R * R
+    t_roof_ms = flops_alg / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    value = world * args.steps / (ms * 1e-3)
+
+    # e2e: the drop-in C-ABI call (enmf_gpu_run_dense) on pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty((M, N), dtype=torch.float64, pin_memory=True)
+        xh.copy_(x)
+        wh = torch.empty((M, R), dtype=torch.float64, pin_memory=True)
+        hh = torch.empty((R, N), dtype=torch.float64, pin_memory=True)
+        wh.copy_(wi)
+        hh.copy_(hi)
+        del x
+        torch.cuda.empty_cache()
+        cfg2 = cfg_c5(args.steps)
+        ctx2 = E.Context(local_rank)
+        xn, wn, hn = xh.numpy(), wh.numpy(), hh.numpy()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        rec2 = ctx2.run(xn, wn, hn, cfg2, E.TimingMode.none)
+        t1 = time.perf_counter()
+        wall = t1 - t0
+        if world > 1:
+            t = torch.tensor([wall], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        e2e = {"value": world * args.steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": int((M * N + M * R + R * N) * 8),
+               "d2h_bytes_per_step": int((M * R + R * N) * 8 + (args.steps + 1) * 56),
+               "step": f"one enmf_gpu_run_dense call: X/W0/H0 host->device, {args.steps} outer iterations, "
+                       f"W/H/records device->host", "seconds": wall,
+               "final_relative_error": rec2.final_relative_error()}
+        ctx2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_throughput(min(host_threads(), args.cpu_threads), 1)
+        except Exception as ex:  # reported, never fatal for the GPU number
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": iter_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch generator on device)",
+                "config": config_block(args, world),
+                "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma (W_yᵀX / X·Tᵀ, 2·r·m·n flop per launch)",
+                             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SRC,
+                             "gemm_ms": gemm_ms,
+                             "iteration": {"flops_alg": flops_alg, "t_roof_ms": t_roof_ms,
+                                           "frac": t_roof_ms / iter_ms,
+                                           "note": "t_roof = (4mnr + 2(m+n)r²) / FP64 peak; HALS sweeps excluded"},
+                             "phases_ms": phases[-1]},
+                "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+                "sweeps": {"h_mean": statistics.mean(sweeps_h) if sweeps_h else None,
+                           "w_mean": statistics.mean(sweeps_w) if sweeps_w else None},
+                "final_relative_error": recs[-1].relative_error if recs else None}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=64)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rc = run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -51,7 +51,10 @@ enum { ENMF_INNER_EXACT = 0, ENMF_INNER_HALS = 1 };
 /* enmf::TimingMode (engine.hpp:58) */
 enum { ENMF_TIMING_WALL = 0, ENMF_TIMING_NONE = 1 };
 /* Arithmetic of the device path. FP64 is the parity path. */
-enum { ENMF_PRECISION_FP64 = 0 };
+enum {
+  ENMF_PRECISION_FP64 = 0,        /* DMMA tensor-core GEMMs, FMA sweeps: the product path */
+  ENMF_PRECISION_FP64_EXACT = 2   /* bitwise-faithful debug path: reference summation order, no FMA */
+};
 
 /* 1:1 with enmf::SolverConfig (engine.hpp:149-173).  `inner_max_sweeps` = 0
  * means "std::nullopt" (derive from the setup/sweep cost ratio). */
@@ -141,7 +144,29 @@ int enmf_gpu_solve(enmf_gpu_ctx* ctx, const double* w0, const double* h0, size_t
                    size_t iters_cap, size_t* n_iters, double* w_out, double* h_out,
                    double* norm_x);
 
-/* ---- public kernels the reference's tests call (host pointers) -------------- */
+/* ---- run session: enmf::run split into its phases (bench / step-wise drivers) --
+ * begin = run()'s prologue (validation, upload, ||X||^2, e(0), capture of one
+ * outer iteration as a CUDA graph); step = enqueue `count` more outer
+ * iterations (engine.hpp:309-440), asynchronous on the context stream; sync =
+ * wait and read records 0..k (returns the error code of a failed iteration);
+ * end = RunRecord::factors (engine.hpp:518-520) and close.  X must already be
+ * loaded (enmf_gpu_load_dense).  At most cfg->max_outer_iterations steps. */
+int enmf_gpu_begin(enmf_gpu_ctx* ctx, const double* w0, const double* h0, size_t r,
+                   int factors_on_device, const enmf_gpu_config* cfg);
+int enmf_gpu_step(enmf_gpu_ctx* ctx, uint64_t count);
+/* One outer iteration launched kernel by kernel with CUDA events between the
+ * phases; phase_ms[0..10] = {gram(W_y)+reinit, W_yᵀX, H update, H extrapolation,
+ * gram(T)+reinit, X·Tᵀ, W update, error products, decide+finalize,
+ * H sweeps, W sweeps}.  Advances the run like enmf_gpu_step(ctx, 1). */
+int enmf_gpu_step_profiled(enmf_gpu_ctx* ctx, double* phase_ms, size_t cap);
+int enmf_gpu_sync(enmf_gpu_ctx* ctx, enmf_gpu_iter* iters, size_t iters_cap, size_t* n_iters);
+int enmf_gpu_end(enmf_gpu_ctx* ctx, double* w_out, double* h_out, double* norm_x);
+/* The context's CUDA stream (cudaStream_t) — for event timing by the caller. */
+void* enmf_gpu_stream(enmf_gpu_ctx* ctx);
+
+/* ---- public kernels the reference's tests call (host pointers) --------------
+ * They run in the context's kernel precision (default ENMF_PRECISION_FP64). */
+int enmf_gpu_set_precision(enmf_gpu_ctx* ctx, int precision);
 /* gram (linalg.hpp:49-64): a m×r → g r×r, bitwise symmetric. */
 int enmf_gpu_gram(enmf_gpu_ctx* ctx, const double* a, size_t m, size_t r, double* g);
 /* cross_wx (linalg.hpp:67-83): w m×r, x m×n → out r×n. */

@@ -11,6 +11,7 @@
  * the reference: they realise the BASELINE.json config descriptions with a fixed
  * documented draw order on one mt19937_64 stream.
  */
+#define _POSIX_C_SOURCE 199309L
 #include "enmf_oracle.h"
 
 #include <float.h>
@@ -19,6 +20,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 static _Thread_local char g_err[512];
 static void set_err(const char* msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
@@ -701,6 +703,41 @@ static int run_impl(const xmat* X, const double* w0, const double* h0, size_t r,
     if (h_out) memcpy(h_out, st.h, sizeof(double) * hsz);
   }
   free(ws); free(st.w); free(st.w_y); free(st.w_n); free(st.h); free(st.h_y); free(st.h_n);
+  return rc;
+}
+
+/* run()'s prologue then `nsteps` step() calls; *seconds = time inside step()
+ * only (bench.py cpu_baseline when oracle/_ref is absent). */
+
+int orc_time_steps(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                   const enmf_gpu_config* cfg, size_t nsteps, double* seconds, double* last_rel_err) {
+  int rc = orc_config_validate(cfg);
+  if (rc) return rc;
+  xmat X = {0, x, NULL, NULL, NULL, m, n, m * n};
+  const double nx2 = orc_frob_norm_sq(x, m * n);
+  ext_state st;
+  const size_t wsz = m * r, hsz = r * n;
+  double* buf = (double*)malloc(sizeof(double) * (3 * wsz + 3 * hsz + 4 * r * r + r * n + 5 * m * r));
+  st.w = buf; st.w_y = st.w + wsz; st.w_n = st.w_y + wsz;
+  st.h = st.w_n + wsz; st.h_y = st.h + hsz; st.h_n = st.h_y + hsz;
+  double* ws = st.h_n + hsz;
+  memcpy(st.w, w0, sizeof(double) * wsz); memcpy(st.w_y, w0, sizeof(double) * wsz);
+  memcpy(st.h, h0, sizeof(double) * hsz); memcpy(st.h_y, h0, sizeof(double) * hsz);
+  st.schedule.beta = cfg->beta0; st.schedule.beta_bar = 1.0; st.schedule.beta_prev = cfg->beta0;
+  st.schedule.gamma = cfg->gamma; st.schedule.gamma_bar = cfg->gamma_bar; st.schedule.eta = cfg->eta;
+  st.restarted = 0;
+  orc_gram_rows(h0, r, n, ws);
+  x_cross_xht(&X, h0, r, ws + r * r);
+  st.err_prev = orc_fast_error(nx2, w0, ws + r * r, ws, m, r);
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  enmf_gpu_iter rec;
+  memset(&rec, 0, sizeof rec);
+  for (uint64_t k = 1; k <= nsteps && rc == ENMF_OK; ++k) rc = step(&X, nx2, &st, cfg, r, k, &rec, ws);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+  if (last_rel_err) *last_rel_err = rec.relative_error;
+  free(buf);
   return rc;
 }
 

@@ -77,6 +77,10 @@ int orc_run_csr(const uint64_t* off, const uint64_t* cidx, const double* vals, s
                 const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
                 size_t* n_iters, double* w_out, double* h_out, double* norm_x);
 
+/* run()'s prologue + nsteps step() calls; *seconds = time inside step() only. */
+int orc_time_steps(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                   const enmf_gpu_config* cfg, size_t nsteps, double* seconds, double* last_rel_err);
+
 /* BASELINE.json config generators (new; not in the reference) */
 int orc_gen_config(int which, size_t m, size_t n, size_t r, uint64_t seed, double* x);
 int orc_gen_docs(size_t m, size_t n, double zipf_s, uint64_t seed, uint64_t** off, uint64_t** cidx,

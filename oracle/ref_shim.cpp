@@ -116,6 +116,41 @@ int ref_run_csr(const uint64_t* off, const uint64_t* cidx, const double* vals, s
   });
 }
 
+// run()'s prologue (engine.hpp:468-503, state exactly as test_engine.cpp:40-55
+// make_state builds it for step-level tests) followed by `nsteps` calls of the
+// reference's own enmf::step (engine.hpp:309-440); *seconds = wall time spent
+// inside step() only.  Used by bench.py --impl reference to time the per-iteration
+// path without the one-off prologue.
+int ref_time_steps(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                   const enmf_gpu_config* cfg, size_t nsteps, double* seconds, double* last_rel_err) {
+  return guard([&] {
+    const auto X = dm(x, m, n);
+    const enmf::SolverConfig c = to_cfg(cfg);
+    c.validate();
+    const double nx2 = enmf::frob_norm_sq(X);
+    enmf::ExtrapolationState st;
+    st.w = dm(w0, m, r);
+    st.h = dm(h0, r, n);
+    st.w_y = st.w;
+    st.h_y = st.h;
+    st.schedule.beta = c.beta0;
+    st.schedule.beta_bar = 1.0;
+    st.schedule.beta_prev = c.beta0;
+    st.schedule.gamma = c.gamma;
+    st.schedule.gamma_bar = c.gamma_bar;
+    st.schedule.eta = c.eta;
+    enmf::GramCache init;
+    init.gram = enmf::gram(st.h.transposed());
+    init.cross = enmf::cross_xht(X, st.h);
+    st.err_prev = enmf::fast_error(nx2, st.w, init, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    enmf::IterationRecord rec;
+    for (size_t k = 1; k <= nsteps; ++k) rec = enmf::step(X, nx2, st, c, k);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (last_rel_err) *last_rel_err = rec.relative_error;
+  });
+}
+
 int ref_gram(const double* a, size_t m, size_t r, double* g) {
   return guard([&] { out(enmf::gram(dm(a, m, r)), g); });
 }

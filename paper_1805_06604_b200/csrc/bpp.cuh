@@ -1,0 +1,244 @@
+// bpp.cuh — batched exact NNLS by block principal pivoting (nnls.hpp:259-406).
+//
+// One warp per right-hand side (column).  The reference groups columns with
+// identical passive sets to share one Cholesky factor; every per-column
+// result (factor, pivot drops/bans, iterates, exchanges) is a function of the
+// passive set alone, so per-column solving reproduces it exactly (SURVEY §3.4,
+// verified column-by-column there).  Every reduction below keeps the
+// reference's sequential order with separately rounded multiply/subtract, so
+// given the same Gram and cross products a column's result is bitwise the
+// reference's:
+//   cholesky       nnls.hpp:215-229  (column j: pivot by lane 0, rows i>j lane-parallel,
+//                                     each with its own sequential p-loop)
+//   cholesky_solve nnls.hpp:232-243  (lane 0, sequential)
+//   refinement     nnls.hpp:349-359  (rows lane-parallel, sequential b-loop)
+//   feasibility    nnls.hpp:362-373  (lane-parallel, sequential a-loop)
+//   exchange rules nnls.hpp:384-400  (full flip / backup(3) / largest index)
+// Passive/banned/infeasible sets are 64-bit masks, so r <= 64.
+#pragma once
+
+#include "common.cuh"
+
+namespace bpp {
+
+constexpr int MAXR = 64;
+
+struct Args {
+  const double* G;        // r×r
+  const double* C;        // r×N, row stride ld
+  const double* H0;       // warm start r×N
+  double* H;              // solution r×N
+  long ld;
+  int r, N;
+  const double* cmax;     // max |C| (device scalar)
+  DevState* st;           // nullable
+  int side;
+  unsigned long long* exchanges;  // total exchanges (atomic)
+  int* rounds;                    // max solves per column (atomic max)
+  int* nonfinite;                 // set if a non-finite value is written
+};
+
+template <int RM, int WPB>
+constexpr int smem_bytes() {
+  // G (RM×RM) + per warp: L (RM×RM), cff row cache not needed, x/d/res (3×RM), fidx (RM ints)
+  return RM * RM * 8 + WPB * (RM * RM * 8 + 3 * RM * 8 + RM * 4);
+}
+
+ENMF_DEV unsigned long long warp_or64(unsigned long long v) {
+  const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)(v & 0xffffffffULL));
+  const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(v >> 32));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+template <int RM, int WPB>
+__global__ void __launch_bounds__(WPB * 32) solve(Args a) {
+  if (a.st && !dev_active(a.st)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int r = a.r;
+  double* Gs = sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* L = sm + RM * RM + warp * (RM * RM + 3 * RM);
+  double* xf = L + RM * RM;
+  double* df = xf + RM;
+  double* rs = df + RM;
+  int* fidx = reinterpret_cast<int*>(sm + RM * RM + WPB * (RM * RM + 3 * RM)) + warp * RM;
+
+  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[e] = a.G[e];
+  __syncthreads();
+
+  double maxd = 0.0;
+  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * r + i]) ? Gs[i * r + i] : maxd;
+  const double pivot_floor = __dmul_rn(1e-12, maxd);
+  const double feas_tol = __dmul_rn(1e-12, __dadd_rn(1.0, *a.cmax));
+  const unsigned long long limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
+
+  for (int col = blockIdx.x * WPB + warp; col < a.N; col += gridDim.x * WPB) {
+    unsigned long long P = 0, B = 0;
+    for (int i = lane; i < r; i += 32)
+      if (a.H0[(long)i * a.ld + col] > 0.0) P |= 1ULL << i;
+    P = warp_or64(P);
+    int best_inf = 0x7fffffff, backup = 3, solves = 0;
+    unsigned long long exch = 0;
+    int f = 0;
+    for (;;) {
+      ++solves;
+      // passive index list (ascending)
+      f = 0;
+      if (lane == 0)
+        for (int i = 0; i < r; ++i)
+          if ((P >> i) & 1ULL) fidx[f++] = i;
+      f = __shfl_sync(0xffffffffu, f, 0);
+      __syncwarp();
+      // factor G[F,F], dropping and banning variables whose pivot collapses
+      for (;;) {
+        if (f == 0) break;
+        int bad = f;
+        for (int j = 0; j < f; ++j) {
+          double ljj = 0.0;
+          int ok = 1;
+          if (lane == 0) {
+            double d = Gs[fidx[j] * r + fidx[j]];
+            for (int p = 0; p < j; ++p) d = __dsub_rn(d, __dmul_rn(L[j * RM + p], L[j * RM + p]));
+            ok = (d > pivot_floor) ? 1 : 0;
+            if (ok) {
+              ljj = __dsqrt_rn(d);
+              L[j * RM + j] = ljj;
+            }
+          }
+          ok = __shfl_sync(0xffffffffu, ok, 0);
+          if (!ok) { bad = j; break; }
+          ljj = __shfl_sync(0xffffffffu, ljj, 0);
+          __syncwarp();
+          for (int i = j + 1 + lane; i < f; i += 32) {
+            double s = Gs[fidx[i] * r + fidx[j]];
+            for (int p = 0; p < j; ++p) s = __dsub_rn(s, __dmul_rn(L[i * RM + p], L[j * RM + p]));
+            L[i * RM + j] = __ddiv_rn(s, ljj);
+          }
+          __syncwarp();
+        }
+        if (bad == f) break;
+        if (lane == 0) {
+          const int var = fidx[bad];
+          P &= ~(1ULL << var);
+          B |= 1ULL << var;
+          for (int q = bad; q + 1 < f; ++q) fidx[q] = fidx[q + 1];
+        }
+        P = __shfl_sync(0xffffffffu, P, 0);
+        B = __shfl_sync(0xffffffffu, B, 0);
+        --f;
+        __syncwarp();
+      }
+      // x_F = chol_solve(C[F,col]) + one refinement step
+      for (int q = lane; q < f; q += 32) df[q] = a.C[(long)fidx[q] * a.ld + col];
+      __syncwarp();
+      auto chol_solve = [&](double* b) {
+        if (lane == 0) {
+          for (int i = 0; i < f; ++i) {
+            double s = b[i];
+            for (int p = 0; p < i; ++p) s = __dsub_rn(s, __dmul_rn(L[i * RM + p], b[p]));
+            b[i] = __ddiv_rn(s, L[i * RM + i]);
+          }
+          for (int ii = f - 1; ii >= 0; --ii) {
+            double s = b[ii];
+            for (int p = ii + 1; p < f; ++p) s = __dsub_rn(s, __dmul_rn(L[p * RM + ii], b[p]));
+            b[ii] = __ddiv_rn(s, L[ii * RM + ii]);
+          }
+        }
+        __syncwarp();
+      };
+      if (f > 0) {
+        for (int q = lane; q < f; q += 32) xf[q] = df[q];
+        __syncwarp();
+        chol_solve(xf);
+        for (int q = lane; q < f; q += 32) {
+          double s = df[q];
+          for (int b2 = 0; b2 < f; ++b2) s = __dsub_rn(s, __dmul_rn(Gs[fidx[q] * r + fidx[b2]], xf[b2]));
+          rs[q] = s;
+        }
+        __syncwarp();
+        chol_solve(rs);
+        for (int q = lane; q < f; q += 32) xf[q] = __dadd_rn(xf[q], rs[q]);
+        __syncwarp();
+      }
+      // infeasible set
+      unsigned long long I = 0;
+      for (int q = lane; q < f; q += 32)
+        if (xf[q] < -feas_tol) I |= 1ULL << fidx[q];
+      for (int i = lane; i < r; i += 32) {
+        if (((P | B) >> i) & 1ULL) continue;
+        double y = -a.C[(long)i * a.ld + col];
+        for (int q = 0; q < f; ++q) y = __dadd_rn(y, __dmul_rn(Gs[i * r + fidx[q]], xf[q]));
+        if (y < -feas_tol) I |= 1ULL << i;
+      }
+      I = warp_or64(I);
+      if (I == 0) break;
+      if (++exch > limit) break;  // the total exceeds the global limit too
+      const int count = __popcll(I);
+      if (count < best_inf) {
+        best_inf = count;
+        backup = 3;
+        P ^= I;
+      } else if (backup > 0) {
+        --backup;
+        P ^= I;
+      } else {
+        P ^= 1ULL << (63 - __clzll(I));
+      }
+    }
+    // write the column: max(x, 0) on F, zero elsewhere
+    int nf = 0;
+    for (int i = lane; i < r; i += 32) a.H[(long)i * a.ld + col] = 0.0;
+    __syncwarp();
+    for (int q = lane; q < f; q += 32) {
+      const double v = xf[q] > 0.0 ? xf[q] : 0.0;
+      a.H[(long)fidx[q] * a.ld + col] = v;
+      nf |= !isfinite(v);
+    }
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) {
+      if (exch) atomicAdd(a.exchanges, exch);
+      atomicMax(a.rounds, solves);
+      if (nf) atomicOr(a.nonfinite, 1);
+    }
+    __syncwarp();
+  }
+}
+
+// Post-solve checks: exchange limit (NoConvergence, nnls.hpp:384-387) and the
+// NaN guard on the solution (engine.hpp:334-337 / 380-383).
+__global__ void check(DevState* st, int side, int r, int N, unsigned long long* exchanges, int* rounds,
+                      int* nonfinite) {
+  if (!st || !dev_active(st)) return;
+  st->bpp_rounds[side] = *rounds;
+  st->bpp_exchanges[side] = *exchanges;
+  if (*exchanges > 3ULL * (unsigned long long)r * (unsigned long long)N) {
+    st->error_code = ENMF_NO_CONVERGENCE;
+    st->active = 0;
+  } else if (*nonfinite) {
+    st->error_code = ENMF_NON_FINITE;
+    st->active = 0;
+  }
+  *exchanges = 0;
+  *rounds = 0;
+  *nonfinite = 0;
+}
+
+// max |C| over r×N (feas_tol, nnls.hpp:271).  Single block, order-independent.
+__global__ void absmax(const double* C, long ld, int r, int N, double* out, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  __shared__ double red[256];
+  double m = 0.0;
+  for (long e = threadIdx.x; e < (long)r * N; e += blockDim.x) {
+    const double v = fabs(C[(e / N) * ld + e % N]);
+    m = (m < v) ? v : m;
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+}  // namespace bpp

@@ -1,0 +1,872 @@
+// engine.cu — host driver and C-ABI of the B200 enmf hot path.
+//
+// Replays enmf::run / enmf::step (engine.hpp:309-521) with every decision
+// taken on the device (DevState), so one outer iteration is one CUDA graph:
+//
+//   iter_begin → gram(W_y)+reinit → W_yᵀX → [HALS sweeps: WHILE node | BPP]
+//   → (hp≥2) H extrapolation → gram(T)+reinit → T·Xᵀ → [HALS | BPP]
+//   → (literal hp1) fresh H_y products → gram(W_n), <W_n, X Tᵀ> → decide → finalize
+//
+// The host only launches the instantiated graph K times and reads the
+// records back at the end (no per-iteration or per-sweep synchronisation).
+// Device layouts: X row-major m×n as given; W kept
+// transposed (Wᵀ, r×m) so the W update sweeps contiguous rows and the X·Tᵀ
+// GEMM writes its result straight into the r×m layout the sweep consumes;
+// H r×n as given.  W is transposed only at entry and exit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "bpp.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "hals.cuh"
+#include "misc.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CU(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      throw Fail{ENMF_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+    }                                                                                \
+  } while (0)
+
+#define CUK() CU(cudaGetLastError())
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t cnt) {
+    if (cnt <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CU(cudaMalloc(&p, std::max<size_t>(cnt, 1) * sizeof(T)));
+    n = cnt;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+constexpr int kSMs = 148;  // B200; refreshed from the device at context creation
+
+}  // namespace
+
+struct enmf_gpu_ctx {
+  int device = 0;
+  int sms = kSMs;
+  cudaStream_t stream = nullptr, body_stream = nullptr;
+  unsigned long long launches = 0;
+  // data matrix
+  DBuf<double> x_own;
+  const double* x = nullptr;
+  size_t m = 0, n = 0;
+  // factors and products
+  DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch;
+  DBuf<double> partials, gain_part, terms, ddpart, dd;
+  DBuf<int> part_nf, flags;
+  DBuf<unsigned> counters;
+  DBuf<unsigned long long> bpp_exch;
+  DBuf<int> bpp_rounds, bpp_nf;
+  DBuf<double> cmax;
+  DBuf<DevState> st;
+  DBuf<enmf_gpu_iter> recs;
+  // instrumentation of the last solve
+  int static_kernels = 0, kernels_per_sweep = 0;
+  // open run session (enmf_gpu_begin .. enmf_gpu_end)
+  struct Session* sess = nullptr;
+  // standalone kernel API
+  int kernel_precision = ENMF_PRECISION_FP64;
+  DBuf<double> ka, kb, kc, kd, ke;
+  DBuf<HalsCtl> kctl;
+};
+
+namespace {
+
+void set_attrs_once() {
+  static bool done = false;
+  if (done) return;
+  auto big = [](const void* f, int bytes) {
+    CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  };
+  big((const void*)gemm::gemm_f64_dmma<false, 2, false>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<false, 2, true>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<false, 1, false>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<false, 1, true>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<true, 2, false>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<true, 2, true>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<true, 1, false>, gemm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma<true, 1, true>, gemm::SMEM_BYTES);
+  big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
+  big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
+  big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
+  big((const void*)hals::sweep_fast<32, 4>, hals::smem_bytes<32, 4>());
+  big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
+  big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
+  done = true;
+}
+
+inline unsigned grid_for(long count, int nt = 256, int maxb = 148 * 8) {
+  long b = (count + nt - 1) / nt;
+  return (unsigned)std::max<long>(1, std::min<long>(b, maxb));
+}
+
+// ---- precision modes ---------------------------------------------------------
+enum { PREC_FAST = ENMF_PRECISION_FP64, PREC_EXACT = 2 };
+
+// ---- contractions --------------------------------------------------------------
+int choose_splits(int tiles, int kblocks, int sms) {
+  if (tiles >= 2 * sms) return 1;
+  const int smax = std::max(1, std::min(kblocks / 4, 512));
+  int best = 1;
+  double best_score = -1.0;
+  for (int s = 1; s <= smax; ++s) {
+    const long ctas = (long)tiles * s;
+    const long waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    const double score = eff - 0.0005 * s;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = s;
+    }
+  }
+  return best;
+}
+
+// C[M×N] = A[M×K] · op(B);  bk: B is N×K (K contiguous) else K×N (N contiguous).
+void gemm_launch(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long lda, const double* B, long ldb,
+                 double* C, long ldc, int M, int N, int K, bool sym, const DevState* st) {
+  using namespace gemm;
+  const int tn = (N + BN - 1) / BN, tm = (M + BM - 1) / BM, tiles = tn * tm;
+  const int kb = (K + BK - 1) / BK;
+  const int S = choose_splits(tiles, kb, c->sms);
+  const bool last = S > 1 && S <= 8;
+  if (S > 1) {
+    c->partials.ensure((size_t)S * M * N);
+    if (last && c->counters.n < (size_t)tiles) {
+      c->counters.ensure(tiles);
+      CU(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned) * tiles, s));
+    }
+  }
+  const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, S > 1 ? c->partials.p : nullptr, c->counters.p, sym ? 1 : 0, st};
+  dim3 grid(tn, tm, S);
+#define GEMM_GO(BKM, V, L) gemm_f64_dmma<BKM, V, L><<<grid, NT, SMEM_BYTES, s>>>(p)
+  if (bk) {
+    if (vec2) { if (last) GEMM_GO(true, 2, true); else GEMM_GO(true, 2, false); }
+    else { if (last) GEMM_GO(true, 1, true); else GEMM_GO(true, 1, false); }
+  } else {
+    if (vec2) { if (last) GEMM_GO(false, 2, true); else GEMM_GO(false, 2, false); }
+    else { if (last) GEMM_GO(false, 1, true); else GEMM_GO(false, 1, false); }
+  }
+#undef GEMM_GO
+  CUK();
+  c->launches++;
+  if (S > 1 && !last) {
+    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(c->partials.p, S, M, N, C, ldc, sym ? 1 : 0, st);
+    CUK();
+    c->launches++;
+  }
+}
+
+// gram of the factor whose columns are the rows of A (r×K, K contiguous) → G (r×r, symmetric).
+void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, long lda, int r, int K, double* G,
+                 const DevState* st) {
+  if (prec == PREC_EXACT) {
+    gemm::gram_exact<<<(r * r + 127) / 128, 128, 0, s>>>(A, lda, r, K, G, st);
+    CUK();
+    c->launches++;
+  } else {
+    gemm_launch(c, s, true, A, lda, A, lda, G, r, r, r, K, true, st);
+  }
+}
+
+// ---- inner solvers ------------------------------------------------------------
+void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
+  const int r = a.r;
+  if (prec == PREC_EXACT || r > 128) {
+    hals::sweep_exact<<<(a.N + hals::NT - 1) / hals::NT, hals::NT, 0, s>>>(a);
+    CUK();
+    hals::gain_exact<<<1, hals::NT, 0, s>>>(a);
+    CUK();
+    c->launches += 2;
+    return;
+  }
+#define SW(S_, T_)                                                                          \
+  hals::sweep_fast<S_, T_><<<(a.N + hals::NT / T_ - 1) / (hals::NT / T_), hals::NT,          \
+                             hals::smem_bytes<S_, T_>(), s>>>(a)
+  if (r <= 16) SW(16, 1);
+  else if (r <= 32) SW(32, 1);
+  else if (r <= 64) SW(32, 2);
+  else SW(32, 4);
+#undef SW
+  CUK();
+  c->launches++;
+}
+
+int hals_grid(int r, int N, int prec) {
+  if (prec == PREC_EXACT || r > 128) return (N + hals::NT - 1) / hals::NT;
+  const int tpc = r <= 32 ? 1 : (r <= 64 ? 2 : 4);
+  return (N + hals::NT / tpc - 1) / (hals::NT / tpc);
+}
+
+void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a) {
+  const int r = a.r;
+  bpp::absmax<<<1, 256, 0, s>>>(a.C, a.ld, r, a.N, const_cast<double*>(a.cmax), a.st);
+  CUK();
+  if (r <= 32) {
+    bpp::solve<32, 8><<<(a.N + 7) / 8, 256, bpp::smem_bytes<32, 8>(), s>>>(a);
+  } else {
+    bpp::solve<64, 4><<<(a.N + 3) / 4, 128, bpp::smem_bytes<64, 4>(), s>>>(a);
+  }
+  CUK();
+  bpp::check<<<1, 1, 0, s>>>(a.st, a.side, r, a.N, a.exchanges, a.rounds, a.nonfinite);
+  CUK();
+  c->launches += 3;
+}
+
+// Captures `body(stream)` as the body of a conditional WHILE node appended to
+// the graph being captured on `s`.
+
+// driver.inc — run/step control flow (included by engine.cu).
+//
+// Session = one enmf::run (engine.hpp:447-521):
+//   begin : validation (engine.hpp:450-459), upload, ||X||^2, e(0) (:487-503),
+//           capture of ONE outer iteration (engine.hpp:309-440) as a CUDA graph
+//   step  : launch the graph `count` times (asynchronous, no host round trip)
+//   sync  : wait, read the IterationRecords, map device error codes
+//   end   : return the accepted factors (RunRecord::factors, :518-520)
+
+// Captures `body(stream)` as the body of a conditional WHILE node appended to
+// the graph being captured on `s`.
+template <class F>
+void capture_while(enmf_gpu_ctx* c, cudaStream_t s, cudaGraphConditionalHandle h, F&& body) {
+  cudaStreamCaptureStatus status;
+  cudaGraph_t graph;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CU(cudaStreamGetCaptureInfo(s, &status, nullptr, &graph, &deps, &ndeps));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CU(cudaGraphAddNode(&node, graph, deps, ndeps, &np));
+  CU(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+  CU(cudaStreamBeginCaptureToGraph(c->body_stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  body(c->body_stream);
+  cudaGraph_t out;
+  CU(cudaStreamEndCapture(c->body_stream, &out));
+}
+
+struct Plan {
+  int m, n, r;
+  int prec;
+  int inner_h, inner_w, hp, extrap, literal;
+  int max_sweeps_h, max_sweeps_w;
+  double stall;
+  uint64_t reinit_seed;
+};
+
+void validate_cfg(const enmf_gpu_config* c) {
+  // SolverConfig::validate (engine.hpp:175-199) with BetaSchedule::validate (:71-81)
+  auto bad = [](const char* m) { throw Fail{ENMF_INVALID_ARGUMENT, m}; };
+  if (c->hp != 1 && c->hp != 2 && c->hp != 3) bad("SolverConfig: hp must be 1, 2 or 3");
+  if (!(c->beta0 >= 0.0) || !(c->beta0 < 1.0)) bad("SolverConfig: beta0 must lie in [0, 1)");
+  if (c->extrapolation_enabled && c->beta0 > 0.0) {
+    if (!(1.0 < c->gamma_bar) || !(c->gamma_bar < c->gamma) || !(c->gamma < c->eta))
+      bad("BetaSchedule: need 1 < gamma_bar < gamma < eta");
+  }
+  if (!(c->max_seconds > 0.0)) bad("SolverConfig: max_seconds must be > 0");
+  if (!(c->inner_sweep_ratio > 0.0)) bad("SolverConfig: inner_sweep_ratio must be > 0");
+  if (!(c->inner_stall_fraction > 0.0) || c->inner_stall_fraction >= 1.0)
+    bad("SolverConfig: inner_stall_fraction must lie in (0, 1)");
+  if ((c->inner_h != ENMF_INNER_EXACT && c->inner_h != ENMF_INNER_HALS) ||
+      (c->inner_w != ENMF_INNER_EXACT && c->inner_w != ENMF_INNER_HALS))
+    bad("SolverConfig: inner solver must be exact or hals");
+  if (c->timing != ENMF_TIMING_WALL && c->timing != ENMF_TIMING_NONE) bad("SolverConfig: bad timing mode");
+  if (c->precision != PREC_FAST && c->precision != PREC_EXACT) bad("SolverConfig: unsupported precision");
+}
+
+// InnerLoopPolicy::derive (nnls.hpp:79-87) via detail::inner_policy (engine.hpp:250-263)
+int derive_sweeps(const enmf_gpu_config* cfg, double setup_flops, size_t rhs, size_t r) {
+  if (cfg->inner_max_sweeps) return (int)std::min<uint64_t>(cfg->inner_max_sweeps, 1u << 30);
+  const double sweep = (double)rhs * (double)r * (double)r;
+  const double rho = sweep > 0.0 ? setup_flops / sweep : 0.0;
+  const double v = std::floor(cfg->inner_sweep_ratio * rho);
+  return (int)std::min<double>(1.0 + v, (double)(1 << 30));
+}
+
+void ensure_buffers(enmf_gpu_ctx* c, size_t m, size_t n, size_t r) {
+  const size_t wsz = m * r, hsz = r * n;
+  c->WT.ensure(wsz); c->WyT.ensure(wsz); c->WnT.ensure(wsz);
+  c->H.ensure(hsz); c->Hy.ensure(hsz); c->Hn.ensure(hsz);
+  c->CH.ensure(hsz); c->P.ensure(wsz); c->Plit.ensure(wsz);
+  c->GH.ensure(r * r); c->GW.ensure(r * r); c->GWn.ensure(r * r); c->Glit.ensure(r * r);
+  c->scratch.ensure(std::max(wsz, hsz));
+  const size_t gp = (size_t)std::max(m, n) + 1024;
+  c->gain_part.ensure(gp * 2);
+  c->part_nf.ensure(gp * 2);
+  c->ddpart.ensure(2 * 4096);
+  c->dd.ensure(8);
+  c->bpp_exch.ensure(2); c->bpp_rounds.ensure(2); c->bpp_nf.ensure(2); c->cmax.ensure(2);
+  c->st.ensure(1);
+  c->flags.ensure(4);
+}
+
+// Products for the error of (W from rows of WTsrc, T): dot = <W, X Tᵀ>, GWn = gram(W).
+void enqueue_error_terms(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, const double* WTsrc, const double* Pm,
+                         DevState* st) {
+  const long wsz = (long)pl.m * pl.r;
+  gram_launch(c, s, pl.prec, WTsrc, pl.m, pl.r, pl.m, c->GWn.p, st);
+  if (pl.prec == PREC_EXACT) {
+    misc::neumaier_exact<<<1, 32, 0, s>>>(WTsrc, Pm, wsz, 1, pl.r, pl.m, c->dd.p, st);
+    CUK();
+    c->launches++;
+  } else {
+    const int nb = (int)std::min<long>(4096, std::max<long>(1, (wsz + 2047) / 2048));
+    misc::dd_partial<<<nb, misc::NT, 0, s>>>(WTsrc, Pm, wsz, c->ddpart.p, c->ddpart.p + 4096, st);
+    CUK();
+    misc::dd_final<<<1, misc::NT, 0, s>>>(c->ddpart.p, c->ddpart.p + 4096, nb, c->dd.p, st);
+    CUK();
+    c->launches += 2;
+  }
+}
+
+// How the data-dependent sweep loop is driven.
+enum InnerMode { INNER_CAPTURE = 0, INNER_HOSTLOOP = 1 };
+
+struct Prof {
+  cudaEvent_t ev[12];
+  double hals_ms[2];
+  int hals_sweeps[2];
+};
+
+void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
+  (void)c;
+  if (p) CU(cudaEventRecord(p->ev[phase], s));
+}
+
+void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, int solver, const double* G,
+                   const double* Cm, const double* Hin, double* Hout, int rows_n, int max_sweeps, DevState* st,
+                   cudaGraphConditionalHandle cond, int mode, Prof* prof) {
+  if (solver == ENMF_INNER_HALS) {
+    hals::Args a{};
+    a.G = G; a.C = Cm; a.Hin = Hin; a.H = Hout; a.ld = rows_n; a.r = pl.r; a.N = rows_n;
+    a.max_sweeps = max_sweeps; a.stall = pl.stall;
+    a.ctl = &st->hals[side];
+    a.part = c->gain_part.p + side * (c->gain_part.n / 2);
+    a.part_nf = c->part_nf.p + side * (c->part_nf.n / 2);
+    a.terms = c->terms.p; a.st = st; a.side = side;
+    a.cond = (unsigned long long)cond; a.use_cond = mode == INNER_CAPTURE ? 1 : 0;
+    hals::reset_ctl<<<1, 1, 0, s>>>(a.ctl, st);
+    CUK();
+    c->launches++;
+    if (mode == INNER_CAPTURE) {
+      capture_while(c, s, cond, [&](cudaStream_t bs) { hals_body(c, bs, a, pl.prec); });
+    } else {
+      // host-driven: one sweep per launch, flag read back after each (profiling / no-graph path)
+      cudaEvent_t e0, e1;
+      CU(cudaEventCreate(&e0));
+      CU(cudaEventCreate(&e1));
+      double ms = 0.0;
+      int sweeps = 0;
+      for (int i = 0; i < max_sweeps; ++i) {
+        CU(cudaEventRecord(e0, s));
+        hals_body(c, s, a, pl.prec);
+        CU(cudaEventRecord(e1, s));
+        HalsCtl hc;
+        CU(cudaMemcpyAsync(&hc, a.ctl, sizeof hc, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, e0, e1));
+        ms += t;
+        sweeps = hc.sweeps;
+        if (!hc.cont) break;
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (prof) {
+        prof->hals_ms[side] = ms;
+        prof->hals_sweeps[side] = sweeps;
+      }
+    }
+  } else {
+    bpp::Args a{};
+    a.G = G; a.C = Cm; a.H0 = Hin; a.H = Hout; a.ld = rows_n; a.r = pl.r; a.N = rows_n;
+    a.cmax = c->cmax.p + side; a.st = st; a.side = side;
+    a.exchanges = c->bpp_exch.p + side; a.rounds = c->bpp_rounds.p + side; a.nonfinite = c->bpp_nf.p + side;
+    bpp_launch(c, s, a);
+  }
+}
+
+// One outer iteration, step() of engine.hpp:309-440.
+void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGraphConditionalHandle ch,
+                       cudaGraphConditionalHandle cw, int mode, Prof* prof) {
+  DevState* st = c->st.p;
+  const int m = pl.m, n = pl.n, r = pl.r;
+  const long wsz = (long)m * r, hsz = (long)r * n;
+  mark(c, s, prof, 0);
+  misc::iter_begin<<<1, 1, 0, s>>>(st);
+  CUK();
+  c->launches++;
+
+  // ---- H update (engine.hpp:323-337) ----
+  gram_launch(c, s, pl.prec, c->WyT.p, m, r, m, c->GH.p, st);
+  misc::reinit_fixup<<<1, misc::NT, 0, s>>>(c->WyT.p, m, r, m, c->GH.p, pl.reinit_seed, 0, st);
+  CUK();
+  c->launches++;
+  mark(c, s, prof, 1);
+  if (pl.prec == PREC_EXACT) {
+    gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
+    CUK();
+    c->launches++;
+  } else {
+    gemm_launch(c, s, false, c->WyT.p, m, c->x, n, c->CH.p, n, r, n, m, false, st);
+  }
+  mark(c, s, prof, 2);
+  enqueue_inner(c, s, pl, 0, pl.inner_h, c->GH.p, c->CH.p, c->Hy.p, c->Hn.p, n, pl.max_sweeps_h, st, ch, mode, prof);
+  mark(c, s, prof, 3);
+
+  // ---- early H extrapolation (engine.hpp:340-347) ----
+  if (pl.hp >= 2) {
+    if (pl.extrap) misc::extrap<<<grid_for(hsz), 256, 0, s>>>(c->Hn.p, c->H.p, c->Hy.p, hsz, pl.hp == 3, st);
+    else misc::copy<<<grid_for(hsz), 256, 0, s>>>(c->Hn.p, c->Hy.p, hsz, st);
+    CUK();
+    c->launches++;
+  }
+  const bool target_hy = pl.hp >= 2 || (pl.literal && pl.extrap);
+  double* T = target_hy ? c->Hy.p : c->Hn.p;
+  mark(c, s, prof, 4);
+
+  // ---- W update (engine.hpp:353-383) ----
+  gram_launch(c, s, pl.prec, T, n, r, n, c->GW.p, st);
+  misc::reinit_fixup<<<1, misc::NT, 0, s>>>(T, n, r, n, c->GW.p, pl.reinit_seed, 1, st);
+  CUK();
+  c->launches++;
+  mark(c, s, prof, 5);
+  auto cross_xht = [&](const double* Tm, double* out) {
+    if (pl.prec == PREC_EXACT) {
+      gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
+      CUK();
+      c->launches++;
+    } else {
+      gemm_launch(c, s, true, Tm, n, c->x, n, out, m, r, m, n, false, st);
+    }
+  };
+  cross_xht(T, c->P.p);
+  mark(c, s, prof, 6);
+  enqueue_inner(c, s, pl, 1, pl.inner_w, c->GW.p, c->P.p, c->WyT.p, c->WnT.p, m, pl.max_sweeps_w, st, cw, mode, prof);
+  mark(c, s, prof, 7);
+
+  // ---- error (engine.hpp:402-416) ----
+  const double* Pe = c->P.p;
+  const double* Ge = c->GW.p;
+  int mode_h = pl.hp >= 2 ? 0 : 1;
+  if (pl.hp == 1 && pl.literal && pl.extrap) {
+    misc::extrap<<<grid_for(hsz), 256, 0, s>>>(c->Hn.p, c->H.p, c->Hy.p, hsz, 0, st);
+    CUK();
+    c->launches++;
+    gram_launch(c, s, pl.prec, c->Hy.p, n, r, n, c->Glit.p, st);
+    cross_xht(c->Hy.p, c->Plit.p);
+    Pe = c->Plit.p;
+    Ge = c->Glit.p;
+    mode_h = 2;
+  }
+  enqueue_error_terms(c, s, pl, c->WnT.p, Pe, st);
+  mark(c, s, prof, 8);
+  misc::decide<<<1, misc::NT, 0, s>>>(st, c->dd.p, c->GWn.p, Ge, r, pl.prec == PREC_EXACT, c->recs.p, 0);
+  CUK();
+  misc::finalize<<<grid_for(std::max(wsz, hsz)), 256, 0, s>>>(c->WT.p, c->WyT.p, c->WnT.p, wsz, c->H.p, c->Hy.p,
+                                                              c->Hn.p, hsz, mode_h, st);
+  CUK();
+  c->launches += 2;
+  mark(c, s, prof, 9);
+}
+
+void set_err(const Fail& f) { g_last_error = f.msg; }
+
+}  // namespace
+
+struct Session {
+  Plan pl{};
+  bool dev_factors = false;
+  size_t m = 0, n = 0, r = 0;
+  size_t K = 0;             // max_outer_iterations
+  size_t launched = 0;      // iterations enqueued so far
+  size_t counted = 0;       // iterations whose kernels were added to c->launches
+  int static_kernels = 0;   // per-iteration kernels outside the sweep loops
+  int kps = 1;              // kernels per HALS sweep
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool failed = false;
+};
+
+namespace {
+
+void close_session(enmf_gpu_ctx* c) {
+  if (!c->sess) return;
+  if (c->sess->exec) cudaGraphExecDestroy(c->sess->exec);
+  if (c->sess->graph) cudaGraphDestroy(c->sess->graph);
+  delete c->sess;
+  c->sess = nullptr;
+}
+
+void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, bool dev_factors,
+                const enmf_gpu_config* cfg) {
+  if (!c) throw Fail{ENMF_INVALID_ARGUMENT, "null context"};
+  if (!cfg) throw Fail{ENMF_INVALID_ARGUMENT, "null config"};
+  CU(cudaSetDevice(c->device));
+  close_session(c);
+  validate_cfg(cfg);
+  if (!c->x) throw Fail{ENMF_INVALID_ARGUMENT, "run: no data matrix loaded"};
+  const size_t m = c->m, n = c->n;
+  if (r == 0) throw Fail{ENMF_INVALID_ARGUMENT, "DenseMatrix: rows and cols must be >= 1"};
+  if (!w0 || !h0) throw Fail{ENMF_INVALID_ARGUMENT, "run: null initial factor"};
+  if (m > (size_t)INT32_MAX || n > (size_t)INT32_MAX || r > 4096)
+    throw Fail{ENMF_INVALID_ARGUMENT, "run: shape exceeds the device path's limits (m,n < 2^31, r <= 4096)"};
+  if ((cfg->inner_h == ENMF_INNER_EXACT || cfg->inner_w == ENMF_INNER_EXACT) && r > 64)
+    throw Fail{ENMF_INVALID_ARGUMENT, "active_set_solve on device supports r <= 64"};
+  if ((cfg->inner_h == ENMF_INNER_HALS || cfg->inner_w == ENMF_INNER_HALS) && r > 1024)
+    throw Fail{ENMF_INVALID_ARGUMENT, "hals_solve on device supports r <= 1024"};
+  if (cfg->max_outer_iterations > (1ULL << 24))
+    throw Fail{ENMF_INVALID_ARGUMENT, "max_outer_iterations exceeds the record buffer limit (2^24)"};
+  const size_t wsz = m * r, hsz = r * n;
+  cudaStream_t s = c->stream;
+  (void)cudaGetLastError();  // drop a stale (non-sticky) error from an earlier failed call
+  set_attrs_once();
+  ensure_buffers(c, m, n, r);
+  if (cfg->precision == PREC_EXACT || r > 128) c->terms.ensure(std::max(wsz, hsz));
+  const size_t K = cfg->max_outer_iterations;
+  c->recs.ensure(K + 1);
+
+  // validate + upload factors (engine.hpp:451-459)
+  if (!dev_factors) {
+    for (size_t i = 0; i < wsz; ++i)
+      if (!std::isfinite(w0[i]) || !(w0[i] >= 0.0))
+        throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
+    for (size_t i = 0; i < hsz; ++i)
+      if (!std::isfinite(h0[i]) || !(h0[i] >= 0.0))
+        throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
+    CU(cudaMemcpyAsync(c->scratch.p, w0, wsz * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(c->H.p, h0, hsz * 8, cudaMemcpyHostToDevice, s));
+  } else {
+    CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), s));
+    misc::check_factor<<<grid_for(wsz), 256, 0, s>>>(w0, wsz, c->flags.p, 1);
+    misc::check_factor<<<grid_for(hsz), 256, 0, s>>>(h0, hsz, c->flags.p, 1);
+    CUK();
+    int bad = 0;
+    CU(cudaMemcpyAsync(&bad, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (bad) throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
+    CU(cudaMemcpyAsync(c->scratch.p, w0, wsz * 8, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(c->H.p, h0, hsz * 8, cudaMemcpyDeviceToDevice, s));
+    c->launches += 2;
+  }
+  {
+    dim3 tb(32, 8), tg((unsigned)((r + 31) / 32), (unsigned)((m + 31) / 32));
+    misc::transpose<<<tg, tb, 0, s>>>(c->scratch.p, c->WT.p, (int)m, (int)r);
+    CUK();
+    c->launches++;
+  }
+  CU(cudaMemcpyAsync(c->WyT.p, c->WT.p, wsz * 8, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(c->Hy.p, c->H.p, hsz * 8, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemsetAsync(c->bpp_exch.p, 0, 2 * sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(c->bpp_rounds.p, 0, 2 * sizeof(int), s));
+  CU(cudaMemsetAsync(c->bpp_nf.p, 0, 2 * sizeof(int), s));
+
+  // run state (engine.hpp:471-481)
+  DevState hs;
+  std::memset(&hs, 0, sizeof hs);
+  hs.beta = cfg->beta0;
+  hs.beta_bar = 1.0;
+  hs.beta_prev = cfg->beta0;
+  hs.gamma = cfg->gamma;
+  hs.gamma_bar = cfg->gamma_bar;
+  hs.eta = cfg->eta;
+  hs.max_seconds = cfg->max_seconds;
+  hs.max_iter = K;
+  hs.active = 1;
+  hs.extrapolation = cfg->extrapolation_enabled ? 1 : 0;
+  hs.hp = cfg->hp;
+  hs.wall = (cfg->timing == ENMF_TIMING_WALL || std::isfinite(cfg->max_seconds)) ? 1 : 0;
+  hs.literal = cfg->literal_hp1_order ? 1 : 0;
+  CU(cudaMemcpyAsync(c->st.p, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
+  DevState* st = c->st.p;
+  misc::run_begin<<<1, 1, 0, s>>>(st);
+  CUK();
+  c->launches++;
+
+  auto* se = new Session();
+  c->sess = se;
+  Plan& pl = se->pl;
+  pl.m = (int)m; pl.n = (int)n; pl.r = (int)r;
+  pl.prec = cfg->precision;
+  pl.inner_h = cfg->inner_h; pl.inner_w = cfg->inner_w; pl.hp = cfg->hp;
+  pl.extrap = cfg->extrapolation_enabled ? 1 : 0;
+  pl.literal = cfg->literal_hp1_order ? 1 : 0;
+  const double setup = (double)m * (double)n * (double)r;  // setup_flop_estimate (engine.hpp:242-244)
+  pl.max_sweeps_h = derive_sweeps(cfg, setup, n, r);
+  pl.max_sweeps_w = derive_sweeps(cfg, setup, m, r);
+  pl.stall = cfg->inner_stall_fraction;
+  pl.reinit_seed = cfg->reinit_seed;
+  se->dev_factors = dev_factors;
+  se->m = m; se->n = n; se->r = r; se->K = K;
+  se->kps = (pl.prec == PREC_EXACT || r > 128) ? 2 : 1;
+
+  // ||X||^2 (linalg.hpp:160-171) and e(0) (engine.hpp:487-503)
+  const long xs = (long)m * n;
+  if (pl.prec == PREC_EXACT) {
+    misc::neumaier_exact<<<1, 32, 0, s>>>(c->x, nullptr, xs, 0, 0, 0, c->dd.p + 2, nullptr);
+    c->launches++;
+  } else {
+    const int nb = (int)std::min<long>(4096, std::max<long>(1, (xs + 4095) / 4096));
+    misc::dd_partial<<<nb, misc::NT, 0, s>>>(c->x, nullptr, xs, c->ddpart.p, c->ddpart.p + 4096, nullptr);
+    misc::dd_final<<<1, misc::NT, 0, s>>>(c->ddpart.p, c->ddpart.p + 4096, nb, c->dd.p + 2, nullptr);
+    c->launches += 2;
+  }
+  CUK();
+  misc::set_norm<<<1, 1, 0, s>>>(st, c->dd.p + 2);
+  CUK();
+  gram_launch(c, s, pl.prec, c->H.p, n, (int)r, (int)n, c->GW.p, st);
+  if (pl.prec == PREC_EXACT) {
+    gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
+                                                                             c->P.p, st);
+    CUK();
+    c->launches++;
+  } else {
+    gemm_launch(c, s, true, c->H.p, n, c->x, n, c->P.p, m, (int)r, (int)m, (int)n, false, st);
+  }
+  enqueue_error_terms(c, s, pl, c->WT.p, c->P.p, st);
+  misc::decide<<<1, misc::NT, 0, s>>>(st, c->dd.p, c->GWn.p, c->GW.p, (int)r, pl.prec == PREC_EXACT, c->recs.p, 1);
+  CUK();
+  c->launches += 2;
+
+  // one outer iteration = one graph; one conditional WHILE node per HALS side
+  if (K > 0) {
+    CU(cudaGraphCreate(&se->graph, 0));
+    cudaGraphConditionalHandle ch = 0, cw = 0;
+    if (pl.inner_h == ENMF_INNER_HALS)
+      CU(cudaGraphConditionalHandleCreate(&ch, se->graph, 1, cudaGraphCondAssignDefault));
+    if (pl.inner_w == ENMF_INNER_HALS)
+      CU(cudaGraphConditionalHandleCreate(&cw, se->graph, 1, cudaGraphCondAssignDefault));
+    const unsigned long long before = c->launches;
+    CU(cudaStreamBeginCaptureToGraph(s, se->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue_iteration(c, s, pl, ch, cw, INNER_CAPTURE, nullptr);
+    } catch (...) {
+      cudaGraph_t g2;
+      cudaStreamEndCapture(s, &g2);
+      close_session(c);
+      throw;
+    }
+    cudaGraph_t g2;
+    CU(cudaStreamEndCapture(s, &g2));
+    const int hals_sides = (pl.inner_h == ENMF_INNER_HALS) + (pl.inner_w == ENMF_INNER_HALS);
+    se->static_kernels = (int)(c->launches - before) - hals_sides * se->kps;
+    c->launches = before;
+    CU(cudaGraphInstantiate(&se->exec, se->graph, 0));
+  }
+}
+
+Session* need_session(enmf_gpu_ctx* c) {
+  if (!c) throw Fail{ENMF_INVALID_ARGUMENT, "null context"};
+  if (!c->sess) throw Fail{ENMF_INVALID_ARGUMENT, "no open run (call enmf_gpu_begin first)"};
+  CU(cudaSetDevice(c->device));
+  return c->sess;
+}
+
+size_t step_impl(enmf_gpu_ctx* c, uint64_t count) {
+  Session* se = need_session(c);
+  const size_t todo = (size_t)std::min<uint64_t>(count, se->K - se->launched);
+  for (size_t k = 0; k < todo; ++k) CU(cudaGraphLaunch(se->exec, c->stream));
+  se->launched += todo;
+  return todo;
+}
+
+// One iteration with direct launches and CUDA events between phases.
+void step_profiled_impl(enmf_gpu_ctx* c, double* phase_ms, size_t cap) {
+  Session* se = need_session(c);
+  if (se->launched >= se->K) throw Fail{ENMF_INVALID_ARGUMENT, "step_profiled: iteration budget exhausted"};
+  Prof p{};
+  for (auto& e : p.ev) CU(cudaEventCreate(&e));
+  const unsigned long long before = c->launches;
+  enqueue_iteration(c, c->stream, se->pl, 0, 0, INNER_HOSTLOOP, &p);
+  c->launches = before;  // counted from the records at sync time
+  CU(cudaStreamSynchronize(c->stream));
+  se->launched += 1;
+  double out[12] = {0};
+  auto el = [&](int a, int b) {
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, p.ev[a], p.ev[b]));
+    return (double)t;
+  };
+  out[0] = el(0, 1);   // iter_begin + gram(W_y) + reinit check
+  out[1] = el(1, 2);   // W_yᵀ X
+  out[2] = p.hals_ms[0] > 0 ? p.hals_ms[0] : el(2, 3);  // H update (sweeps only / BPP)
+  out[3] = el(3, 4);   // H extrapolation
+  out[4] = el(4, 5);   // gram(T) + reinit check
+  out[5] = el(5, 6);   // T Xᵀ
+  out[6] = p.hals_ms[1] > 0 ? p.hals_ms[1] : el(6, 7);  // W update
+  out[7] = el(7, 8);   // error products
+  out[8] = el(8, 9);   // decide + finalize
+  out[9] = p.hals_sweeps[0];
+  out[10] = p.hals_sweeps[1];
+  for (auto& e : p.ev) cudaEventDestroy(e);
+  for (size_t i = 0; i < cap && i < 11; ++i) phase_ms[i] = out[i];
+}
+
+size_t sync_impl(enmf_gpu_ctx* c, enmf_gpu_iter* iters, size_t cap, size_t* n_iters) {
+  Session* se = need_session(c);
+  DevState out;
+  CU(cudaMemcpyAsync(&out, c->st.p, sizeof out, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const size_t done = (size_t)out.k;
+  std::vector<enmf_gpu_iter> recs(done + 1);
+  CU(cudaMemcpy(recs.data(), c->recs.p, (done + 1) * sizeof(enmf_gpu_iter), cudaMemcpyDeviceToHost));
+  // kernels actually executed: static part per iteration + the sweeps taken
+  for (size_t k = se->counted + 1; k <= done; ++k) {
+    unsigned long long sw = 0;
+    if (se->pl.inner_h == ENMF_INNER_HALS) sw += recs[k].inner_h_count;
+    if (se->pl.inner_w == ENMF_INNER_HALS) sw += recs[k].inner_w_count;
+    c->launches += (unsigned long long)se->static_kernels + sw * se->kps;
+  }
+  se->counted = std::max(se->counted, done);
+  const size_t count = done + 1;
+  if (iters) std::memcpy(iters, recs.data(), std::min(count, cap) * sizeof(enmf_gpu_iter));
+  if (n_iters) *n_iters = count;
+  if (out.error_code != ENMF_OK) {
+    se->failed = true;
+    const char* what = out.error_code == ENMF_NON_FINITE ? "iteration produced a non-finite value"
+                       : out.error_code == ENMF_NO_CONVERGENCE
+                           ? "no convergence (degenerate factor column persists after reinitialization, or "
+                             "active_set_solve exchange limit exceeded)"
+                           : "device error";
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s at iteration %llu", what, (unsigned long long)out.k);
+    throw Fail{out.error_code, buf};
+  }
+  return count;
+}
+
+void end_impl(enmf_gpu_ctx* c, double* w_out, double* h_out, double* norm_x_out) {
+  Session* se = need_session(c);
+  cudaStream_t s = c->stream;
+  const size_t m = se->m, n = se->n, r = se->r;
+  if (norm_x_out) {
+    DevState out;
+    CU(cudaMemcpyAsync(&out, c->st.p, sizeof out, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *norm_x_out = out.norm_x;
+  }
+  if (w_out) {
+    dim3 tb(32, 8), tg((unsigned)((m + 31) / 32), (unsigned)((r + 31) / 32));
+    misc::transpose<<<tg, tb, 0, s>>>(c->WT.p, c->scratch.p, (int)r, (int)m);
+    CUK();
+    c->launches++;
+    CU(cudaMemcpyAsync(w_out, c->scratch.p, m * r * 8,
+                       se->dev_factors ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  }
+  if (h_out)
+    CU(cudaMemcpyAsync(h_out, c->H.p, r * n * 8, se->dev_factors ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       s));
+  CU(cudaStreamSynchronize(s));
+  close_session(c);
+}
+
+// enmf::run: begin + K steps + sync + end.
+int solve_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, bool dev_factors,
+               const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap, size_t* n_iters, double* w_out,
+               double* h_out, double* norm_x_out) {
+  begin_impl(c, w0, h0, r, dev_factors, cfg);
+  try {
+    step_impl(c, cfg->max_outer_iterations);
+    sync_impl(c, iters, iters_cap, n_iters);
+  } catch (...) {
+    close_session(c);
+    throw;
+  }
+  end_impl(c, w_out, h_out, norm_x_out);
+  return ENMF_OK;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    return f();
+  } catch (const Fail& e) {
+    set_err(e);
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ENMF_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int enmf_gpu_begin(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, int factors_on_device,
+                   const enmf_gpu_config* cfg) {
+  return guard([&] {
+    begin_impl(c, w0, h0, r, factors_on_device != 0, cfg);
+    return ENMF_OK;
+  });
+}
+
+int enmf_gpu_step(enmf_gpu_ctx* c, uint64_t count) {
+  return guard([&] {
+    step_impl(c, count);
+    return ENMF_OK;
+  });
+}
+
+int enmf_gpu_step_profiled(enmf_gpu_ctx* c, double* phase_ms, size_t cap) {
+  return guard([&] {
+    step_profiled_impl(c, phase_ms, cap);
+    return ENMF_OK;
+  });
+}
+
+int enmf_gpu_sync(enmf_gpu_ctx* c, enmf_gpu_iter* iters, size_t cap, size_t* n_iters) {
+  return guard([&] {
+    sync_impl(c, iters, cap, n_iters);
+    return ENMF_OK;
+  });
+}
+
+int enmf_gpu_end(enmf_gpu_ctx* c, double* w_out, double* h_out, double* norm_x) {
+  return guard([&] {
+    end_impl(c, w_out, h_out, norm_x);
+    return ENMF_OK;
+  });
+}
+
+void* enmf_gpu_stream(enmf_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+}  // extern "C"
+
+#include "cabi.inc"
+#include "kernels_api.inc"

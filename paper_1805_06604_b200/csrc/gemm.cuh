@@ -1,0 +1,276 @@
+// gemm.cuh — FP64 contractions of the enmf hot path on sm_100a.
+//
+// One tensor-core kernel serves every dense contraction of step()
+// (engine.hpp:309-440):
+//   C_H  = W_yᵀ X       cross_wx   linalg.hpp:67-83    A = W_yᵀ (r×m), B = X   (K×N, N-contiguous)
+//   P    = T Xᵀ = (X Tᵀ)ᵀ cross_xht linalg.hpp:107-124  A = T    (r×n), B = X   (N×K, K-contiguous)
+//   G    = A Aᵀ         gram       linalg.hpp:49-64    A = W_yᵀ | T | W_nᵀ,  B = A (K-contiguous)
+// Blackwell has no FP64 tcgen05 kind, so the FP64 tensor path is the legacy
+// warp-level DMMA: PTX mma.sync.m8n8k4.f64, which ptxas lowers to one native
+// DMMA.8x8x4 on sm_100a (measured 37.1 TFLOP/s peak on B200 vs 33.8 for DFMA,
+// profiles/r01_fp64_peak.txt).  Tiles stream through a 3-stage cp.async ring
+// in shared memory with bank-conflict-free padded layouts; split-K keeps all
+// 148 SMs busy on the skinny r×32768 outputs and its partials are reduced in a
+// fixed order (deterministic).
+//
+// The *_exact kernels are the bitwise-faithful debug path (precision =
+// ENMF_PRECISION_FP64_EXACT): one thread per output element summing in the
+// reference's sequential order with separately rounded multiply and add.
+#pragma once
+
+#include "common.cuh"
+
+namespace gemm {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, NT = 256;
+constexpr int LDA_S = BK + 4;   // A tile [m][k]
+constexpr int LDB_N = BN + 4;   // B tile [k][n]   (B_KMAJOR = false)
+constexpr int LDB_K = BK + 4;   // B tile [n][k]   (B_KMAJOR = true)
+constexpr int A_STAGE = BM * LDA_S;
+constexpr int B_STAGE = (BN * LDB_K > BK * LDB_N) ? BN * LDB_K : BK * LDB_N;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(double);
+
+ENMF_DEV void cp_async16(double* smem, const double* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+ENMF_DEV void cp_async8(double* smem, const double* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+ENMF_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+ENMF_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+ENMF_DEV void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct Params {
+  const double* A; long lda;     // M×K, K contiguous
+  const double* B; long ldb;     // B_KMAJOR: N×K (K contiguous) ; else K×N (N contiguous)
+  double* C; long ldc;           // M×N
+  int M, N, K;
+  int splits;                    // split-K factor (gridDim.z)
+  double* partials;              // splits × M × N (splits > 1)
+  unsigned* counters;            // one per output tile (REDUCE_LAST)
+  int sym;                       // write C[i][j] = C[j][i] from i <= j (Gram)
+  const DevState* st;            // nullable: skip work when !st->active
+};
+
+// Loads one BM×BK tile of a K-contiguous operand (rows row0.., k0..).
+template <int VEC>
+ENMF_DEV void load_kmajor(double* s, int lds, const double* g, long ld, int rows_valid, int row0,
+                          int k0, int K, int nrows) {
+  constexpr int CH = BK / VEC;  // chunks per row
+  for (int c = threadIdx.x; c < nrows * CH; c += NT) {
+    const int row = c / CH, col = (c % CH) * VEC;
+    const int gr = row0 + row, gk = k0 + col;
+    int valid = 0;
+    if (gr < rows_valid && gk < K) valid = (K - gk >= VEC) ? VEC : (K - gk);
+    const double* src = valid ? g + (long)gr * ld + gk : g;
+    if (VEC == 2) cp_async16(s + row * lds + col, src, valid * 8);
+    else cp_async8(s + row * lds + col, src, valid * 8);
+  }
+}
+// Loads a BK×BN tile of an N-contiguous operand (k rows k0.., cols n0..).
+template <int VEC>
+ENMF_DEV void load_nmajor(double* s, const double* g, long ld, int k0, int K, int n0, int N) {
+  constexpr int CH = BN / VEC;
+  for (int c = threadIdx.x; c < BK * CH; c += NT) {
+    const int row = c / CH, col = (c % CH) * VEC;
+    const int gk = k0 + row, gn = n0 + col;
+    int valid = 0;
+    if (gk < K && gn < N) valid = (N - gn >= VEC) ? VEC : (N - gn);
+    const double* src = valid ? g + (long)gk * ld + gn : g;
+    if (VEC == 2) cp_async16(s + row * LDB_N + col, src, valid * 8);
+    else cp_async8(s + row * LDB_N + col, src, valid * 8);
+  }
+}
+
+// C[M×N] (+)= A · op(B) on DMMA.  grid = (ceil(N/BN), ceil(M/BM), splits).
+template <bool B_KMAJOR, int VEC, bool REDUCE_LAST>
+__global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
+  if (p.st && !dev_active(p.st)) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int KB = (p.K + BK - 1) / BK;
+  const int per = (KB + p.splits - 1) / p.splits;
+  const int kb0 = blockIdx.z * per;
+  const int kb1 = min(KB, kb0 + per);
+  const int nk = max(0, kb1 - kb0);
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int kb, int stage) {
+    const int k0 = (kb0 + kb) * BK;
+    load_kmajor<VEC>(As + stage * A_STAGE, LDA_S, p.A, p.lda, p.M, m0, k0, p.K, BM);
+    if (B_KMAJOR) load_kmajor<VEC>(Bs + stage * B_STAGE, LDB_K, p.B, p.ldb, p.N, n0, k0, p.K, BN);
+    else load_nmajor<VEC>(Bs + stage * B_STAGE, p.B, p.ldb, k0, p.K, n0, p.N);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_commit();
+  }
+  for (int kb = 0; kb < nk; ++kb) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kb + STAGES - 1;
+      if (nxt < nk) issue(nxt, nxt % STAGES);
+      cp_commit();
+    }
+    const double* as = As + (kb % STAGES) * A_STAGE + (wm * 64 + g) * LDA_S + t;
+    const double* bs = Bs + (kb % STAGES) * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[8], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) a[mi] = as[mi * 8 * LDA_S + kk * 4];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        if (B_KMAJOR) b[ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kk * 4 + t];
+        else b[ni] = bs[(kk * 4 + t) * LDB_N + wn * 32 + ni * 8 + g];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+  }
+  cp_wait<0>();
+
+  // ---- epilogue ----
+  const bool split = p.splits > 1;
+  double* out = split ? p.partials + (long)blockIdx.z * p.M * p.N : p.C;
+  const long ldo = split ? p.N : p.ldc;
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const int row = m0 + wm * 64 + mi * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int col = n0 + wn * 32 + ni * 8 + 2 * t;
+      if (!split && p.sym) {
+        // Gram without split: keep the upper triangle, mirror it.
+        for (int e = 0; e < 2; ++e) {
+          const int c = col + e;
+          if (c < p.N && row <= c) {
+            out[(long)row * ldo + c] = acc[mi][ni][e];
+            out[(long)c * ldo + row] = acc[mi][ni][e];
+          }
+        }
+      } else if (col + 1 < p.N && ((ldo & 1) == 0)) {
+        *reinterpret_cast<double2*>(out + (long)row * ldo + col) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (col < p.N) out[(long)row * ldo + col] = acc[mi][ni][0];
+        if (col + 1 < p.N) out[(long)row * ldo + col + 1] = acc[mi][ni][1];
+      }
+    }
+  }
+  if (!split || !REDUCE_LAST) return;
+
+  // Last CTA of this output tile sums the partials in split order 0..S-1.
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* ctr = p.counters + blockIdx.y * gridDim.x + blockIdx.x;
+    const unsigned prev = atomicAdd(ctr, 1u);
+    s_last = (prev == (unsigned)p.splits - 1) ? 1u : 0u;
+    if (s_last) *ctr = 0;  // re-arm for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+  const long MN = (long)p.M * p.N;
+  for (int e = tid; e < rows * cols; e += NT) {
+    const int i = m0 + e / cols, j = n0 + e % cols;
+    if (p.sym && i > j) continue;
+    const double* src = p.partials + (long)i * p.N + j;
+    double v = __ldcg(src);
+    for (int s = 1; s < p.splits; ++s) v = __dadd_rn(v, __ldcg(src + s * MN));
+    p.C[(long)i * p.ldc + j] = v;
+    if (p.sym) p.C[(long)j * p.ldc + i] = v;
+  }
+}
+
+// Separate split-K reduction (fixed order), used when one output tile has
+// many splits (the r×r Grams: K = 32768, 1 tile, 148 splits).
+__global__ void reduce_splits(const double* __restrict__ part, int splits, int M, int N,
+                              double* __restrict__ C, long ldc, int sym, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long MN = (long)M * N;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < MN; e += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    if (sym && i > j) continue;
+    double v = part[e];
+    for (int s = 1; s < splits; ++s) v = __dadd_rn(v, part[e + s * MN]);
+    C[(long)i * ldc + j] = v;
+    if (sym) C[(long)j * ldc + i] = v;
+  }
+}
+
+// ---- bitwise-faithful kernels (reference summation order, no FMA) --------
+
+// gram (linalg.hpp:49-64) of the K×r matrix whose column k is row k of A
+// (A r×K, K contiguous):  g[k][j] = sum_i A[k][i]*A[j][i], i ascending, k<=j, mirrored.
+__global__ void gram_exact(const double* __restrict__ A, long lda, int r, int K, double* __restrict__ G,
+                           const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= r * r) return;
+  const int k = idx / r, j = idx % r;
+  if (k > j) return;
+  const double* ak = A + (long)k * lda;
+  const double* aj = A + (long)j * lda;
+  double s = 0.0;
+  for (int i = 0; i < K; ++i) s = __dadd_rn(s, __dmul_rn(ak[i], aj[i]));
+  G[k * r + j] = s;
+  G[j * r + k] = s;
+}
+
+// cross_wx (linalg.hpp:67-83): out[k][j] = sum_i W[i][k]*X[i][j], i ascending; W given as WT (r×m).
+__global__ void cross_wx_exact(const double* __restrict__ WT, const double* __restrict__ X, int m, int n,
+                               int r, double* __restrict__ out, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long idx = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (idx >= (long)r * n) return;
+  const int k = (int)(idx / n), j = (int)(idx % n);
+  const double* wk = WT + (long)k * m;
+  double s = 0.0;
+  for (int i = 0; i < m; ++i) s = __dadd_rn(s, __dmul_rn(wk[i], X[(long)i * n + j]));
+  out[idx] = s;
+}
+
+// cross_xht (linalg.hpp:107-124): xht[i][k] = sum_j X[i][j]*T[k][j], j ascending;
+// written transposed: P[k][i].
+__global__ void cross_xht_exact(const double* __restrict__ X, const double* __restrict__ T, int m, int n,
+                                int r, double* __restrict__ P, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long idx = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (idx >= (long)r * m) return;
+  const int k = (int)(idx / m), i = (int)(idx % m);
+  const double* xi = X + (long)i * n;
+  const double* tk = T + (long)k * n;
+  double s = 0.0;
+  for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(xi[j], tk[j]));
+  P[idx] = s;
+}
+
+}  // namespace gemm

@@ -1,0 +1,287 @@
+"""GPU tier: the B200 path vs the oracle / the reference's golden fixtures,
+through the C-ABI (libenmf_gpu.so).
+
+Bars (BASELINE.json north_star), FP64:
+  * accept/restart sequence identical;
+  * per-iteration relative error within 1e-9 relative (iterations whose error
+    is below 1e-6·||X|| excluded, as the reference's own tests do,
+    test_engine.cpp:67-81);
+  * final W, H within 1e-6 relative (max-norm relative to the factor's scale).
+The bitwise-faithful mode (Precision.fp64_exact) must reproduce the reference
+bit for bit.
+"""
+import numpy as np
+import pytest
+
+import paper_1805_06604_b200 as E
+from oracle.oracle import preset
+
+pytestmark = pytest.mark.gpu
+
+PRESETS = ["e-ahals-hp3", "e-ahals-hp1", "e-anls-hp1", "anls", "ahals", "e-anls-hp3"]
+REL_ERR_TOL = 1e-9
+FACTOR_TOL = 1e-6
+
+
+def _cfg(name, iters, prec=E.Precision.fp64, **kw):
+    c = E.algorithm_config(name)
+    c.max_outer_iterations = iters
+    c.precision = prec
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def _cfg_from_meta(meta, prec):
+    c = E.SolverConfig(inner_h=E.InnerSolver(meta["inner_h"]), inner_w=E.InnerSolver(meta["inner_w"]),
+                       hp=meta["hp"], beta0=meta["beta0"], gamma=meta["gamma"], gamma_bar=meta["gamma_bar"],
+                       eta=meta["eta"], max_outer_iterations=meta["max_outer_iterations"],
+                       extrapolation_enabled=bool(meta["extrapolation_enabled"]),
+                       literal_hp1_order=bool(meta["literal_hp1_order"]),
+                       inner_max_sweeps=meta["inner_max_sweeps"] or None, reinit_seed=meta["reinit_seed"],
+                       precision=prec)
+    return c
+
+
+def assert_parity(rec, err_ref, restarted_ref, w_ref, h_ref, norm_x, tol=REL_ERR_TOL):
+    err = rec.column("error")
+    assert len(err) == len(err_ref)
+    assert np.array_equal(rec.column("restarted").astype(np.int32), np.asarray(restarted_ref, dtype=np.int32))
+    keep = err_ref > 1e-6 * norm_x
+    dev = np.abs(err[keep] - err_ref[keep]) / err_ref[keep]
+    assert dev.max(initial=0.0) <= tol, f"max relative error deviation {dev.max():.3e}"
+    assert np.max(np.abs(rec.factors.w - w_ref)) <= FACTOR_TOL * np.max(np.abs(w_ref))
+    assert np.max(np.abs(rec.factors.h - h_ref)) <= FACTOR_TOL * np.max(np.abs(h_ref))
+
+
+def assert_bitwise(rec, g):
+    assert np.array_equal(rec.column("error"), g["error"])
+    assert np.array_equal(rec.column("restarted").astype(np.int32), g["restarted"].astype(np.int32))
+    assert np.array_equal(rec.column("beta"), g["beta"])
+    assert np.array_equal(rec.factors.w, g["w"]) and np.array_equal(rec.factors.h, g["h"])
+
+
+# ---------------------------------------------------------------- config 1
+@pytest.mark.parametrize("name", PRESETS)
+def test_c1_exact_mode_bitwise_vs_reference(ctx, golden, name):
+    inp = golden.load("c1_inputs")
+    g = golden.load(f"c1_{name}")
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg(name, 200, E.Precision.fp64_exact), E.TimingMode.none)
+    assert_bitwise(rec, g)
+    assert rec.norm_x == float(g["norm_x"])
+
+
+@pytest.mark.parametrize("name", PRESETS)
+def test_c1_fast_mode_parity(ctx, golden, name):
+    inp = golden.load("c1_inputs")
+    g = golden.load(f"c1_{name}")
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg(name, 200), E.TimingMode.none)
+    assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]))
+
+
+def test_c1_known_answer_fast(ctx, golden):
+    inp = golden.load("c1_inputs")
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg("e-ahals-hp3", 200), E.TimingMode.none)
+    ka = golden.meta["known_answers"]["c1_e-ahals-hp3_final_relative_error"]
+    assert abs(rec.final_relative_error() - ka) <= 1e-9 * ka
+    assert int(rec.column("restarted").sum()) == 5
+
+
+# ------------------------------------------------------- every config branch
+VARIANTS = ["small_hals_hp2", "small_hals_hp1_literal", "small_exact_hp2", "small_exact_hp1_literal",
+            "small_hals_noextrap", "small_hals_beta0", "small_mixed_hals_exact", "small_hals_sweeps3"]
+
+
+@pytest.mark.parametrize("tag", VARIANTS)
+def test_variants_exact_bitwise(ctx, golden, tag):
+    inp = golden.load("small_inputs")
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg_from_meta(golden.meta[tag], E.Precision.fp64_exact),
+                  E.TimingMode.none)
+    assert_bitwise(rec, golden.load(tag))
+
+
+@pytest.mark.parametrize("tag", [t for t in VARIANTS if "literal" not in t])
+def test_variants_fast_parity(ctx, golden, tag):
+    inp = golden.load("small_inputs")
+    g = golden.load(tag)
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg_from_meta(golden.meta[tag], E.Precision.fp64),
+                  E.TimingMode.none)
+    assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]))
+
+
+@pytest.mark.parametrize("tag", ["reinit_hals", "reinit_exact"])
+@pytest.mark.parametrize("prec", [E.Precision.fp64_exact, E.Precision.fp64])
+def test_dead_column_reinit(ctx, golden, tag, prec):
+    """engine.hpp:268-296: redraw from mt19937_64(mix_seed(seed, 2k, attempt)) on the device."""
+    inp = golden.load("reinit_inputs")
+    g = golden.load(tag)
+    rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg_from_meta(golden.meta[tag], prec), E.TimingMode.none)
+    assert rec.iterations[1].reinit_events & 1
+    if prec == E.Precision.fp64_exact:
+        assert_bitwise(rec, g)
+    else:
+        assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]))
+
+
+# ----------------------------------------------- configs 2 and 3 (shortened)
+def test_c2_image_shaped_parity(ctx, port):
+    """BASELINE config 2 shape (10304×400, r=40, 70%-sparse W0, noise, rescaled), 12 iterations."""
+    x = port.gen_config(2, 10304, 400, 40, 1)
+    w0, h0 = port.random_init(10304, 400, 40, 2)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=12))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 12), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+
+
+def test_c3_eanls_parity(ctx, port):
+    """BASELINE config 3 (2000×2000, r=30, E-ANLS hp1, BPP both sides), 4 iterations."""
+    x = port.gen_config(3, 2000, 2000, 30, 1)
+    w0, h0 = port.random_init(2000, 2000, 30, 2)
+    ref = port.run_dense(x, w0, h0, preset("e-anls-hp1", max_outer_iterations=4))
+    rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 4), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+
+
+# --------------------------------------------------------------- kernels
+def test_kernels_vs_golden(ctx, golden):
+    k = golden.load("kernels")
+    g = ctx.gram(k["w"])
+    assert np.array_equal(g, g.T), "gram must be bitwise symmetric"
+    assert np.max(np.abs(g - k["gram"]) / np.abs(k["gram"])) <= 1e-13
+    c = ctx.cross_wx(k["w"], k["x"])
+    assert np.max(np.abs(c - k["cross"]) / np.abs(k["cross"])) <= 1e-13
+    hb, _ = ctx.active_set_solve(k["gram"], k["cross"], np.abs(k["h0"]))
+    assert np.array_equal(hb, k["bpp"]), "BPP is bitwise-faithful given identical inputs"
+    hh, _ = ctx.hals_solve(k["gram"], k["cross"], k["h0"], 25, 0.01)
+    assert np.max(np.abs(hh - k["hals"])) <= 1e-9 * np.max(np.abs(k["hals"]))
+
+
+def test_exact_kernels_bitwise(ctx, golden):
+    k = golden.load("kernels")
+    ctx.set_precision(E.Precision.fp64_exact)
+    try:
+        assert np.array_equal(ctx.gram(k["w"]), k["gram"])
+        assert np.array_equal(ctx.cross_wx(k["w"], k["x"]), k["cross"])
+        hh, _ = ctx.hals_solve(k["gram"], k["cross"], k["h0"], 25, 0.01)
+        assert np.array_equal(hh, k["hals"])
+    finally:
+        ctx.set_precision(E.Precision.fp64)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 5, 3), (129, 131, 17), (300, 257, 128), (64, 1000, 65)])
+def test_gemm_ragged_shapes(ctx, port, shape):
+    m, n, r = shape
+    rng = np.random.default_rng(m * 7 + n)
+    w, x, h = rng.random((m, r)), rng.random((m, n)) - 0.3, rng.random((r, n))
+    np.testing.assert_allclose(ctx.cross_wx(w, x), port.cross_wx(w, x), rtol=1e-12, atol=1e-12 * m)
+    np.testing.assert_allclose(ctx.cross_xht(x, h), port.cross_xht(x, h), rtol=1e-12, atol=1e-12 * n)
+    g = ctx.gram(w)
+    assert np.array_equal(g, g.T)
+    np.testing.assert_allclose(g, port.gram(w), rtol=1e-12)
+
+
+def test_fast_error_vs_direct(ctx, port):
+    """engine.hpp:121-136 vs the direct residual (test_engine.cpp:102-115), 1e-10."""
+    rng = np.random.default_rng(83)
+    for _ in range(10):
+        w, h, x = rng.random((30, 5)), rng.random((5, 40)), rng.random((30, 40))
+        direct = np.linalg.norm(x - w @ h)
+        fast = ctx.fast_error(port.lib.orc_frob_norm_sq(np.ascontiguousarray(x), x.size), w,
+                              port.cross_xht(x, h), port.gram(h.T.copy()))
+        assert abs(fast - direct) <= 1e-10 * direct
+
+
+def test_bpp_vs_oracle_random(ctx, port):
+    rng = np.random.default_rng(7)
+    for r in (1, 3, 8, 20, 33, 64):
+        w = rng.random((r + 10, r))
+        x = rng.random((r + 10, 50)) - 0.4
+        G, Cm = port.gram(w), port.cross_wx(w, x)
+        h0 = np.maximum(rng.random((r, 50)) - 0.5, 0)
+        a, ra = ctx.active_set_solve(G, Cm, h0)
+        b, rb = port.active_set_solve(G, Cm, h0)
+        assert np.array_equal(a, b) and ra == rb, r
+
+
+def test_rank_deficient_gram_bpp(ctx, port):
+    rng = np.random.default_rng(3)
+    w = rng.random((20, 6))
+    w[:, 5] = w[:, 0] + w[:, 1]      # rank-deficient Gram: pivot drop + ban path
+    G, Cm = port.gram(w), port.cross_wx(w, rng.random((20, 30)))
+    a, _ = ctx.active_set_solve(G, Cm, np.ones((6, 30)))
+    b, _ = port.active_set_solve(G, Cm, np.ones((6, 30)))
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ error paths
+def test_invalid_inputs(ctx):
+    x = np.random.default_rng(0).random((10, 8))
+    w, h = np.random.default_rng(1).random((10, 3)), np.random.default_rng(2).random((3, 8))
+    with pytest.raises(E.InvalidArgument):
+        ctx.run(x, -w, h, _cfg("e-ahals-hp3", 2))
+    with pytest.raises(E.InvalidArgument):
+        ctx.run(x, w, h, _cfg("e-ahals-hp3", 2, hp=4))
+    bad = x.copy()
+    bad[0, 0] = np.nan
+    with pytest.raises(E.InvalidArgument):
+        ctx.run(bad, w, h, _cfg("e-ahals-hp3", 2))
+    with pytest.raises(E.DegenerateColumn):
+        ctx.hals_solve(np.zeros((2, 2)), np.zeros((2, 3)), np.zeros((2, 3)), 3)
+    # a valid call still works after the failures (no sticky state)
+    rec = ctx.run(x, w, h, _cfg("e-ahals-hp3", 3))
+    assert len(rec.iterations) == 4
+
+
+def test_empty_budget_and_wall_timing(ctx):
+    x = np.random.default_rng(0).random((16, 12))
+    w, h = np.random.default_rng(1).random((16, 3)), np.random.default_rng(2).random((3, 12))
+    rec = ctx.run(x, w, h, _cfg("e-ahals-hp3", 0))
+    assert len(rec.iterations) == 1
+    assert np.array_equal(rec.factors.w, w) and np.array_equal(rec.factors.h, h)
+    rec = ctx.run(x, w, h, _cfg("e-ahals-hp3", 20), E.TimingMode.wall)
+    el = rec.column("elapsed_seconds")
+    assert np.all(np.diff(el) > 0)   # strictly increasing (engine.hpp:509-514)
+
+
+def test_deterministic_reruns(ctx, golden):
+    inp = golden.load("c1_inputs")
+    a = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg("e-ahals-hp3", 50), E.TimingMode.none)
+    b = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg("e-ahals-hp3", 50), E.TimingMode.none)
+    assert np.array_equal(a.column("error"), b.column("error"))
+    assert np.array_equal(a.factors.w, b.factors.w) and np.array_equal(a.factors.h, b.factors.h)
+
+
+# ------------------------------------------- full-size, size-independent properties
+def test_c5_full_size_properties(ctx):
+    """m = n = 32768, r = 128 (BASELINE config 5): the device-reported error equals
+    the directly computed residual ||X - WH||_F (torch FP64) — the trace identity at
+    full size (hp = 1: the error is taken at the accepted pair (W_n, H_n)) — and no
+    two consecutive raises."""
+    torch = pytest.importorskip("torch")
+    m = n = 32768
+    r = 128
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.randn(m, n, device=dev, dtype=torch.float64, generator=g).abs_().mul_(0.01)
+    x.addmm_(torch.rand(m, r, device=dev, dtype=torch.float64, generator=g),
+             torch.rand(r, n, device=dev, dtype=torch.float64, generator=g))
+    wi = torch.rand(m, r, device=dev, dtype=torch.float64, generator=g)
+    hi = torch.rand(r, n, device=dev, dtype=torch.float64, generator=g)
+    wo = torch.empty_like(wi)
+    ho = torch.empty_like(hi)
+    ctx.load_device(x.data_ptr(), m, n)
+    cfg = _cfg("e-ahals-hp1", 6)
+    rec = ctx.solve_device(wi.data_ptr(), hi.data_ptr(), r, cfg, wo.data_ptr(), ho.data_ptr())
+    err = rec.column("error")
+    restarted = rec.column("restarted")
+    # last accepted pair = returned factors; its error is the last non-restarted record
+    k_acc = max(k for k in range(len(err)) if k == 0 or not restarted[k])
+    direct = torch.linalg.norm(x - wo @ ho).item()
+    if k_acc == len(err) - 1:
+        assert abs(direct - err[k_acc]) <= 1e-9 * direct
+    ups = np.diff(err) > 0
+    assert not np.any(ups[1:] & ups[:-1])
+    assert err[-1] < err[0]
+    assert np.all(wo.cpu().numpy() >= 0) and np.all(ho.cpu().numpy() >= 0)
