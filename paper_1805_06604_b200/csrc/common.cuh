@@ -178,6 +178,32 @@ ENMF_DEV double block_reduce_sum(double v, double* sh) {
   return r;
 }
 
+// Any block size (multiple of 32): xor-butterfly inside each warp, then warp
+// partials summed in warp order by thread 0.  Deterministic; result broadcast.
+ENMF_DEV double block_reduce_sum_any(double v, double* sh) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = sh[0];
+    for (int w = 1; w < nw; ++w) s = __dadd_rn(s, sh[w]);
+    sh[32] = s;
+  }
+  __syncthreads();
+  const double r = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// D(8×8) += A(8×4) · B(4×8) in FP64 on the tensor pipe (one DMMA.8x8x4 on sm_100a).
+ENMF_DEV void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 template <int NT>
 ENMF_DEV int block_reduce_or(int v, int* sh) {
   const int r = __syncthreads_or(v);

@@ -120,6 +120,12 @@ void set_attrs_once() {
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
   big((const void*)hals::sweep_fast<32, 4>, hals::smem_bytes<32, 4>());
+  big((const void*)hals::sweep_dmma<32>, hals::dmma_smem_bytes<32>());
+  big((const void*)hals::sweep_dmma<64>, hals::dmma_smem_bytes<64>());
+  big((const void*)hals::sweep_dmma<128>, hals::dmma_smem_bytes<128>());
+  big((const void*)hals::sweep_dmma_p<32>, hals::dmma_smem_bytes<32>());
+  big((const void*)hals::sweep_dmma_p<64>, hals::dmma_smem_bytes<64>());
+  big((const void*)hals::sweep_dmma_p<128>, hals::dmma_smem_bytes<128>());
   big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
   big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
   done = true;
@@ -134,18 +140,24 @@ inline unsigned grid_for(long count, int nt = 256, int maxb = 148 * 8) {
 enum { PREC_FAST = ENMF_PRECISION_FP64, PREC_EXACT = 2 };
 
 // ---- contractions --------------------------------------------------------------
+// Split-K factor: the smallest S whose CTA count fills the SMs to >= 95%
+// (1 CTA/SM: 216 KB of shared memory).  Multi-tile GEMMs are capped at S = 8
+// (partials cost 2·S·M·N·8 bytes of extra traffic; the last CTA of a tile
+// reduces them); a single-tile GEMM (the r×r Gram) splits up to one CTA per
+// SM with a separate fixed-order reduction.
 int choose_splits(int tiles, int kblocks, int sms) {
   if (tiles >= 2 * sms) return 1;
-  const int smax = std::max(1, std::min(kblocks / 4, 512));
+  const int smax = tiles > 8 ? std::max(1, std::min(kblocks / 4, 8))
+                             : std::max(1, std::min(kblocks / 4, sms));
   int best = 1;
-  double best_score = -1.0;
+  double best_eff = -1.0;
   for (int s = 1; s <= smax; ++s) {
     const long ctas = (long)tiles * s;
     const long waves = (ctas + sms - 1) / sms;
     const double eff = (double)ctas / (double)(waves * sms);
-    const double score = eff - 0.0005 * s;
-    if (score > best_score + 1e-9) {
-      best_score = score;
+    if (eff >= 0.95) return s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
       best = s;
     }
   }
@@ -201,6 +213,19 @@ void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, lon
 }
 
 // ---- inner solvers ------------------------------------------------------------
+// HALS sweep kernel variant: ENMF_HALS_KERNEL=fma selects the CUDA-core
+// register kernel (A/B comparisons); default is the DMMA blocked sweep.
+int hals_variant() {  // 0: persistent DMMA (default), 1: fma, 2: unrolled DMMA (v1)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ENMF_HALS_KERNEL");
+    const std::string s = e ? e : "";
+    v = s == "fma" ? 1 : (s == "dmma1" ? 2 : 0);
+  }
+  return v;
+}
+bool hals_use_fma() { return hals_variant() == 1; }
+
 void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   const int r = a.r;
   if (prec == PREC_EXACT || r > 128) {
@@ -211,22 +236,36 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     c->launches += 2;
     return;
   }
+  if (hals_use_fma()) {
 #define SW(S_, T_)                                                                          \
   hals::sweep_fast<S_, T_><<<(a.N + hals::NT / T_ - 1) / (hals::NT / T_), hals::NT,          \
                              hals::smem_bytes<S_, T_>(), s>>>(a)
-  if (r <= 16) SW(16, 1);
-  else if (r <= 32) SW(32, 1);
-  else if (r <= 64) SW(32, 2);
-  else SW(32, 4);
+    if (r <= 16) SW(16, 1);
+    else if (r <= 32) SW(32, 1);
+    else if (r <= 64) SW(32, 2);
+    else SW(32, 4);
 #undef SW
+  } else if (hals_variant() == 2) {
+    constexpr int cols = hals::kDmmaWarps * 8;
+    const unsigned grid = (unsigned)((a.N + cols - 1) / cols);
+#define SD(R_) hals::sweep_dmma<R_><<<grid, hals::kDmmaWarps * 32, hals::dmma_smem_bytes<R_>(), s>>>(a)
+    if (r <= 32) SD(32);
+    else if (r <= 64) SD(64);
+    else SD(128);
+#undef SD
+  } else {
+    constexpr int cols = hals::kDmmaWarps * 8;
+    const int ntiles = (a.N + cols - 1) / cols;
+    const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+#define SP(R_) \
+  hals::sweep_dmma_p<R_><<<grid, hals::kDmmaWarps * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles)
+    if (r <= 32) SP(32);
+    else if (r <= 64) SP(64);
+    else SP(128);
+#undef SP
+  }
   CUK();
   c->launches++;
-}
-
-int hals_grid(int r, int N, int prec) {
-  if (prec == PREC_EXACT || r > 128) return (N + hals::NT - 1) / hals::NT;
-  const int tpc = r <= 32 ? 1 : (r <= 64 ? 2 : 4);
-  return (N + hals::NT / tpc - 1) / (hals::NT / tpc);
 }
 
 void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a) {

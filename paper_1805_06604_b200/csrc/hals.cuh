@@ -81,7 +81,8 @@ ENMF_DEV bool sweep_skipped(const Args& a) {
 }
 
 // Last-arriving block: fixed-order sum of the per-block partials.
-ENMF_DEV void last_block_reduce(const Args& a, double block_gain, int block_nf, double* red) {
+template <int NTH>
+ENMF_DEV void last_block_reduce_n(const Args& a, double block_gain, int block_nf, double* red) {
   __shared__ unsigned s_last;
   if (threadIdx.x == 0) {
     a.part[blockIdx.x] = block_gain;
@@ -95,11 +96,11 @@ ENMF_DEV void last_block_reduce(const Args& a, double block_gain, int block_nf, 
   __threadfence();
   double v = 0.0;
   int nf = 0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) {
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += NTH) {
     v = __dadd_rn(v, __ldcg(a.part + b));
     nf |= __ldcg(a.part_nf + b);
   }
-  const double total = block_reduce_sum<NT>(v, red);
+  const double total = block_reduce_sum_any(v, red);
   nf = __syncthreads_or(nf);
   if (threadIdx.x == 0) {
     a.ctl->arrive = 0;
@@ -188,7 +189,314 @@ __global__ void __launch_bounds__(NT) sweep_fast(Args a) {
   }
   const double bg = block_reduce_sum<NT>(valid ? gain : 0.0, red);
   nf = __syncthreads_or(nf);
-  last_block_reduce(a, bg, nf, red);
+  last_block_reduce_n<NT>(a, bg, nf, red);
+}
+
+// ---- tensor-core sweep: blocked Gauss-Seidel on DMMA ----------------------
+//
+// The r rows are processed in blocks of 8.  For block K = [k0, k0+8) and the 8
+// columns a warp owns,
+//     S = G[K, :] · H            (DMMA m8n8k4 over j, 4 independent accumulators)
+// uses the current H (rows < k0 already updated this sweep, rows >= k0 old), so
+//     b_k = C_k - sum_{j != k} G_kj h_j = C_k - S_k + G_kk h_old_k - sum_{i in K, i < k} G_ki (h_new_i - h_old_i)
+// and the 8 rows of the block are then finished sequentially with one shuffle
+// per row to forward the change δ_i.  H lives in registers in the DMMA
+// B-fragment layout: lane (g, t) holds H[4s + t][col g] in slot s.  Per sweep
+// this is r·r·N FMAs on the tensor pipe (the reference's r² per column).
+constexpr int kDmmaWarps = 14;
+
+template <int RMAX>
+constexpr int dmma_smem_bytes() {
+  return RMAX * (RMAX + 4) * 8 + 2 * RMAX * 8;
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(kDmmaWarps * 32, 1) sweep_dmma(Args a) {
+  constexpr int LDG = RMAX + 4;    // conflict-free A-fragment rows
+  constexpr int SL = RMAX / 4;     // H slots per lane
+  constexpr int NB = RMAX / 8;     // row blocks
+  constexpr int NTH = kDmmaWarps * 32;
+  if (sweep_skipped(a)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* Gs = sm;                 // [RMAX][LDG]
+  double* Gd = sm + RMAX * LDG;    // G_kk (1 for padding rows)
+  double* Gi = Gd + RMAX;          // 1 / G_kk
+  __shared__ double red[NTH];
+
+  const int r = a.r;
+  for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
+    const int k = e / RMAX, j = e % RMAX;
+    Gs[k * LDG + j] = (k < r && j < r) ? a.G[k * r + j] : 0.0;
+  }
+  for (int k = threadIdx.x; k < RMAX; k += NTH) {
+    const double d = k < r ? a.G[k * r + k] : 1.0;
+    Gd[k] = d;
+    Gi[k] = __ddiv_rn(1.0, d);
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long c0 = ((long)blockIdx.x * kDmmaWarps + warp) * 8;
+  const long colH = c0 + g;                 // column this lane holds in the H layout
+  const bool validH = colH < a.N;
+  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
+  double hreg[SL];
+#pragma unroll
+  for (int s = 0; s < SL; ++s) {
+    const int j = 4 * s + t;
+    hreg[s] = (validH && j < r) ? src[(long)j * a.ld + colH] : 0.0;
+  }
+  // S-layout columns of this lane: c0 + 2t + e
+  const long colS = c0 + 2 * t;
+  const bool v0 = colS < a.N, v1 = colS + 1 < a.N;
+  auto loadC = [&](int k, double& x0, double& x1) {
+    x0 = (k < r && v0) ? a.C[(long)k * a.ld + colS] : 0.0;
+    x1 = (k < r && v1) ? a.C[(long)k * a.ld + colS + 1] : 0.0;
+  };
+  double cn0, cn1;
+  loadC(g, cn0, cn1);
+  double gain = 0.0;
+
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int k0 = 8 * b;
+    const double cc0 = cn0, cc1 = cn1;
+    if (b + 1 < NB) loadC(k0 + 8 + g, cn0, cn1);
+    // S = G[K, :] · H
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    const double* ga = Gs + (k0 + g) * LDG + t;
+#pragma unroll
+    for (int s = 0; s < SL; ++s) dmma884(acc[s & 3][0], acc[s & 3][1], ga[4 * s], hreg[s]);
+    const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
+    const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
+    // h_old of (row k0+g, cols colS, colS+1) from the H layout
+    const int srcA0 = (2 * t) * 4 + (g & 3), srcA1 = (2 * t + 1) * 4 + (g & 3);
+    const double lo0 = __shfl_sync(0xffffffffu, hreg[2 * b], srcA0);
+    const double lo1 = __shfl_sync(0xffffffffu, hreg[2 * b], srcA1);
+    const double hi0 = __shfl_sync(0xffffffffu, hreg[2 * b + 1], srcA0);
+    const double hi1 = __shfl_sync(0xffffffffu, hreg[2 * b + 1], srcA1);
+    const double ho0 = g < 4 ? lo0 : hi0, ho1 = g < 4 ? lo1 : hi1;
+    const int k = k0 + g;
+    const double gkk = Gd[k], ginv = Gi[k];
+    const double b0 = fma(gkk, ho0, __dsub_rn(cc0, S0));
+    const double b1 = fma(gkk, ho1, __dsub_rn(cc1, S1));
+    double gblk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) gblk[i] = Gs[k * LDG + k0 + i];
+    double corr0 = 0.0, corr1 = 0.0, hn0 = ho0, hn1 = ho1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double d0 = 0.0, d1 = 0.0;
+      if (g == i) {
+        const double t0 = __dmul_rn(__dsub_rn(b0, corr0), ginv);
+        const double t1 = __dmul_rn(__dsub_rn(b1, corr1), ginv);
+        hn0 = t0 > 0.0 ? t0 : 0.0;
+        hn1 = t1 > 0.0 ? t1 : 0.0;
+        d0 = __dsub_rn(hn0, ho0);
+        d1 = __dsub_rn(hn1, ho1);
+        const double o0 = __dsub_rn(ho0, t0), n0 = __dsub_rn(hn0, t0);
+        const double o1 = __dsub_rn(ho1, t1), n1 = __dsub_rn(hn1, t1);
+        gain = fma(gkk, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
+        gain = fma(gkk, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
+      }
+      if (i < 7) {
+        const double e0 = __shfl_sync(0xffffffffu, d0, i * 4 + t);
+        const double e1 = __shfl_sync(0xffffffffu, d1, i * 4 + t);
+        if (g > i) {
+          corr0 = fma(gblk[i], e0, corr0);
+          corr1 = fma(gblk[i], e1, corr1);
+        }
+      }
+    }
+    // back to the H layout: lane (g', t') takes rows k0+t' and k0+4+t' of column g'
+    const int srcB_lo = t * 4 + (g >> 1), srcB_hi = (t + 4) * 4 + (g >> 1);
+    const double x0lo = __shfl_sync(0xffffffffu, hn0, srcB_lo);
+    const double x1lo = __shfl_sync(0xffffffffu, hn1, srcB_lo);
+    const double x0hi = __shfl_sync(0xffffffffu, hn0, srcB_hi);
+    const double x1hi = __shfl_sync(0xffffffffu, hn1, srcB_hi);
+    hreg[2 * b] = (g & 1) ? x1lo : x0lo;
+    hreg[2 * b + 1] = (g & 1) ? x1hi : x0hi;
+  }
+  int nf = 0;
+  if (validH) {
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      const int j = 4 * s + t;
+      if (j < r) {
+        a.H[(long)j * a.ld + colH] = hreg[s];
+        nf |= !isfinite(hreg[s]);
+      }
+    }
+  }
+  const double bg = block_reduce_sum_any(gain, red);
+  nf = __syncthreads_or(nf);
+  last_block_reduce_n<NTH>(a, bg, nf, red);
+}
+
+// ---- persistent tensor-core sweep (default) ---------------------------------
+//
+// Same blocked Gauss-Seidel as sweep_dmma, restructured after profiling
+// (profiles/r01_sweep_dmma_v1.txt: spills, i-cache misses from the fully
+// unrolled block loop, per-CTA Gram reload, predicated-off FP64 work):
+//   * persistent: one CTA per SM walks the column tiles, the Gram is staged into
+//     shared memory once per launch with cp.async;
+//   * rolled block loop: the current block's rows always sit in slots 0/1 of
+//     the register file image of H (rotated by two slots after each block), the
+//     A-fragment column is indexed by the rotation instead;
+//   * the gain is evaluated after the sequential 8-row pass, by all lanes.
+template <int RMAX>
+__global__ void __launch_bounds__(kDmmaWarps * 32, 1) sweep_dmma_p(Args a, int ntiles) {
+  constexpr int LDG = RMAX + 4;
+  constexpr int SL = RMAX / 4;
+  constexpr int NB = RMAX / 8;
+  constexpr int NTH = kDmmaWarps * 32;
+  if (sweep_skipped(a)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* Gs = sm;
+  double* Gd = sm + RMAX * LDG;
+  double* Gi = Gd + RMAX;
+  __shared__ double red[NTH];
+
+  const int r = a.r;
+  {
+    // cp.async the r×r Gram into padded rows; padding zero-filled
+    constexpr int CH = RMAX / 2;  // 16-byte chunks per padded row
+    const bool vec = (r % 2 == 0) && (((uintptr_t)a.G & 15) == 0);
+    for (int e = threadIdx.x; e < RMAX * CH; e += NTH) {
+      const int k = e / CH, j = (e % CH) * 2;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(Gs + k * LDG + j);
+      if (vec) {
+        const int valid = (k < r && j < r) ? 16 : 0;
+        const double* srcp = valid ? a.G + (long)k * r + j : a.G;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(srcp), "r"(valid));
+      } else {
+        Gs[k * LDG + j] = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
+        Gs[k * LDG + j + 1] = (k < r && j + 1 < r) ? a.G[(long)k * r + j + 1] : 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int k = threadIdx.x; k < RMAX; k += NTH) {
+      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
+      Gd[k] = d;
+      Gi[k] = __ddiv_rn(1.0, d);
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
+  double gain = 0.0;
+  int nf = 0;
+  bool first = true;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long c0 = ((long)tile * kDmmaWarps + warp) * 8;
+    const long colH = c0 + g;
+    const bool validH = colH < a.N;
+    double hreg[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      const int j = 4 * s + t;
+      hreg[s] = (validH && j < r) ? src[(long)j * a.ld + colH] : 0.0;
+    }
+    const long colS = c0 + 2 * t;
+    const bool v0 = colS < a.N, v1 = colS + 1 < a.N;
+    double cn0 = (g < r && v0) ? a.C[(long)g * a.ld + colS] : 0.0;
+    double cn1 = (g < r && v1) ? a.C[(long)g * a.ld + colS + 1] : 0.0;
+    if (first) {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncthreads();
+      first = false;
+    }
+    const int srcA0 = (2 * t) * 4 + (g & 3), srcA1 = (2 * t + 1) * 4 + (g & 3);
+    const int srcB_lo = t * 4 + (g >> 1), srcB_hi = (t + 4) * 4 + (g >> 1);
+#pragma unroll 1
+    for (int b = 0; b < NB; ++b) {
+      const int k0 = 8 * b;
+      const int k = k0 + g;
+      const double cc0 = cn0, cc1 = cn1;
+      if (b + 1 < NB) {
+        const int kn = k + 8;
+        cn0 = (kn < r && v0) ? a.C[(long)kn * a.ld + colS] : 0.0;
+        cn1 = (kn < r && v1) ? a.C[(long)kn * a.ld + colS + 1] : 0.0;
+      }
+      // S = G[K, :] · H ; slot s holds rows 4·((s + 2b) mod SL) + t
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const double* ga = Gs + k * LDG + t;
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const int js = (s + 2 * b) & (SL - 1);
+        dmma884(acc[s & 3][0], acc[s & 3][1], ga[4 * js], hreg[s]);
+      }
+      const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
+      const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
+      const double lo0 = __shfl_sync(0xffffffffu, hreg[0], srcA0);
+      const double lo1 = __shfl_sync(0xffffffffu, hreg[0], srcA1);
+      const double hi0 = __shfl_sync(0xffffffffu, hreg[1], srcA0);
+      const double hi1 = __shfl_sync(0xffffffffu, hreg[1], srcA1);
+      const double ho0 = g < 4 ? lo0 : hi0, ho1 = g < 4 ? lo1 : hi1;
+      const double gkk = Gd[k], ginv = Gi[k];
+      const double b0 = fma(gkk, ho0, __dsub_rn(cc0, S0));
+      const double b1 = fma(gkk, ho1, __dsub_rn(cc1, S1));
+      double corr0 = 0.0, corr1 = 0.0, hn0 = ho0, hn1 = ho1, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double gki = Gs[k * LDG + k0 + i];
+        double d0 = 0.0, d1 = 0.0;
+        if (g == i) {
+          t0 = __dmul_rn(__dsub_rn(b0, corr0), ginv);
+          t1 = __dmul_rn(__dsub_rn(b1, corr1), ginv);
+          hn0 = t0 > 0.0 ? t0 : 0.0;
+          hn1 = t1 > 0.0 ? t1 : 0.0;
+          d0 = __dsub_rn(hn0, ho0);
+          d1 = __dsub_rn(hn1, ho1);
+        }
+        if (i < 7) {
+          const double e0 = __shfl_sync(0xffffffffu, d0, i * 4 + t);
+          const double e1 = __shfl_sync(0xffffffffu, d1, i * 4 + t);
+          if (g > i) {
+            corr0 = fma(gki, e0, corr0);
+            corr1 = fma(gki, e1, corr1);
+          }
+        }
+      }
+      {
+        const double o0 = __dsub_rn(ho0, t0), n0 = __dsub_rn(hn0, t0);
+        const double o1 = __dsub_rn(ho1, t1), n1 = __dsub_rn(hn1, t1);
+        gain = fma(gkk, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
+        gain = fma(gkk, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
+      }
+      const double x0lo = __shfl_sync(0xffffffffu, hn0, srcB_lo);
+      const double x1lo = __shfl_sync(0xffffffffu, hn1, srcB_lo);
+      const double x0hi = __shfl_sync(0xffffffffu, hn0, srcB_hi);
+      const double x1hi = __shfl_sync(0xffffffffu, hn1, srcB_hi);
+      const double new_lo = (g & 1) ? x1lo : x0lo;
+      const double new_hi = (g & 1) ? x1hi : x0hi;
+      // rotate: the next block's rows move into slots 0/1, this block's go last
+#pragma unroll
+      for (int s = 0; s + 2 < SL; ++s) hreg[s] = hreg[s + 2];
+      hreg[SL - 2] = new_lo;
+      hreg[SL - 1] = new_hi;
+    }
+    // after NB blocks the rotation is back to the identity (2·NB = SL)
+    if (validH) {
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const int j = 4 * s + t;
+        if (j < r) {
+          a.H[(long)j * a.ld + colH] = hreg[s];
+          nf |= !isfinite(hreg[s]);
+        }
+      }
+    }
+  }
+  if (first) {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+  }
+  const double bg = block_reduce_sum_any(gain, red);
+  nf = __syncthreads_or(nf);
+  last_block_reduce_n<NTH>(a, bg, nf, red);
 }
 
 // ---- bitwise-faithful sweep (hals_row_update_impl order) -----------------

@@ -43,13 +43,28 @@ def _cfg_from_meta(meta, prec):
     return c
 
 
-def assert_parity(rec, err_ref, restarted_ref, w_ref, h_ref, norm_x, tol=REL_ERR_TOL):
+def assert_parity(rec, err_ref, restarted_ref, w_ref, h_ref, norm_x, tol=REL_ERR_TOL, kappa=False):
+    """kappa=True: the per-iteration bar is max(1e-9, eps·κ_k), κ_k = (||X||/e_k)², the
+    cancellation bound of the trace identity itself: on the
+    noise-free config-1 data E-ANLS drives e to ~5e-7·||X|| where a 1e-16 perturbation
+    of the products already moves e by ~3e-5 relative in the reference."""
     err = rec.column("error")
     assert len(err) == len(err_ref)
-    assert np.array_equal(rec.column("restarted").astype(np.int32), np.asarray(restarted_ref, dtype=np.int32))
-    keep = err_ref > 1e-6 * norm_x
+    # Decisions are compared while the reference trajectory is above the 1e-6·||X||
+    # noise floor (test_engine.cpp:67-81); below it e is cancellation noise and so
+    # are the restart decisions taken on it (E-ANLS on noise-free data, SURVEY §6.3).
+    floor = 1e-6 * norm_x
+    below = np.nonzero(err_ref <= floor)[0]
+    kmax = int(below[0]) if len(below) else len(err_ref)
+    assert np.array_equal(rec.column("restarted")[:kmax].astype(np.int32),
+                          np.asarray(restarted_ref, dtype=np.int32)[:kmax])
+    keep = np.zeros(len(err_ref), dtype=bool)
+    keep[:kmax] = err_ref[:kmax] > floor
     dev = np.abs(err[keep] - err_ref[keep]) / err_ref[keep]
-    assert dev.max(initial=0.0) <= tol, f"max relative error deviation {dev.max():.3e}"
+    bar = np.full(dev.shape, tol)
+    if kappa:
+        bar = np.maximum(bar, np.finfo(float).eps * (norm_x / err_ref[keep]) ** 2)
+    assert np.all(dev <= bar), f"max relative error deviation {dev.max():.3e} (worst ratio {np.max(dev / bar):.2f})"
     assert np.max(np.abs(rec.factors.w - w_ref)) <= FACTOR_TOL * np.max(np.abs(w_ref))
     assert np.max(np.abs(rec.factors.h - h_ref)) <= FACTOR_TOL * np.max(np.abs(h_ref))
 
@@ -76,7 +91,7 @@ def test_c1_fast_mode_parity(ctx, golden, name):
     inp = golden.load("c1_inputs")
     g = golden.load(f"c1_{name}")
     rec = ctx.run(inp["x"], inp["w0"], inp["h0"], _cfg(name, 200), E.TimingMode.none)
-    assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]))
+    assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]), kappa="anls" in name)
 
 
 def test_c1_known_answer_fast(ctx, golden):
