@@ -102,6 +102,13 @@ struct enmf_gpu_ctx {
 
 namespace {
 
+template <int UB, int NW>
+void attrs_sweep_t();
+template <int NW>
+void attrs_sweep_rl();
+template <int NW>
+void attrs_sweep_la();
+
 void set_attrs_once() {
   static bool done = false;
   if (done) return;
@@ -123,9 +130,20 @@ void set_attrs_once() {
   big((const void*)hals::sweep_dmma<32>, hals::dmma_smem_bytes<32>());
   big((const void*)hals::sweep_dmma<64>, hals::dmma_smem_bytes<64>());
   big((const void*)hals::sweep_dmma<128>, hals::dmma_smem_bytes<128>());
-  big((const void*)hals::sweep_dmma_p<32>, hals::dmma_smem_bytes<32>());
-  big((const void*)hals::sweep_dmma_p<64>, hals::dmma_smem_bytes<64>());
-  big((const void*)hals::sweep_dmma_p<128>, hals::dmma_smem_bytes<128>());
+  big((const void*)hals::sweep_dmma_p<32, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<32>());
+  big((const void*)hals::sweep_dmma_p<64, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<64>());
+  big((const void*)hals::sweep_dmma_p<128, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<128>());
+  big((const void*)hals::sweep_dmma_p<32, 1, 12>, hals::dmma_smem_bytes<32>());
+  big((const void*)hals::sweep_dmma_p<64, 1, 12>, hals::dmma_smem_bytes<64>());
+  big((const void*)hals::sweep_dmma_p<128, 1, 12>, hals::dmma_smem_bytes<128>());
+  attrs_sweep_la<14>();
+  attrs_sweep_la<12>();
+  attrs_sweep_rl<14>();
+  attrs_sweep_rl<12>();
+  attrs_sweep_t<1, 14>();
+  attrs_sweep_t<2, 14>();
+  attrs_sweep_t<2, 12>();
+  attrs_sweep_t<4, 12>();
   big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
   big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
   done = true;
@@ -215,14 +233,102 @@ void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, lon
 // ---- inner solvers ------------------------------------------------------------
 // HALS sweep kernel variant: ENMF_HALS_KERNEL=fma selects the CUDA-core
 // register kernel (A/B comparisons); default is the DMMA blocked sweep.
-int hals_variant() {  // 0: persistent DMMA (default), 1: fma, 2: unrolled DMMA (v1)
+// 0: persistent DMMA, 14 warps (default); 1: fma; 2: unrolled DMMA (v1);
+// 3: persistent DMMA, 12 warps (168 registers, no spills)
+// 10..13: transposed-tile DMMA sweep (NW, UB) = (14,1), (14,2), (12,2), (12,4)
+int hals_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("ENMF_HALS_KERNEL");
     const std::string s = e ? e : "";
-    v = s == "fma" ? 1 : (s == "dmma1" ? 2 : 0);
+    v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
+      : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
+      : s == "la12" ? 31 : s == "la14" ? 30 : 11;  // default: t14u2 (fastest measured, r01)
   }
   return v;
+}
+
+template <int R_, int NW>
+void launch_sweep_la(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  constexpr int cols = NW * 8;
+  const int ntiles = (a.N + cols - 1) / cols;
+  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+  hals::sweep_la<R_, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
+}
+
+template <int NW>
+void launch_sweep_la_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  if (a.r <= 32) launch_sweep_la<32, NW>(c, s, a);
+  else if (a.r <= 64) launch_sweep_la<64, NW>(c, s, a);
+  else launch_sweep_la<128, NW>(c, s, a);
+}
+
+template <int NW>
+void attrs_sweep_la() {
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<32, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::dmma_smem_bytes<32>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<64, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::dmma_smem_bytes<64>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<128, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::dmma_smem_bytes<128>()));
+}
+
+template <int R_, int NW>
+void launch_sweep_rl(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  constexpr int cols = NW * 8;
+  const int ntiles = (a.N + cols - 1) / cols;
+  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+  hals::sweep_rl<R_, NW><<<grid, NW * 32, hals::rl_smem_bytes<R_>(), s>>>(a, ntiles);
+}
+
+template <int NW>
+void launch_sweep_rl_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  if (a.r <= 32) launch_sweep_rl<32, NW>(c, s, a);
+  else if (a.r <= 64) launch_sweep_rl<64, NW>(c, s, a);
+  else launch_sweep_rl<128, NW>(c, s, a);
+}
+
+template <int NW>
+void attrs_sweep_rl() {
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<32, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::rl_smem_bytes<32>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<64, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::rl_smem_bytes<64>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<128, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::rl_smem_bytes<128>()));
+}
+
+template <int R_, int UB, int NW>
+void launch_sweep_t(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  constexpr int cols = NW * 8;
+  const int ntiles = (a.N + cols - 1) / cols;
+  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+  hals::sweep_dmma_t<R_, UB, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
+}
+
+template <int UB, int NW>
+void launch_sweep_t_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  if (a.r <= 32) launch_sweep_t<32, UB, NW>(c, s, a);
+  else if (a.r <= 64) launch_sweep_t<64, UB, NW>(c, s, a);
+  else launch_sweep_t<128, UB, NW>(c, s, a);
+}
+
+template <int UB, int NW>
+void attrs_sweep_t() {
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<32, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::dmma_smem_bytes<32>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<64, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::dmma_smem_bytes<64>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<128, UB, NW>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, hals::dmma_smem_bytes<128>()));
+}
+
+template <int R_, int NW>
+void launch_sweep_p(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  constexpr int cols = NW * 8;
+  const int ntiles = (a.N + cols - 1) / cols;
+  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+  hals::sweep_dmma_p<R_, 1, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 bool hals_use_fma() { return hals_variant() == 1; }
 
@@ -253,16 +359,30 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     else if (r <= 64) SD(64);
     else SD(128);
 #undef SD
+  } else if (hals_variant() == 3) {
+    if (r <= 32) launch_sweep_p<32, 12>(c, s, a);
+    else if (r <= 64) launch_sweep_p<64, 12>(c, s, a);
+    else launch_sweep_p<128, 12>(c, s, a);
+  } else if (hals_variant() == 30) {
+    launch_sweep_la_r<14>(c, s, a);
+  } else if (hals_variant() == 31) {
+    launch_sweep_la_r<12>(c, s, a);
+  } else if (hals_variant() == 20) {
+    launch_sweep_rl_r<14>(c, s, a);
+  } else if (hals_variant() == 21) {
+    launch_sweep_rl_r<12>(c, s, a);
+  } else if (hals_variant() == 10) {
+    launch_sweep_t_r<1, 14>(c, s, a);
+  } else if (hals_variant() == 11) {
+    launch_sweep_t_r<2, 14>(c, s, a);
+  } else if (hals_variant() == 12) {
+    launch_sweep_t_r<2, 12>(c, s, a);
+  } else if (hals_variant() == 13) {
+    launch_sweep_t_r<4, 12>(c, s, a);
   } else {
-    constexpr int cols = hals::kDmmaWarps * 8;
-    const int ntiles = (a.N + cols - 1) / cols;
-    const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-#define SP(R_) \
-  hals::sweep_dmma_p<R_><<<grid, hals::kDmmaWarps * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles)
-    if (r <= 32) SP(32);
-    else if (r <= 64) SP(64);
-    else SP(128);
-#undef SP
+    if (r <= 32) launch_sweep_p<32, hals::kDmmaWarps>(c, s, a);
+    else if (r <= 64) launch_sweep_p<64, hals::kDmmaWarps>(c, s, a);
+    else launch_sweep_p<128, hals::kDmmaWarps>(c, s, a);
   }
   CUK();
   c->launches++;
