@@ -108,6 +108,8 @@ template <int NW>
 void attrs_sweep_rl();
 template <int NW>
 void attrs_sweep_la();
+template <int UB, int NW>
+void attrs_sweep_cv();
 
 void set_attrs_once() {
   static bool done = false;
@@ -136,6 +138,9 @@ void set_attrs_once() {
   big((const void*)hals::sweep_dmma_p<32, 1, 12>, hals::dmma_smem_bytes<32>());
   big((const void*)hals::sweep_dmma_p<64, 1, 12>, hals::dmma_smem_bytes<64>());
   big((const void*)hals::sweep_dmma_p<128, 1, 12>, hals::dmma_smem_bytes<128>());
+  attrs_sweep_cv<2, 14>();
+  attrs_sweep_cv<1, 14>();
+  attrs_sweep_cv<2, 12>();
   attrs_sweep_la<14>();
   attrs_sweep_la<12>();
   attrs_sweep_rl<14>();
@@ -243,9 +248,40 @@ int hals_variant() {
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
       : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : 11;  // default: t14u2 (fastest measured, r01)
+      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : 11;  // default t14u2
   }
   return v;
+}
+
+template <int R_, int UB, int NW, int MODE = 0>
+void launch_sweep_cv(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  constexpr int cols = NW * 8;
+  const int ntiles = (a.N + cols - 1) / cols;
+  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<R_, UB, NW, MODE>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, hals::cv_smem_bytes<R_>()));
+    attr = true;
+  }
+  hals::sweep_cv<R_, UB, NW, MODE><<<grid, NW * 32, hals::cv_smem_bytes<R_>(), s>>>(a, ntiles);
+}
+
+template <int UB, int NW>
+void launch_sweep_cv_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  if (a.r <= 32) launch_sweep_cv<32, UB, NW>(c, s, a);
+  else if (a.r <= 64) launch_sweep_cv<64, UB, NW>(c, s, a);
+  else launch_sweep_cv<128, UB, NW>(c, s, a);
+}
+
+template <int UB, int NW>
+void attrs_sweep_cv() {
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<32, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::cv_smem_bytes<32>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<64, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::cv_smem_bytes<64>()));
+  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<128, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          hals::cv_smem_bytes<128>()));
 }
 
 template <int R_, int NW>
@@ -363,6 +399,20 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     if (r <= 32) launch_sweep_p<32, 12>(c, s, a);
     else if (r <= 64) launch_sweep_p<64, 12>(c, s, a);
     else launch_sweep_p<128, 12>(c, s, a);
+  } else if (hals_variant() == 40) {
+    launch_sweep_cv_r<2, 14>(c, s, a);
+  } else if (hals_variant() == 41) {
+    launch_sweep_cv_r<1, 14>(c, s, a);
+  } else if (hals_variant() == 42) {
+    launch_sweep_cv_r<2, 12>(c, s, a);
+  } else if (hals_variant() == 43) {   // timing experiment: skeleton (no row chain; wrong results)
+    launch_sweep_cv<128, 2, 14, 1>(c, s, a);
+  } else if (hals_variant() == 44) {   // timing experiment: no phase barriers
+    launch_sweep_cv<128, 2, 14, 2>(c, s, a);
+  } else if (hals_variant() == 45) {   // timing experiment: per-phase clock64 profile into a.terms
+    launch_sweep_cv<128, 2, 14, 3>(c, s, a);
+  } else if (hals_variant() == 46) {   // timing experiment: same, one warp per CTA (no contention)
+    launch_sweep_cv<128, 2, 1, 3>(c, s, a);
   } else if (hals_variant() == 30) {
     launch_sweep_la_r<14>(c, s, a);
   } else if (hals_variant() == 31) {

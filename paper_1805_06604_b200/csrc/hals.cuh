@@ -697,7 +697,223 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_dmma_t(Args a, int ntiles) {
   last_block_reduce_n<NTH>(a, bg, nf, red);
 }
 
-// ---- look-ahead tensor-core sweep (default) ----------------------------------
+// ---- phase-convoy tensor-core sweep (default) --------------------------------
+//
+// Measured on B200 (tools/probe/contend_probe.cu, profiles/r01_notes.md): FP64
+// scalar instructions share the FP64 pipe with DMMA, and a dependent DADD/DMUL
+// waits ~16 cycles per DMMA-issuing warp on its SM sub-partition (8 -> 56
+// cycles with three).  The row-by-row block solve is a chain of such ops, so
+// interleaving it with other warps' DMMAs (all previous variants) stretches it
+// ~5×.  Here all warps of the CTA move in lock-step phases separated by
+// __syncthreads: every warp issues its block products (DMMA phase, pipe
+// saturated), then every warp solves its block (scalar phase, pipe free).
+// The solve chain is also shortened: the diagonal block's lower triangle
+// (diagonal included) is zeroed in the DMMA operand, so
+//     b_k = C_k - S_k - sum_{j<k in block} G_kj h_new_j
+// needs one DMUL + one DFMA per row on the chain, and max(t, 0) is an integer
+// compare (t > 0 exactly: 0 < bits(t) <= bits(+inf)).
+ENMF_DEV double pos_part(double t) {
+  const long long b = __double_as_longlong(t);
+  return (b > 0 && b <= 0x7FF0000000000000LL) ? t : 0.0;
+}
+
+template <int RMAX>
+constexpr int cv_smem_bytes() {
+  return RMAX * (RMAX + 4) * 8 + 2 * RMAX * 8 + (RMAX / 8) * 72 * 8;
+}
+
+// MODE (timing experiments only): 0 = normal, 1 = skeleton without the row
+// chain (wrong results), 2 = no phase barriers.
+template <int RMAX, int UB, int NW, int MODE = 0>
+__global__ void __launch_bounds__(NW * 32, 1) sweep_cv(Args a, int ntiles) {
+  constexpr int LDG = RMAX + 4;
+  constexpr int SL = RMAX / 4;
+  constexpr int NB = RMAX / 8;
+  constexpr int NTH = NW * 32;
+  static_assert(NB % UB == 0, "row blocks per group");
+  if (sweep_skipped(a)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* Gs = sm;                  // skewed G, diagonal blocks: strictly upper part only
+  double* Gd = sm + RMAX * LDG;
+  double* Gi = Gd + RMAX;
+  double* GL = Gi + RMAX;           // [NB][8][9]: strictly lower part of each diagonal block
+  __shared__ double red[NTH];
+
+  const int r = a.r;
+  for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
+    const int k = e / RMAX, c = e % RMAX;
+    const int j = (c + 8 * (k / 8)) & (RMAX - 1);
+    const double v = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
+    const bool diagblk = c < 8;      // rotated column c in [0, 8) <=> j in k's own block
+    Gs[k * LDG + c] = (diagblk && c <= (k & 7)) ? 0.0 : v;
+    if (diagblk) GL[(k >> 3) * 72 + (k & 7) * 9 + c] = (c < (k & 7)) ? v : 0.0;
+  }
+  for (int k = threadIdx.x; k < RMAX; k += NTH) {
+    const double d = k < r ? a.G[(long)k * r + k] : 1.0;
+    Gd[k] = d;
+    Gi[k] = __ddiv_rn(1.0, d);
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
+  double gain = 0.0;
+  int nf = 0;
+  const int sg0 = g * 4 + ((2 * t) & 3), sg1 = g * 4 + ((2 * t + 1) & 3);
+  const bool upper = t >= 2;
+  const int ss_lo = g * 4 + (t >> 1), ss_hi = g * 4 + 2 + (t >> 1);
+  const bool odd = t & 1;
+  long long prof[6] = {0, 0, 0, 0, 0, 0};   // MODE 3: dmma, bar1, scalar, bar2, tile-load, total
+  const long long tstart = (MODE == 3) ? clock64() : 0;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long col = ((long)tile * NW + warp) * 8 + g;
+    const bool valid = col < a.N;
+    long long tl0 = 0;
+    if (MODE == 3) tl0 = clock64();
+    double hreg[SL];
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      const int j = 4 * s + t;
+      hreg[s] = (valid && j < r) ? src[(long)j * a.ld + col] : 0.0;
+    }
+    const double* cp = a.C + col;
+    double cn0 = (valid && 2 * t < r) ? cp[(long)(2 * t) * a.ld] : 0.0;
+    double cn1 = (valid && 2 * t + 1 < r) ? cp[(long)(2 * t + 1) * a.ld] : 0.0;
+    if (MODE == 3) {
+      if (hreg[SL - 1] == 12345.678 || cn1 == 0.123) gain += 1.0;
+      prof[4] += clock64() - tl0;
+    }
+    const double* gbase = Gs + g * LDG + t;
+#pragma unroll 1
+    for (int q = 0; q < NB / UB; ++q) {
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int b = UB * q + u;
+        const int k0 = 8 * b;
+        const int ka = k0 + 2 * t;
+        const double cc0 = cn0, cc1 = cn1;
+        if (b + 1 < NB) {
+          cn0 = (valid && ka + 8 < r) ? cp[(long)(ka + 8) * a.ld] : 0.0;
+          cn1 = (valid && ka + 9 < r) ? cp[(long)(ka + 9) * a.ld] : 0.0;
+        }
+        long long tk0 = 0;
+        if (MODE == 3) tk0 = clock64();
+        // ---- DMMA phase ----
+        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        const double* gb = gbase + k0 * LDG;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) {
+          const int c = (4 * s - 8 * u + RMAX) & (RMAX - 1);
+          dmma884(acc[s & 3][0], acc[s & 3][1], hreg[s], gb[c]);
+        }
+        const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
+        const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
+        if (MODE == 3) {
+          // force completion of the products before reading the clock
+          if (S0 == 12345.678 && S1 == 0.5) gain += 1.0;
+          prof[0] += clock64() - tk0;
+        }
+        const double xa0 = __shfl_sync(0xffffffffu, hreg[2 * u], sg0);
+        const double xb0 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg0);
+        const double xa1 = __shfl_sync(0xffffffffu, hreg[2 * u], sg1);
+        const double xb1 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg1);
+        const double x0 = upper ? xb0 : xa0, x1 = upper ? xb1 : xa1;
+        double b0 = __dsub_rn(cc0, S0);
+        double b1 = __dsub_rn(cc1, S1);
+        const double* gl0 = GL + b * 72 + (2 * t) * 9;
+        const double* gl1 = gl0 + 9;
+        const double i00 = Gi[ka], i11 = Gi[ka + 1];
+        const double l10 = gl1[2 * t];    // G[ka+1][ka]
+        long long tk1 = 0;
+        if (MODE == 3) tk1 = clock64();
+        if (MODE != 2) __syncthreads();
+        long long tk2 = 0;
+        if (MODE == 3) {
+          tk2 = clock64();
+          prof[1] += tk2 - tk1;
+        }
+        // ---- scalar phase: rows k0..k0+7 in order, row k0+i in lane t = i/2 ----
+        double t0 = 0.0, t1 = 0.0, h0 = 0.0, h1 = 0.0;
+        if (MODE == 1) {
+          t0 = __dmul_rn(b0, i00); h0 = pos_part(t0);
+          t1 = __dmul_rn(b1, i11); h1 = pos_part(t1);
+        }
+#pragma unroll
+        for (int i = 0; i < (MODE == 1 ? 0 : 8); i += 2) {
+          const double tt0 = __dmul_rn(b0, i00);
+          const double hh0 = pos_part(tt0);
+          const double tt1 = __dmul_rn(fma(-l10, hh0, b1), i11);
+          const double hh1 = pos_part(tt1);
+          if (2 * t == i) {
+            t0 = tt0; h0 = hh0; t1 = tt1; h1 = hh1;
+          }
+          if (i < 6) {
+            const double e0 = __shfl_sync(0xffffffffu, hh0, g * 4 + i / 2);
+            const double e1 = __shfl_sync(0xffffffffu, hh1, g * 4 + i / 2);
+            if (2 * t > i) {
+              b0 = fma(-gl0[i], e0, b0);
+              b1 = fma(-gl1[i], e0, b1);
+              b0 = fma(-gl0[i + 1], e1, b0);
+              b1 = fma(-gl1[i + 1], e1, b1);
+            }
+          }
+        }
+        {
+          const double g00 = Gd[ka], g11 = Gd[ka + 1];
+          const double o0 = __dsub_rn(x0, t0), n0 = __dsub_rn(h0, t0);
+          const double o1 = __dsub_rn(x1, t1), n1 = __dsub_rn(h1, t1);
+          gain = fma(g00, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
+          gain = fma(g11, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
+        }
+        const double y0 = __shfl_sync(0xffffffffu, h0, ss_lo);
+        const double y1 = __shfl_sync(0xffffffffu, h1, ss_lo);
+        const double z0 = __shfl_sync(0xffffffffu, h0, ss_hi);
+        const double z1 = __shfl_sync(0xffffffffu, h1, ss_hi);
+        hreg[2 * u] = odd ? y1 : y0;
+        hreg[2 * u + 1] = odd ? z1 : z0;
+        long long tk3 = 0;
+        if (MODE == 3) {
+          if (hreg[2 * u] == 12345.678) gain += 1.0;
+          tk3 = clock64();
+          prof[2] += tk3 - tk2;
+        }
+        if (MODE != 2) __syncthreads();
+        if (MODE == 3) prof[3] += clock64() - tk3;
+      }
+      if (NB / UB > 1) {
+        double tmp[2 * UB];
+#pragma unroll
+        for (int s = 0; s < 2 * UB; ++s) tmp[s] = hreg[s];
+#pragma unroll
+        for (int s = 0; s + 2 * UB < SL; ++s) hreg[s] = hreg[s + 2 * UB];
+#pragma unroll
+        for (int s = 0; s < 2 * UB; ++s) hreg[SL - 2 * UB + s] = tmp[s];
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const int j = 4 * s + t;
+        if (j < r) {
+          a.H[(long)j * a.ld + col] = hreg[s];
+          nf |= !isfinite(hreg[s]);
+        }
+      }
+    }
+  }
+  if (MODE == 3 && lane == 0 && a.terms) {
+    prof[5] = clock64() - tstart;
+    double* o = a.terms + ((long)blockIdx.x * NW + warp) * 8;
+    for (int i = 0; i < 6; ++i) o[i] = (double)prof[i];
+  }
+  const double bg = block_reduce_sum_any(gain, red);
+  nf = __syncthreads_or(nf);
+  last_block_reduce_n<NTH>(a, bg, nf, red);
+}
+
+// ---- look-ahead tensor-core sweep ---------------------------------------------
 //
 // Left-looking blocked Gauss-Seidel (sweep_dmma_t layout: lane (g, t) owns rows
 // k0+2t, k0+2t+1 of column g in the block being solved) with a one-block
