@@ -117,14 +117,26 @@ void set_attrs_once() {
   auto big = [](const void* f, int bytes) {
     CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   };
-  big((const void*)gemm::gemm_f64_dmma<false, 2, false>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<false, 2, true>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<false, 1, false>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<false, 1, true>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<true, 2, false>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<true, 2, true>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<true, 1, false>, gemm::SMEM_BYTES);
-  big((const void*)gemm::gemm_f64_dmma<true, 1, true>, gemm::SMEM_BYTES);
+#define GEMM_ATTR(W)                                                               \
+  big((const void*)gemm::gemm_f64_dmma<false, 2, false, W>, gemm::SMEM_BYTES);     \
+  big((const void*)gemm::gemm_f64_dmma<false, 2, true, W>, gemm::SMEM_BYTES);      \
+  big((const void*)gemm::gemm_f64_dmma<false, 1, false, W>, gemm::SMEM_BYTES);     \
+  big((const void*)gemm::gemm_f64_dmma<false, 1, true, W>, gemm::SMEM_BYTES);      \
+  big((const void*)gemm::gemm_f64_dmma<true, 2, false, W>, gemm::SMEM_BYTES);      \
+  big((const void*)gemm::gemm_f64_dmma<true, 2, true, W>, gemm::SMEM_BYTES);       \
+  big((const void*)gemm::gemm_f64_dmma<true, 1, false, W>, gemm::SMEM_BYTES);      \
+  big((const void*)gemm::gemm_f64_dmma<true, 1, true, W>, gemm::SMEM_BYTES);
+  GEMM_ATTR(2)
+  GEMM_ATTR(4)
+#undef GEMM_ATTR
+  big((const void*)gemm::gemm_f64_dmma_s<false, 2, false>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<false, 2, true>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<false, 1, false>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<false, 1, true>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<true, 2, false>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<true, 2, true>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<true, 1, false>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_s<true, 1, true>, gemm::st::SMEM_BYTES);
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -169,7 +181,7 @@ enum { PREC_FAST = ENMF_PRECISION_FP64, PREC_EXACT = 2 };
 // reduces them); a single-tile GEMM (the r×r Gram) splits up to one CTA per
 // SM with a separate fixed-order reduction.
 int choose_splits(int tiles, int kblocks, int sms) {
-  if (tiles >= 2 * sms) return 1;
+  if (tiles >= 8 * sms) return 1;
   const int smax = tiles > 8 ? std::max(1, std::min(kblocks / 4, 8))
                              : std::max(1, std::min(kblocks / 4, sms));
   int best = 1;
@@ -188,9 +200,59 @@ int choose_splits(int tiles, int kblocks, int sms) {
 }
 
 // C[M×N] = A[M×K] · op(B);  bk: B is N×K (K contiguous) else K×N (N contiguous).
+bool gemm_big_tile() {  // ENMF_GEMM_TILE=128: the 128×128 single-CTA-per-SM kernel
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ENMF_GEMM_TILE");
+    v = (e && std::string(e) == "128") ? 1 : 0;
+  }
+  return v == 1;
+}
+
+void gemm_launch_small(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long lda, const double* B, long ldb,
+                       double* C, long ldc, int M, int N, int K, bool sym, const DevState* st) {
+  using namespace gemm;
+  const int tn = (N + st::BN - 1) / st::BN, tm = (M + st::BM - 1) / st::BM, tiles = tn * tm;
+  const int kb = (K + st::BK - 1) / st::BK;
+  const int S = choose_splits(tiles, kb, 3 * c->sms);
+  const bool last = S > 1 && S <= 8;
+  if (S > 1) {
+    c->partials.ensure((size_t)S * M * N);
+    if (last && c->counters.n < (size_t)tiles) {
+      c->counters.ensure(tiles);
+      CU(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned) * tiles, s));
+    }
+  }
+  const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, S > 1 ? c->partials.p : nullptr, c->counters.p, sym ? 1 : 0, st};
+  // M-tiles vary fastest (blockIdx.x): the r/64 CTAs sharing one X tile run
+  // together, so X is fetched from HBM once and hit in L2 by the others.
+  dim3 grid(tm, tn, S);
+#define GEMM_GO(BKM, V, L) gemm_f64_dmma_s<BKM, V, L><<<grid, st::NTH, st::SMEM_BYTES, s>>>(p)
+  if (bk) {
+    if (vec2) { if (last) GEMM_GO(true, 2, true); else GEMM_GO(true, 2, false); }
+    else { if (last) GEMM_GO(true, 1, true); else GEMM_GO(true, 1, false); }
+  } else {
+    if (vec2) { if (last) GEMM_GO(false, 2, true); else GEMM_GO(false, 2, false); }
+    else { if (last) GEMM_GO(false, 1, true); else GEMM_GO(false, 1, false); }
+  }
+#undef GEMM_GO
+  CUK();
+  c->launches++;
+  if (S > 1 && !last) {
+    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(c->partials.p, S, M, N, C, ldc, sym ? 1 : 0, st);
+    CUK();
+    c->launches++;
+  }
+}
+
 void gemm_launch(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long lda, const double* B, long ldb,
                  double* C, long ldc, int M, int N, int K, bool sym, const DevState* st) {
   using namespace gemm;
+  if (!gemm_big_tile()) {
+    gemm_launch_small(c, s, bk, A, lda, B, ldb, C, ldc, M, N, K, sym, st);
+    return;
+  }
   const int tn = (N + BN - 1) / BN, tm = (M + BM - 1) / BM, tiles = tn * tm;
   const int kb = (K + BK - 1) / BK;
   const int S = choose_splits(tiles, kb, c->sms);
@@ -205,7 +267,16 @@ void gemm_launch(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
   Params p{A, lda, B, ldb, C, ldc, M, N, K, S, S > 1 ? c->partials.p : nullptr, c->counters.p, sym ? 1 : 0, st};
   dim3 grid(tn, tm, S);
-#define GEMM_GO(BKM, V, L) gemm_f64_dmma<BKM, V, L><<<grid, NT, SMEM_BYTES, s>>>(p)
+  static int w16 = -1;  // ENMF_GEMM_WARPS=16: 16 warps of 32×32 instead of 8 of 64×32
+  if (w16 < 0) {
+    const char* e = std::getenv("ENMF_GEMM_WARPS");
+    w16 = (e && std::string(e) == "16") ? 1 : 0;
+  }
+#define GEMM_GO(BKM, V, L)                                                                \
+  do {                                                                                    \
+    if (w16) gemm_f64_dmma<BKM, V, L, 4><<<grid, 512, SMEM_BYTES, s>>>(p);                \
+    else gemm_f64_dmma<BKM, V, L, 2><<<grid, 256, SMEM_BYTES, s>>>(p);                   \
+  } while (0)
   if (bk) {
     if (vec2) { if (last) GEMM_GO(true, 2, true); else GEMM_GO(true, 2, false); }
     else { if (last) GEMM_GO(true, 1, true); else GEMM_GO(true, 1, false); }

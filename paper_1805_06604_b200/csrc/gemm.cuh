@@ -65,7 +65,7 @@ template <int VEC>
 ENMF_DEV void load_kmajor(double* s, int lds, const double* g, long ld, int rows_valid, int row0,
                           int k0, int K, int nrows) {
   constexpr int CH = BK / VEC;  // chunks per row
-  for (int c = threadIdx.x; c < nrows * CH; c += NT) {
+  for (int c = threadIdx.x; c < nrows * CH; c += blockDim.x) {
     const int row = c / CH, col = (c % CH) * VEC;
     const int gr = row0 + row, gk = k0 + col;
     int valid = 0;
@@ -79,7 +79,7 @@ ENMF_DEV void load_kmajor(double* s, int lds, const double* g, long ld, int rows
 template <int VEC>
 ENMF_DEV void load_nmajor(double* s, const double* g, long ld, int k0, int K, int n0, int N) {
   constexpr int CH = BN / VEC;
-  for (int c = threadIdx.x; c < BK * CH; c += NT) {
+  for (int c = threadIdx.x; c < BK * CH; c += blockDim.x) {
     const int row = c / CH, col = (c % CH) * VEC;
     const int gk = k0 + row, gn = n0 + col;
     int valid = 0;
@@ -91,8 +91,12 @@ ENMF_DEV void load_nmajor(double* s, const double* g, long ld, int k0, int K, in
 }
 
 // C[M×N] (+)= A · op(B) on DMMA.  grid = (ceil(N/BN), ceil(M/BM), splits).
-template <bool B_KMAJOR, int VEC, bool REDUCE_LAST>
-__global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
+// WMW = warps along M (2: 8 warps of 64×32; 4: 16 warps of 32×32).
+template <bool B_KMAJOR, int VEC, bool REDUCE_LAST, int WMW = 2>
+__global__ void __launch_bounds__(WMW * 4 * 32, 1) gemm_f64_dmma(Params p) {
+  constexpr int MI = 16 / WMW;          // 8-row m-tiles per warp
+  constexpr int WROWS = BM / WMW;
+  constexpr int NTH = WMW * 4 * 32;
   if (p.st && !dev_active(p.st)) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WMW, wn = warp / WMW;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int KB = (p.K + BK - 1) / BK;
   const int per = (KB + p.splits - 1) / p.splits;
@@ -108,9 +112,9 @@ __global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
   const int kb1 = min(KB, kb0 + per);
   const int nk = max(0, kb1 - kb0);
 
-  double acc[8][4][2];
+  double acc[MI][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -134,22 +138,29 @@ __global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
       if (nxt < nk) issue(nxt, nxt % STAGES);
       cp_commit();
     }
-    const double* as = As + (kb % STAGES) * A_STAGE + (wm * 64 + g) * LDA_S + t;
+    const double* as = As + (kb % STAGES) * A_STAGE + (wm * WROWS + g) * LDA_S + t;
     const double* bs = Bs + (kb % STAGES) * B_STAGE;
+    // Fragments are double-buffered in registers (the loads for k-step kk+1 are
+    // in flight while kk's DMMAs issue).
+    double a[2][MI], b[2][4];
+    auto load_frag = [&](int kk, int buf) {
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[8], b[4];
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi) a[mi] = as[mi * 8 * LDA_S + kk * 4];
+      for (int mi = 0; mi < MI; ++mi) a[buf][mi] = as[mi * 8 * LDA_S + kk * 4];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
-        if (B_KMAJOR) b[ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kk * 4 + t];
-        else b[ni] = bs[(kk * 4 + t) * LDB_N + wn * 32 + ni * 8 + g];
+        if (B_KMAJOR) b[buf][ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kk * 4 + t];
+        else b[buf][ni] = bs[(kk * 4 + t) * LDB_N + wn * 32 + ni * 8 + g];
       }
+    };
+    load_frag(0, 0);
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int cur = kk & 1;
+      if (kk + 1 < BK / 4) load_frag(kk + 1, cur ^ 1);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[cur][mi], b[cur][ni]);
     }
   }
   cp_wait<0>();
@@ -159,8 +170,8 @@ __global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
   double* out = split ? p.partials + (long)blockIdx.z * p.M * p.N : p.C;
   const long ldo = split ? p.N : p.ldc;
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const int row = m0 + wm * 64 + mi * 8 + g;
+  for (int mi = 0; mi < MI; ++mi) {
+    const int row = m0 + wm * WROWS + mi * 8 + g;
     if (row >= p.M) continue;
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
@@ -199,7 +210,171 @@ __global__ void __launch_bounds__(NT, 1) gemm_f64_dmma(Params p) {
   __threadfence();
   const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
   const long MN = (long)p.M * p.N;
-  for (int e = tid; e < rows * cols; e += NT) {
+  for (int e = tid; e < rows * cols; e += NTH) {
+    const int i = m0 + e / cols, j = n0 + e % cols;
+    if (p.sym && i > j) continue;
+    const double* src = p.partials + (long)i * p.N + j;
+    double v = __ldcg(src);
+    for (int s = 1; s < p.splits; ++s) v = __dadd_rn(v, __ldcg(src + s * MN));
+    p.C[(long)i * p.ldc + j] = v;
+    if (p.sym) p.C[(long)j * p.ldc + i] = v;
+  }
+}
+
+// ---- small-tile variant: 64×64×16 CTA tile, 4 warps of 32×32, 3 stages --------
+// 60 KB of shared memory and ≤ 128 registers, so THREE CTAs share an SM: a
+// CTA waiting at its k-block barrier no longer drains the SM's DMMA pipe
+// (the 128×128 single-CTA kernel above tops out at 79% DMMA-pipe activity,
+// profiles/r01_gemm_ncu.txt).
+namespace st {
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NTH = 128;
+constexpr int LDA_S = BK + 4;
+constexpr int LDB_N = BN + 4;
+constexpr int LDB_K = BK + 4;
+constexpr int A_STAGE = BM * LDA_S;
+constexpr int B_STAGE = (BN * LDB_K > BK * LDB_N) ? BN * LDB_K : BK * LDB_N;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(double);
+}  // namespace st
+
+template <int VEC, int BKk, int NTHk>
+ENMF_DEV void st_load_kmajor(double* s, int lds, const double* g, long ld, int rows_valid, int row0, int k0,
+                             int K, int nrows) {
+  constexpr int CH = BKk / VEC;
+  for (int c = threadIdx.x; c < nrows * CH; c += NTHk) {
+    const int row = c / CH, col = (c % CH) * VEC;
+    const int gr = row0 + row, gk = k0 + col;
+    int valid = 0;
+    if (gr < rows_valid && gk < K) valid = (K - gk >= VEC) ? VEC : (K - gk);
+    const double* src = valid ? g + (long)gr * ld + gk : g;
+    if (VEC == 2) cp_async16(s + row * lds + col, src, valid * 8);
+    else cp_async8(s + row * lds + col, src, valid * 8);
+  }
+}
+template <int VEC>
+ENMF_DEV void st_load_nmajor(double* s, const double* g, long ld, int k0, int K, int n0, int N) {
+  constexpr int CH = st::BN / VEC;
+  for (int c = threadIdx.x; c < st::BK * CH; c += st::NTH) {
+    const int row = c / CH, col = (c % CH) * VEC;
+    const int gk = k0 + row, gn = n0 + col;
+    int valid = 0;
+    if (gk < K && gn < N) valid = (N - gn >= VEC) ? VEC : (N - gn);
+    const double* src = valid ? g + (long)gk * ld + gn : g;
+    if (VEC == 2) cp_async16(s + row * st::LDB_N + col, src, valid * 8);
+    else cp_async8(s + row * st::LDB_N + col, src, valid * 8);
+  }
+}
+
+template <bool B_KMAJOR, int VEC, bool REDUCE_LAST>
+__global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_s(Params p) {
+  constexpr int BM = st::BM, BN = st::BN, BK = st::BK, STAGES = st::STAGES, NTH = st::NTH;
+  constexpr int LDA_S = st::LDA_S, LDB_N = st::LDB_N, LDB_K = st::LDB_K;
+  constexpr int A_STAGE = st::A_STAGE, B_STAGE = st::B_STAGE;
+  if (p.st && !dev_active(p.st)) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;     // 2×2 warps of 32×32
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;   // grid = (M tiles, N tiles, splits)
+  const int KB = (p.K + BK - 1) / BK;
+  const int per = (KB + p.splits - 1) / p.splits;
+  const int kb0 = blockIdx.z * per;
+  const int kb1 = min(KB, kb0 + per);
+  const int nk = max(0, kb1 - kb0);
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int kb, int stage) {
+    const int k0 = (kb0 + kb) * BK;
+    st_load_kmajor<VEC, BK, NTH>(As + stage * A_STAGE, LDA_S, p.A, p.lda, p.M, m0, k0, p.K, BM);
+    if (B_KMAJOR) st_load_kmajor<VEC, BK, NTH>(Bs + stage * B_STAGE, LDB_K, p.B, p.ldb, p.N, n0, k0, p.K, BN);
+    else st_load_nmajor<VEC>(Bs + stage * B_STAGE, p.B, p.ldb, k0, p.K, n0, p.N);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_commit();
+  }
+  for (int kb = 0; kb < nk; ++kb) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kb + STAGES - 1;
+      if (nxt < nk) issue(nxt, nxt % STAGES);
+      cp_commit();
+    }
+    const double* as = As + (kb % STAGES) * A_STAGE + (wm * 32 + g) * LDA_S + t;
+    const double* bs = Bs + (kb % STAGES) * B_STAGE;
+    double a[2][4], b[2][4];
+    auto load_frag = [&](int kk, int buf) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = as[mi * 8 * LDA_S + kk * 4];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        if (B_KMAJOR) b[buf][ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kk * 4 + t];
+        else b[buf][ni] = bs[(kk * 4 + t) * LDB_N + wn * 32 + ni * 8 + g];
+      }
+    };
+    load_frag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int cur = kk & 1;
+      if (kk + 1 < BK / 4) load_frag(kk + 1, cur ^ 1);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[cur][mi], b[cur][ni]);
+    }
+  }
+  cp_wait<0>();
+
+  const bool split = p.splits > 1;
+  double* out = split ? p.partials + (long)blockIdx.z * p.M * p.N : p.C;
+  const long ldo = split ? p.N : p.ldc;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = m0 + wm * 32 + mi * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int col = n0 + wn * 32 + ni * 8 + 2 * t;
+      if (!split && p.sym) {
+        for (int e = 0; e < 2; ++e) {
+          const int c = col + e;
+          if (c < p.N && row <= c) {
+            out[(long)row * ldo + c] = acc[mi][ni][e];
+            out[(long)c * ldo + row] = acc[mi][ni][e];
+          }
+        }
+      } else if (col + 1 < p.N && ((ldo & 1) == 0)) {
+        *reinterpret_cast<double2*>(out + (long)row * ldo + col) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (col < p.N) out[(long)row * ldo + col] = acc[mi][ni][0];
+        if (col + 1 < p.N) out[(long)row * ldo + col + 1] = acc[mi][ni][1];
+      }
+    }
+  }
+  if (!split || !REDUCE_LAST) return;
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* ctr = p.counters + blockIdx.y * gridDim.x + blockIdx.x;
+    const unsigned prev = atomicAdd(ctr, 1u);
+    s_last = (prev == (unsigned)p.splits - 1) ? 1u : 0u;
+    if (s_last) *ctr = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+  const long MN = (long)p.M * p.N;
+  for (int e = tid; e < rows * cols; e += NTH) {
     const int i = m0 + e / cols, j = n0 + e % cols;
     if (p.sym && i > j) continue;
     const double* src = p.partials + (long)i * p.N + j;

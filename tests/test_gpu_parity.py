@@ -65,8 +65,15 @@ def assert_parity(rec, err_ref, restarted_ref, w_ref, h_ref, norm_x, tol=REL_ERR
     if kappa:
         bar = np.maximum(bar, np.finfo(float).eps * (norm_x / err_ref[keep]) ** 2)
     assert np.all(dev <= bar), f"max relative error deviation {dev.max():.3e} (worst ratio {np.max(dev / bar):.2f})"
-    assert np.max(np.abs(rec.factors.w - w_ref)) <= FACTOR_TOL * np.max(np.abs(w_ref))
-    assert np.max(np.abs(rec.factors.h - h_ref)) <= FACTOR_TOL * np.max(np.abs(h_ref))
+    if kmax == len(err_ref):
+        assert np.max(np.abs(rec.factors.w - w_ref)) <= FACTOR_TOL * np.max(np.abs(w_ref))
+        assert np.max(np.abs(rec.factors.h - h_ref)) <= FACTOR_TOL * np.max(np.abs(h_ref))
+    else:
+        # Below the noise floor restart decisions are rounding noise, and an exact
+        # factorization (noise-free low-rank data) is not unique: compare what the
+        # trajectory determines, the reconstruction W·H, within 1e-6·||X||.
+        wh, wh_ref = rec.factors.w @ rec.factors.h, w_ref @ h_ref
+        assert np.linalg.norm(wh - wh_ref) <= FACTOR_TOL * norm_x
 
 
 def assert_bitwise(rec, g):
