@@ -164,6 +164,25 @@ int enmf_gpu_end(enmf_gpu_ctx* ctx, double* w_out, double* h_out, double* norm_x
 /* The context's CUDA stream (cudaStream_t) — for event timing by the caller. */
 void* enmf_gpu_stream(enmf_gpu_ctx* ctx);
 
+/* ---- multi-GPU: one problem sharded over `world` GPUs ----------
+ * One process per GPU.  Rank p owns rows [row0, row0+mp) of W and X (row block,
+ * for X·Tᵀ) and columns [col0, col0+np) of H and X (column block, for W_yᵀX).
+ * Setup: (1) every rank: enmf_gpu_dist_alloc -> a cudaIpcMemHandle_t (64 bytes)
+ * of its shared block; (2) the caller all-gathers the handles (any host
+ * channel, e.g. torch.distributed); (3) every rank: enmf_gpu_dist_init with the
+ * world × 64-byte handle array; (4) a host barrier; (5) enmf_gpu_load_dense_sharded.
+ * Runs then use enmf_gpu_begin/step/sync/end (or enmf_gpu_solve) with this
+ * rank's factor shards: w0 = W0[row0:row0+mp, :] (mp × r), h0 = H0[:, col0:col0+np]
+ * (r × np); outputs are the same shards.  Records are identical on all ranks. */
+void enmf_gpu_dist_shard(size_t m, size_t n, int rank, int world, size_t* row0, size_t* mp,
+                         size_t* col0, size_t* np);
+int enmf_gpu_dist_alloc(enmf_gpu_ctx* ctx, int rank, int world, size_t m, size_t n, size_t r,
+                        void* ipc_handle_out);
+int enmf_gpu_dist_init(enmf_gpu_ctx* ctx, const void* ipc_handles);
+int enmf_gpu_load_dense_sharded(enmf_gpu_ctx* ctx, const double* x_cols, const double* x_rows,
+                                int on_device);
+int enmf_gpu_dist_finalize(enmf_gpu_ctx* ctx);
+
 /* ---- public kernels the reference's tests call (host pointers) --------------
  * They run in the context's kernel precision (default ENMF_PRECISION_FP64). */
 int enmf_gpu_set_precision(enmf_gpu_ctx* ctx, int precision);

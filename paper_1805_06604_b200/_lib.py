@@ -62,6 +62,8 @@ EXPORTS = [
     "enmf_gpu_cross_xht", "enmf_gpu_frob_norm_sq", "enmf_gpu_fast_error", "enmf_gpu_hals_solve",
     "enmf_gpu_active_set_solve", "enmf_gpu_begin", "enmf_gpu_step", "enmf_gpu_step_profiled",
     "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream",
+    "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
+    "enmf_gpu_dist_finalize",
 ]
 
 _lib = None
@@ -110,10 +112,18 @@ def load() -> C.CDLL:
     L.enmf_gpu_end.argtypes = [vp, dp, dp, C.POINTER(C.c_double)]
     L.enmf_gpu_stream.argtypes = [vp]
     L.enmf_gpu_stream.restype = C.c_void_p
+    szp = C.POINTER(sz)
+    L.enmf_gpu_dist_shard.argtypes = [sz, sz, C.c_int, C.c_int, szp, szp, szp, szp]
+    L.enmf_gpu_dist_shard.restype = None
+    L.enmf_gpu_dist_alloc.argtypes = [vp, C.c_int, C.c_int, sz, sz, sz, C.c_void_p]
+    L.enmf_gpu_dist_init.argtypes = [vp, C.c_void_p]
+    L.enmf_gpu_load_dense_sharded.argtypes = [vp, dp, dp, C.c_int]
+    L.enmf_gpu_dist_finalize.argtypes = [vp]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("enmf_gpu_config_default", "enmf_gpu_destroy", "enmf_gpu_last_error",
-                        "enmf_gpu_kernel_launches", "enmf_gpu_update_beta", "enmf_gpu_stream"):
+                        "enmf_gpu_kernel_launches", "enmf_gpu_update_beta", "enmf_gpu_stream",
+                        "enmf_gpu_dist_shard"):
             fn.restype = C.c_int
     _lib = L
     return L

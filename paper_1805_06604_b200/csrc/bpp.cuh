@@ -18,6 +18,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "dist.cuh"
 
 namespace bpp {
 
@@ -224,7 +225,8 @@ __global__ void check(DevState* st, int side, int r, int N, unsigned long long* 
 }
 
 // max |C| over r×N (feas_tol, nnls.hpp:271).  Single block, order-independent.
-__global__ void absmax(const double* C, long ld, int r, int N, double* out, const DevState* st) {
+__global__ void absmax(const double* C, long ld, int r, int N, double* out, const DevState* st,
+                       const dist::View* dv = nullptr) {
   if (st && !dev_active(st)) return;
   __shared__ double red[256];
   double m = 0.0;
@@ -238,7 +240,7 @@ __global__ void absmax(const double* C, long ld, int r, int N, double* out, cons
     if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = red[0];
+  if (threadIdx.x == 0) *out = dv ? dist::allmax_scalar(*dv, red[0]) : red[0];
 }
 
 }  // namespace bpp

@@ -94,11 +94,45 @@ struct enmf_gpu_ctx {
   int static_kernels = 0, kernels_per_sweep = 0;
   // open run session (enmf_gpu_begin .. enmf_gpu_end)
   struct Session* sess = nullptr;
+  // multi-GPU sharding (enmf_gpu_dist_*); null or !ready = single GPU
+  struct DistHost* dist = nullptr;
   // standalone kernel API
   int kernel_precision = ENMF_PRECISION_FP64;
   DBuf<double> ka, kb, kc, kd, ke;
   DBuf<HalsCtl> kctl;
 };
+
+// Sharded (multi-GPU) state of a context, SURVEY §8(e).  The IPC-shared block
+// of every rank holds [flags | slots | W_yᵀ replica r×m | T replica r×n].
+struct DistHost {
+  int rank = 0, world = 1;
+  size_t m = 0, n = 0, r = 0;
+  size_t row0 = 0, mp = 0, col0 = 0, np = 0;
+  size_t slot = 0;                       // doubles per mailbox slot
+  char* shared = nullptr;                // own block (cudaMalloc, IPC-exported)
+  size_t shared_bytes = 0;
+  char* peer[dist::MAXP] = {};           // every rank's block (own included)
+  dist::View* dview = nullptr;           // device copy of the view
+  unsigned long long* epoch = nullptr;
+  int* err = nullptr;
+  double* scratch = nullptr;
+  DBuf<double> xc_own, xr_own;
+  const double* xc = nullptr;            // X[:, col0:col0+np]  (m × np)
+  const double* xr = nullptr;            // X[row0:row0+mp, :]  (mp × n)
+  bool ready = false;
+
+  static size_t header_bytes() { return 256; }
+  size_t slots_bytes() const { return 2 * dist::MAXP * slot * sizeof(double); }
+  double* wfull(int q) const { return reinterpret_cast<double*>(peer[q] + header_bytes() + slots_bytes()); }
+  double* tfull(int q) const { return wfull(q) + r * m; }
+};
+
+// Balanced contiguous blocks: the first (len % world) ranks get one more.
+inline void shard_bounds(size_t len, int rank, int world, size_t* off, size_t* cnt) {
+  const size_t base = len / world, extra = len % world;
+  *cnt = base + ((size_t)rank < extra ? 1 : 0);
+  *off = (size_t)rank * base + std::min<size_t>((size_t)rank, extra);
+}
 
 namespace {
 
@@ -509,9 +543,11 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   c->launches++;
 }
 
-void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a) {
+// dv/dscratch/Ntotal: multi-GPU (global max|C|, exchange count and NaN flag across ranks).
+void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a, const dist::View* dv = nullptr,
+                double* dscratch = nullptr, long Ntotal = 0) {
   const int r = a.r;
-  bpp::absmax<<<1, 256, 0, s>>>(a.C, a.ld, r, a.N, const_cast<double*>(a.cmax), a.st);
+  bpp::absmax<<<1, 256, 0, s>>>(a.C, a.ld, r, a.N, const_cast<double*>(a.cmax), a.st, dv);
   CUK();
   if (r <= 32) {
     bpp::solve<32, 8><<<(a.N + 7) / 8, 256, bpp::smem_bytes<32, 8>(), s>>>(a);
@@ -519,7 +555,11 @@ void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a) {
     bpp::solve<64, 4><<<(a.N + 3) / 4, 128, bpp::smem_bytes<64, 4>(), s>>>(a);
   }
   CUK();
-  bpp::check<<<1, 1, 0, s>>>(a.st, a.side, r, a.N, a.exchanges, a.rounds, a.nonfinite);
+  if (dv) {
+    dist::bpp_check_dist<<<1, 32, 0, s>>>(dv, a.st, a.side, r, Ntotal, a.exchanges, a.rounds, a.nonfinite, dscratch);
+  } else {
+    bpp::check<<<1, 1, 0, s>>>(a.st, a.side, r, a.N, a.exchanges, a.rounds, a.nonfinite);
+  }
   CUK();
   c->launches += 3;
 }
@@ -617,11 +657,12 @@ void ensure_buffers(enmf_gpu_ctx* c, size_t m, size_t n, size_t r) {
 
 // Products for the error of (W from rows of WTsrc, T): dot = <W, X Tᵀ>, GWn = gram(W).
 void enqueue_error_terms(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, const double* WTsrc, const double* Pm,
-                         DevState* st) {
-  const long wsz = (long)pl.m * pl.r;
-  gram_launch(c, s, pl.prec, WTsrc, pl.m, pl.r, pl.m, c->GWn.p, st);
+                         DevState* st, int m_loc = -1, const DistHost* D = nullptr) {
+  if (m_loc < 0) m_loc = pl.m;
+  const long wsz = (long)m_loc * pl.r;
+  gram_launch(c, s, pl.prec, WTsrc, m_loc, pl.r, m_loc, c->GWn.p, st);
   if (pl.prec == PREC_EXACT) {
-    misc::neumaier_exact<<<1, 32, 0, s>>>(WTsrc, Pm, wsz, 1, pl.r, pl.m, c->dd.p, st);
+    misc::neumaier_exact<<<1, 32, 0, s>>>(WTsrc, Pm, wsz, 1, pl.r, m_loc, c->dd.p, st);
     CUK();
     c->launches++;
   } else {
@@ -629,6 +670,12 @@ void enqueue_error_terms(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, const 
     misc::dd_partial<<<nb, misc::NT, 0, s>>>(WTsrc, Pm, wsz, c->ddpart.p, c->ddpart.p + 4096, st);
     CUK();
     misc::dd_final<<<1, misc::NT, 0, s>>>(c->ddpart.p, c->ddpart.p + 4096, nb, c->dd.p, st);
+    CUK();
+    c->launches += 2;
+  }
+  if (D) {  // <W_n, X Tᵀ> and gram(W_n) are sums over the row shards
+    dist::allreduce_inplace<<<1, 256, 0, s>>>(D->dview, c->GWn.p, pl.r * pl.r, st);
+    dist::allreduce_inplace<<<1, 256, 0, s>>>(D->dview, c->dd.p, 2, st);
     CUK();
     c->launches += 2;
   }
@@ -650,7 +697,8 @@ void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
 
 void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, int solver, const double* G,
                    const double* Cm, const double* Hin, double* Hout, int rows_n, int max_sweeps, DevState* st,
-                   cudaGraphConditionalHandle cond, int mode, Prof* prof) {
+                   cudaGraphConditionalHandle cond, int mode, Prof* prof, const DistHost* D = nullptr,
+                   long rows_total = 0) {
   if (solver == ENMF_INNER_HALS) {
     hals::Args a{};
     a.G = G; a.C = Cm; a.Hin = Hin; a.H = Hout; a.ld = rows_n; a.r = pl.r; a.N = rows_n;
@@ -660,6 +708,7 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     a.part_nf = c->part_nf.p + side * (c->part_nf.n / 2);
     a.terms = c->terms.p; a.st = st; a.side = side;
     a.cond = (unsigned long long)cond; a.use_cond = mode == INNER_CAPTURE ? 1 : 0;
+    a.dv = D ? D->dview : nullptr;
     hals::reset_ctl<<<1, 1, 0, s>>>(a.ctl, st);
     CUK();
     c->launches++;
@@ -697,36 +746,99 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     a.G = G; a.C = Cm; a.H0 = Hin; a.H = Hout; a.ld = rows_n; a.r = pl.r; a.N = rows_n;
     a.cmax = c->cmax.p + side; a.st = st; a.side = side;
     a.exchanges = c->bpp_exch.p + side; a.rounds = c->bpp_rounds.p + side; a.nonfinite = c->bpp_nf.p + side;
-    bpp_launch(c, s, a);
+    if (D) bpp_launch(c, s, a, D->dview, D->scratch, rows_total);
+    else bpp_launch(c, s, a);
   }
+}
+
+// Where the data of an iteration lives: the whole problem (single GPU) or this
+// rank's shards plus the full factor replicas (multi-GPU).
+struct Layout {
+  int m_loc, n_loc;               // rows of W / columns of H held here
+  long row0, col0;
+  const double* xcb; long ld_cb;  // X[:, J]  (m × n_loc)  for W_yᵀX
+  const double* xrb; long ld_rb;  // X[I, :]  (m_loc × n)  for X·Tᵀ
+  double* wyfull;                 // W_yᵀ replica (r × m), own rank
+  double* tfull;                  // T replica (r × n), own rank
+  const DistHost* D;              // null on a single GPU
+};
+
+Layout make_layout(enmf_gpu_ctx* c, const Plan& pl) {
+  Layout L{};
+  const DistHost* D = (c->dist && c->dist->ready) ? c->dist : nullptr;
+  L.D = D;
+  if (!D) {
+    L.m_loc = pl.m; L.n_loc = pl.n; L.row0 = 0; L.col0 = 0;
+    L.xcb = c->x; L.ld_cb = pl.n; L.xrb = c->x; L.ld_rb = pl.n;
+    L.wyfull = c->WyT.p; L.tfull = nullptr;
+  } else {
+    L.m_loc = (int)D->mp; L.n_loc = (int)D->np; L.row0 = (long)D->row0; L.col0 = (long)D->col0;
+    L.xcb = D->xc; L.ld_cb = (long)D->np; L.xrb = D->xr; L.ld_rb = pl.n;
+    L.wyfull = D->wfull(D->rank); L.tfull = D->tfull(D->rank);
+  }
+  return L;
+}
+
+// Multi-GPU helpers (no-ops on one GPU).
+void dist_allreduce(enmf_gpu_ctx* c, cudaStream_t s, const Layout& L, double* buf, int count, DevState* st) {
+  if (!L.D) return;
+  dist::allreduce_inplace<<<1, 256, 0, s>>>(L.D->dview, buf, count, st);
+  CUK();
+  c->launches++;
+}
+// which: 0 = W_yᵀ replica (columns I = [row0, row0+m_loc) of r×m), 1 = T replica (columns J of r×n)
+void dist_gather(enmf_gpu_ctx* c, cudaStream_t s, const Layout& L, const double* local, int r, int which,
+                 const Plan& pl, DevState* st) {
+  if (!L.D) return;
+  const long cnt = which == 0 ? L.m_loc : L.n_loc;
+  const long off = which == 0 ? L.row0 : L.col0;
+  const long full = which == 0 ? pl.m : pl.n;
+  dist::scatter_shard_k<<<grid_for((long)r * cnt), 256, 0, s>>>(L.D->dview, local, r, cnt, off, full, which, st);
+  dist::barrier_k<<<1, 32, 0, s>>>(L.D->dview, st);
+  CUK();
+  c->launches += 2;
 }
 
 // One outer iteration, step() of engine.hpp:309-440.
 void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGraphConditionalHandle ch,
                        cudaGraphConditionalHandle cw, int mode, Prof* prof) {
   DevState* st = c->st.p;
+  const Layout L = make_layout(c, pl);
+  const DistHost* D = L.D;
   const int m = pl.m, n = pl.n, r = pl.r;
-  const long wsz = (long)m * r, hsz = (long)r * n;
+  const int ml = L.m_loc, nl = L.n_loc;
+  const long wsz = (long)ml * r, hsz = (long)r * nl;
   mark(c, s, prof, 0);
   misc::iter_begin<<<1, 1, 0, s>>>(st);
   CUK();
   c->launches++;
 
+  auto fixup = [&](double* A, int cnt, long off, long full, int which, double* G, int side) {
+    if (D) {
+      dist::reinit_fixup_dist<<<1, 256, 0, s>>>(D->dview, A, r, cnt, off, full, which, G, pl.reinit_seed, side, st);
+    } else {
+      misc::reinit_fixup<<<1, misc::NT, 0, s>>>(A, cnt, r, cnt, G, pl.reinit_seed, side, st);
+    }
+    CUK();
+    c->launches++;
+  };
+
   // ---- H update (engine.hpp:323-337) ----
-  gram_launch(c, s, pl.prec, c->WyT.p, m, r, m, c->GH.p, st);
-  misc::reinit_fixup<<<1, misc::NT, 0, s>>>(c->WyT.p, m, r, m, c->GH.p, pl.reinit_seed, 0, st);
-  CUK();
-  c->launches++;
+  // (multi-GPU: the W_yᵀ replica was assembled at the end of the previous iteration / in begin)
+  gram_launch(c, s, pl.prec, c->WyT.p, ml, r, ml, c->GH.p, st);
+  dist_allreduce(c, s, L, c->GH.p, r * r, st);
+  fixup(c->WyT.p, ml, L.row0, m, 0, c->GH.p, 0);
   mark(c, s, prof, 1);
   if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
     c->launches++;
   } else {
-    gemm_launch(c, s, false, c->WyT.p, m, c->x, n, c->CH.p, n, r, n, m, false, st);
+    gemm_launch(c, s, false, L.wyfull, m, L.xcb, L.ld_cb, c->CH.p, nl, r, nl, m, false, st);
   }
   mark(c, s, prof, 2);
-  enqueue_inner(c, s, pl, 0, pl.inner_h, c->GH.p, c->CH.p, c->Hy.p, c->Hn.p, n, pl.max_sweeps_h, st, ch, mode, prof);
+  enqueue_inner(c, s, pl, 0, pl.inner_h, c->GH.p, c->CH.p, c->Hy.p, c->Hn.p, nl, pl.max_sweeps_h, st, ch, mode, prof,
+                D, n);
   mark(c, s, prof, 3);
 
   // ---- early H extrapolation (engine.hpp:340-347) ----
@@ -741,10 +853,10 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   mark(c, s, prof, 4);
 
   // ---- W update (engine.hpp:353-383) ----
-  gram_launch(c, s, pl.prec, T, n, r, n, c->GW.p, st);
-  misc::reinit_fixup<<<1, misc::NT, 0, s>>>(T, n, r, n, c->GW.p, pl.reinit_seed, 1, st);
-  CUK();
-  c->launches++;
+  dist_gather(c, s, L, T, r, 1, pl, st);                 // T replica for X·Tᵀ
+  gram_launch(c, s, pl.prec, T, nl, r, nl, c->GW.p, st);
+  dist_allreduce(c, s, L, c->GW.p, r * r, st);
+  fixup(T, nl, L.col0, n, 1, c->GW.p, 1);
   mark(c, s, prof, 5);
   auto cross_xht = [&](const double* Tm, double* out) {
     if (pl.prec == PREC_EXACT) {
@@ -752,12 +864,13 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
       CUK();
       c->launches++;
     } else {
-      gemm_launch(c, s, true, Tm, n, c->x, n, out, m, r, m, n, false, st);
+      gemm_launch(c, s, true, D ? L.tfull : Tm, n, L.xrb, L.ld_rb, out, ml, r, ml, n, false, st);
     }
   };
   cross_xht(T, c->P.p);
   mark(c, s, prof, 6);
-  enqueue_inner(c, s, pl, 1, pl.inner_w, c->GW.p, c->P.p, c->WyT.p, c->WnT.p, m, pl.max_sweeps_w, st, cw, mode, prof);
+  enqueue_inner(c, s, pl, 1, pl.inner_w, c->GW.p, c->P.p, c->WyT.p, c->WnT.p, ml, pl.max_sweeps_w, st, cw, mode,
+                prof, D, m);
   mark(c, s, prof, 7);
 
   // ---- error (engine.hpp:402-416) ----
@@ -768,13 +881,15 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
     misc::extrap<<<grid_for(hsz), 256, 0, s>>>(c->Hn.p, c->H.p, c->Hy.p, hsz, 0, st);
     CUK();
     c->launches++;
-    gram_launch(c, s, pl.prec, c->Hy.p, n, r, n, c->Glit.p, st);
+    dist_gather(c, s, L, c->Hy.p, r, 1, pl, st);
+    gram_launch(c, s, pl.prec, c->Hy.p, nl, r, nl, c->Glit.p, st);
+    dist_allreduce(c, s, L, c->Glit.p, r * r, st);
     cross_xht(c->Hy.p, c->Plit.p);
     Pe = c->Plit.p;
     Ge = c->Glit.p;
     mode_h = 2;
   }
-  enqueue_error_terms(c, s, pl, c->WnT.p, Pe, st);
+  enqueue_error_terms(c, s, pl, c->WnT.p, Pe, st, ml, D);
   mark(c, s, prof, 8);
   misc::decide<<<1, misc::NT, 0, s>>>(st, c->dd.p, c->GWn.p, Ge, r, pl.prec == PREC_EXACT, c->recs.p, 0);
   CUK();
@@ -782,6 +897,7 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
                                                               c->Hn.p, hsz, mode_h, st);
   CUK();
   c->launches += 2;
+  dist_gather(c, s, L, c->WyT.p, r, 0, pl, st);          // W_yᵀ replica for the next iteration
   mark(c, s, prof, 9);
 }
 
@@ -793,6 +909,7 @@ struct Session {
   Plan pl{};
   bool dev_factors = false;
   size_t m = 0, n = 0, r = 0;
+  size_t ml = 0, nl = 0;    // local extents (rows of W, columns of H held here)
   size_t K = 0;             // max_outer_iterations
   size_t launched = 0;      // iterations enqueued so far
   size_t counted = 0;       // iterations whose kernels were added to c->launches
@@ -820,8 +937,15 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   CU(cudaSetDevice(c->device));
   close_session(c);
   validate_cfg(cfg);
-  if (!c->x) throw Fail{ENMF_INVALID_ARGUMENT, "run: no data matrix loaded"};
+  const DistHost* D = (c->dist && c->dist->ready) ? c->dist : nullptr;
+  if (!D && !c->x) throw Fail{ENMF_INVALID_ARGUMENT, "run: no data matrix loaded"};
+  if (D && (!D->xc || !D->xr)) throw Fail{ENMF_INVALID_ARGUMENT, "run: no sharded data loaded"};
+  if (D && cfg->precision == PREC_EXACT)
+    throw Fail{ENMF_INVALID_ARGUMENT, "the bitwise-faithful precision is single-GPU only"};
+  if (D && r != D->r) throw Fail{ENMF_INVALID_ARGUMENT, "run: rank differs from the one the shared buffers were sized for"};
   const size_t m = c->m, n = c->n;
+  // local extents: the whole problem on one GPU, this rank's shards otherwise
+  const size_t ml = D ? D->mp : m, nl = D ? D->np : n;
   if (r == 0) throw Fail{ENMF_INVALID_ARGUMENT, "DenseMatrix: rows and cols must be >= 1"};
   if (!w0 || !h0) throw Fail{ENMF_INVALID_ARGUMENT, "run: null initial factor"};
   if (m > (size_t)INT32_MAX || n > (size_t)INT32_MAX || r > 4096)
@@ -832,11 +956,11 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     throw Fail{ENMF_INVALID_ARGUMENT, "hals_solve on device supports r <= 1024"};
   if (cfg->max_outer_iterations > (1ULL << 24))
     throw Fail{ENMF_INVALID_ARGUMENT, "max_outer_iterations exceeds the record buffer limit (2^24)"};
-  const size_t wsz = m * r, hsz = r * n;
+  const size_t wsz = ml * r, hsz = r * nl;
   cudaStream_t s = c->stream;
   (void)cudaGetLastError();  // drop a stale (non-sticky) error from an earlier failed call
   set_attrs_once();
-  ensure_buffers(c, m, n, r);
+  ensure_buffers(c, ml, nl, r);
   if (cfg->precision == PREC_EXACT || r > 128) c->terms.ensure(std::max(wsz, hsz));
   const size_t K = cfg->max_outer_iterations;
   c->recs.ensure(K + 1);
@@ -865,8 +989,8 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     c->launches += 2;
   }
   {
-    dim3 tb(32, 8), tg((unsigned)((r + 31) / 32), (unsigned)((m + 31) / 32));
-    misc::transpose<<<tg, tb, 0, s>>>(c->scratch.p, c->WT.p, (int)m, (int)r);
+    dim3 tb(32, 8), tg((unsigned)((r + 31) / 32), (unsigned)((ml + 31) / 32));
+    misc::transpose<<<tg, tb, 0, s>>>(c->scratch.p, c->WT.p, (int)ml, (int)r);
     CUK();
     c->launches++;
   }
@@ -913,32 +1037,39 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   pl.reinit_seed = cfg->reinit_seed;
   se->dev_factors = dev_factors;
   se->m = m; se->n = n; se->r = r; se->K = K;
+  se->ml = ml; se->nl = nl;
   se->kps = (pl.prec == PREC_EXACT || r > 128) ? 2 : 1;
+  const Layout L = make_layout(c, pl);
 
   // ||X||^2 (linalg.hpp:160-171) and e(0) (engine.hpp:487-503)
-  const long xs = (long)m * n;
+  const double* xnorm = D ? D->xr : c->x;   // multi-GPU: the row blocks partition X
+  const long xs = (long)ml * n;
   if (pl.prec == PREC_EXACT) {
-    misc::neumaier_exact<<<1, 32, 0, s>>>(c->x, nullptr, xs, 0, 0, 0, c->dd.p + 2, nullptr);
+    misc::neumaier_exact<<<1, 32, 0, s>>>(xnorm, nullptr, xs, 0, 0, 0, c->dd.p + 2, nullptr);
     c->launches++;
   } else {
     const int nb = (int)std::min<long>(4096, std::max<long>(1, (xs + 4095) / 4096));
-    misc::dd_partial<<<nb, misc::NT, 0, s>>>(c->x, nullptr, xs, c->ddpart.p, c->ddpart.p + 4096, nullptr);
+    misc::dd_partial<<<nb, misc::NT, 0, s>>>(xnorm, nullptr, xs, c->ddpart.p, c->ddpart.p + 4096, nullptr);
     misc::dd_final<<<1, misc::NT, 0, s>>>(c->ddpart.p, c->ddpart.p + 4096, nb, c->dd.p + 2, nullptr);
     c->launches += 2;
   }
   CUK();
+  dist_allreduce(c, s, L, c->dd.p + 2, 2, st);
   misc::set_norm<<<1, 1, 0, s>>>(st, c->dd.p + 2);
   CUK();
-  gram_launch(c, s, pl.prec, c->H.p, n, (int)r, (int)n, c->GW.p, st);
+  gram_launch(c, s, pl.prec, c->H.p, nl, (int)r, (int)nl, c->GW.p, st);
+  dist_allreduce(c, s, L, c->GW.p, (int)(r * r), st);
+  dist_gather(c, s, L, c->H.p, (int)r, 1, pl, st);       // H0 replica for X·H0ᵀ
+  dist_gather(c, s, L, c->WT.p, (int)r, 0, pl, st);      // W0ᵀ replica for iteration 1's W_yᵀX
   if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);
     CUK();
     c->launches++;
   } else {
-    gemm_launch(c, s, true, c->H.p, n, c->x, n, c->P.p, m, (int)r, (int)m, (int)n, false, st);
+    gemm_launch(c, s, true, D ? L.tfull : c->H.p, n, L.xrb, L.ld_rb, c->P.p, ml, (int)r, (int)ml, (int)n, false, st);
   }
-  enqueue_error_terms(c, s, pl, c->WT.p, c->P.p, st);
+  enqueue_error_terms(c, s, pl, c->WT.p, c->P.p, st, (int)ml, D);
   misc::decide<<<1, misc::NT, 0, s>>>(st, c->dd.p, c->GWn.p, c->GW.p, (int)r, pl.prec == PREC_EXACT, c->recs.p, 1);
   CUK();
   c->launches += 2;
@@ -1053,7 +1184,7 @@ size_t sync_impl(enmf_gpu_ctx* c, enmf_gpu_iter* iters, size_t cap, size_t* n_it
 void end_impl(enmf_gpu_ctx* c, double* w_out, double* h_out, double* norm_x_out) {
   Session* se = need_session(c);
   cudaStream_t s = c->stream;
-  const size_t m = se->m, n = se->n, r = se->r;
+  const size_t m = se->ml, n = se->nl, r = se->r;   // this rank's shards (the whole factors on one GPU)
   if (norm_x_out) {
     DevState out;
     CU(cudaMemcpyAsync(&out, c->st.p, sizeof out, cudaMemcpyDeviceToHost, s));
@@ -1148,5 +1279,6 @@ void* enmf_gpu_stream(enmf_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; 
 
 }  // extern "C"
 
+#include "dist_api.inc"
 #include "cabi.inc"
 #include "kernels_api.inc"

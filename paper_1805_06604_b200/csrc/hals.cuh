@@ -23,6 +23,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "dist.cuh"
 
 namespace hals {
 
@@ -45,6 +46,7 @@ struct Args {
   int side;               // 0: H update, 1: W update (error message / flags)
   unsigned long long cond;  // cudaGraphConditionalHandle (0 = none)
   int use_cond;
+  const dist::View* dv;     // multi-GPU: all-reduce the sweep gain across ranks (nullable)
 };
 
 ENMF_DEV void set_cond(const Args& a, unsigned v) {
@@ -100,10 +102,11 @@ ENMF_DEV void last_block_reduce_n(const Args& a, double block_gain, int block_nf
     v = __dadd_rn(v, __ldcg(a.part + b));
     nf |= __ldcg(a.part_nf + b);
   }
-  const double total = block_reduce_sum_any(v, red);
+  double total = block_reduce_sum_any(v, red);
   nf = __syncthreads_or(nf);
   if (threadIdx.x == 0) {
     a.ctl->arrive = 0;
+    if (a.dv) dist::allreduce_gain(*a.dv, total, nf, &total, &nf);  // global stall rule
     finish_sweep(a, total, nf);
   }
 }
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kDmmaWarps * 32, 1) sweep_dmma(Args a) {
   double* Gs = sm;                 // [RMAX][LDG]
   double* Gd = sm + RMAX * LDG;    // G_kk (1 for padding rows)
   double* Gi = Gd + RMAX;          // 1 / G_kk
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_dmma_p(Args a, int ntiles) {
   double* Gs = sm;
   double* Gd = sm + RMAX * LDG;
   double* Gi = Gd + RMAX;
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   {
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_dmma_t(Args a, int ntiles) {
   double* Gs = sm;
   double* Gd = sm + RMAX * LDG;
   double* Gi = Gd + RMAX;
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   {
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_cv(Args a, int ntiles) {
   double* Gd = sm + RMAX * LDG;
   double* Gi = Gd + RMAX;
   double* GL = Gi + RMAX;           // [NB][8][9]: strictly lower part of each diagonal block
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
@@ -936,7 +939,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_la(Args a, int ntiles) {
   double* Gs = sm;
   double* Gd = sm + RMAX * LDG;
   double* Gi = Gd + RMAX;
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   {
@@ -1138,7 +1141,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_rl(Args a, int ntiles) {
   double* Gd = sm + RMAX * LDG;     // G_kk (1 on padding rows)
   double* Gi = Gd + RMAX;           // 1 / G_kk
   double* GL = Gi + RMAX;           // [NB][8][8] +G strictly lower part of each diagonal block
-  __shared__ double red[NTH];
+  __shared__ double red[NTH + 33];
 
   const int r = a.r;
   for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {

@@ -307,3 +307,35 @@ def test_c5_full_size_properties(ctx):
     assert not np.any(ups[1:] & ups[:-1])
     assert err[-1] < err[0]
     assert np.all(wo.cpu().numpy() >= 0) and np.all(ho.cpu().numpy() >= 0)
+
+
+# ---------------------------------------------------- multi-GPU engine, world 1
+@pytest.mark.parametrize("alg,shape", [("e-ahals-hp3", (1030, 400, 40)), ("e-ahals-hp1", (300, 257, 17)),
+                                       ("e-anls-hp1", (400, 300, 12))])
+def test_sharded_engine_world1_matches_single(ctx, port, alg, shape):
+    """The sharded engine (peer-memory all-gathers, mailbox all-reduces, per-sweep
+    gain exchange, csrc/dist.cuh) driven with one rank must reproduce the
+    single-GPU path: same restarts, errors within 1e-9, factors within 1e-6."""
+    from paper_1805_06604_b200.dist import ShardedContext
+    m, n, r = shape
+    x = port.gen_config(2, m, n, r, 5) if alg != "e-anls-hp1" else port.gen_config(3, m, n, r, 5)
+    w0, h0 = port.random_init(m, n, r, 6)
+    cfg = _cfg(alg, 15)
+    single = ctx.run(x, w0, h0, cfg, E.TimingMode.none)
+    sc = ShardedContext(0, 0, 1, m, n, r, lambda b: [b])
+    try:
+        sc.load_sharded(*sc.shard_x(x))
+        sc.begin(w0, h0, cfg)
+        sc.step(cfg.max_outer_iterations)
+        recs = sc.sync()
+        w = np.empty((m, r))
+        h = np.empty((r, n))
+        sc.end(w.ctypes.data, h.ctypes.data)
+    finally:
+        sc.finalize()
+    e = np.array([it.error for it in recs])
+    es = single.column("error")
+    assert np.array_equal(np.array([it.restarted for it in recs]), single.column("restarted"))
+    assert np.max(np.abs(e - es) / es) <= 1e-9
+    assert np.max(np.abs(w - single.factors.w)) <= 1e-6 * np.max(np.abs(single.factors.w))
+    assert np.max(np.abs(h - single.factors.h)) <= 1e-6 * np.max(np.abs(single.factors.h))
