@@ -16,9 +16,13 @@ cores), clocks and gpu_launches.
 unmodified headers compiled in place; the C restatement if _ref is absent) on
 the host cores, same metric/config, each step a bounded sample.
 
-Multi-GPU (torchrun, N > 1): each rank runs its own C5 problem (replicas, no
-collective; SURVEY §8(e) sharding of ONE problem is the next row), value = the
-sum over ranks of K / (max over ranks of the device time).
+Multi-GPU (torchrun, N > 1): ONE C5 problem sharded over the ranks (SURVEY
+§8(e), paper_1805_06604_b200/dist.py): rank p holds X[:, J_p] and X[I_p, :] and
+the factor shards; the engine exchanges factor shards, r×r partials and one
+scalar per HALS sweep through CUDA-IPC peer memory (csrc/dist.cuh).  Strong
+scaling: value = K / (max over ranks of the device time of K iterations).
+X is defined tile-wise (4096² tiles, each from its own seeded generator) so
+every rank builds exactly its blocks of the same matrix.
 """
 from __future__ import annotations
 
@@ -55,7 +59,8 @@ def config_block(args, world):
             "m": M, "n": N, "r": R, "algorithm": "e-ahals-hp3", "precision": "fp64",
             "beta0": 0.5, "eta": 1.5, "gamma": 1.01, "gamma_bar": 1.005,
             "l2": "inputs larger than L2 (X = 8.59 GB FP64 vs 126 MB L2); no flush needed",
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+            "parallelism": f"sharded x{world} (X column+row blocks, peer-memory exchanges)" if world > 1
+            else "single GPU"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -195,7 +200,7 @@ def run_reference(args, rank, world):
     value = total_units / total_sec
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_sec / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_block(args, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": res["kind"],
                              "sample": res["sample"]},
@@ -205,34 +210,74 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------- our arm
-def gen_c5(device, seed):
+TILE = 4096
+
+
+def gen_factors(device, seed):
+    """W0 (m×r), H0 (r×n) of X and the initial factors Wi, Hi (full, same on every rank)."""
     import torch
     g = torch.Generator(device=device).manual_seed(seed)
     w0 = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
     h0 = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
-    x = torch.randn(M, N, device=device, dtype=torch.float64, generator=g)
-    x.abs_().mul_(0.01)
-    x.addmm_(w0, h0)
-    del w0, h0
     wi = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
     hi = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
-    return x, wi, hi
+    return w0, h0, wi, hi
+
+
+def gen_block(w0, h0, r0, r1, c0, c1, seed):
+    """X[r0:r1, c0:c1] of X = W0·H0 + |N(0, 0.01²)|, the noise drawn per TILE² tile."""
+    import torch
+    dev = w0.device
+    out = torch.empty((r1 - r0, c1 - c0), device=dev, dtype=torch.float64)
+    for bi in range(r0 // TILE, (r1 + TILE - 1) // TILE):
+        for bj in range(c0 // TILE, (c1 + TILE - 1) // TILE):
+            g = torch.Generator(device=dev).manual_seed(seed * 1000003 + bi * 4099 + bj)
+            t = torch.randn(TILE, TILE, device=dev, dtype=torch.float64, generator=g)
+            i0, i1 = max(r0, bi * TILE), min(r1, (bi + 1) * TILE)
+            j0, j1 = max(c0, bj * TILE), min(c1, (bj + 1) * TILE)
+            blk = t[i0 - bi * TILE:i1 - bi * TILE, j0 - bj * TILE:j1 - bj * TILE].abs_().mul_(0.01)
+            blk.addmm_(w0[i0:i1], h0[:, j0:j1])
+            out[i0 - r0:i1 - r0, j0 - c0:j1 - c0] = blk
+            del t
+    return out
+
+
+def _make_context(E, dist_mod, local_rank, rank, world, xs, exchange):
+    """Single-GPU Context with X loaded, or this rank's ShardedContext."""
+    if world == 1:
+        ctx = E.Context(local_rank)
+        ctx.load_device(xs[0].data_ptr(), M, N)
+        return ctx
+    ctx = dist_mod.ShardedContext(local_rank, rank, world, M, N, R, exchange)
+    ctx.load_sharded_device(xs[0].data_ptr(), xs[1].data_ptr())
+    return ctx
 
 
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_1805_06604_b200 as E
+    from paper_1805_06604_b200 import dist as D
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    x, wi, hi = gen_c5(dev, 1234 + rank)
+    seed = 1234
+    w0, h0, wi, hi = gen_factors(dev, seed)
+    r0, mp, c0, np_ = D.shard_bounds_py(M, N, rank, world)
+    if world == 1:
+        xs = (gen_block(w0, h0, 0, M, 0, N, seed),)
+        wi_s, hi_s = wi, hi
+    else:
+        xs = (gen_block(w0, h0, 0, M, c0, c0 + np_, seed), gen_block(w0, h0, r0, r0 + mp, 0, N, seed))
+        wi_s = wi[r0:r0 + mp].contiguous()
+        hi_s = hi[:, c0:c0 + np_].contiguous()
+    del w0, h0
     torch.cuda.synchronize()
-    ctx = E.Context(local_rank)
-    ctx.load_device(x.data_ptr(), M, N)
+    exchange = D.torch_exchange() if world > 1 else None
+    ctx = _make_context(E, D, local_rank, rank, world, xs, exchange)
     prof_steps = 2
     cfg = cfg_c5(args.warmup + args.steps + prof_steps)
-    ctx.begin_device(wi.data_ptr(), hi.data_ptr(), R, cfg)
+    ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg)
     ctx.step(args.warmup)
     ctx.sync()
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
@@ -264,46 +309,66 @@ def run_ours(args, rank, world, local_rank):
     phases = [ctx.step_profiled() for _ in range(prof_steps)]
     ctx.sync()
     ctx.end()
+    if world > 1:
+        ctx.finalize()
+    ctx.close()
     gemm_ms = statistics.mean([(p["cross_wx"] + p["cross_xht"]) / 2 for p in phases])
-    gemm_flops = 2.0 * R * M * N
+    # per-launch algorithmic flops: 2·r·m·n on one GPU, 2·r·m·n/P on each rank when sharded
+    gemm_flops = 2.0 * R * M * N / world
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
     iter_ms = ms / args.steps
     flops_alg = 4.0 * M * N * R + 2.0 * (M + N) * R * R
-    t_roof_ms = flops_alg / (FP64_PEAK_TFLOPS * 1e12) * 1e3
-    value = world * args.steps / (ms * 1e-3)
+    t_roof_ms = flops_alg / world / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    value = args.steps / (ms * 1e-3)
 
-    # e2e: the drop-in C-ABI call (enmf_gpu_run_dense) on pinned host buffers
+    # e2e: the public API on pinned host buffers (single GPU: the drop-in C-ABI call
+    # enmf_gpu_run_dense; sharded: load_sharded/begin/step/sync/end of this rank's blocks)
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty((M, N), dtype=torch.float64, pin_memory=True)
-        xh.copy_(x)
-        wh = torch.empty((M, R), dtype=torch.float64, pin_memory=True)
-        hh = torch.empty((R, N), dtype=torch.float64, pin_memory=True)
-        wh.copy_(wi)
-        hh.copy_(hi)
-        del x
+        pin = lambda t: torch.empty(t.shape, dtype=torch.float64, pin_memory=True).copy_(t)
+        xh = [pin(x) for x in xs]
+        wh, hh = pin(wi_s), pin(hi_s)
+        del xs
         torch.cuda.empty_cache()
         cfg2 = cfg_c5(args.steps)
-        ctx2 = E.Context(local_rank)
-        xn, wn, hn = xh.numpy(), wh.numpy(), hh.numpy()
+        if world == 1:
+            ctx2 = E.Context(local_rank)
+        else:
+            ctx2 = D.ShardedContext(local_rank, rank, world, M, N, R, exchange)
+        xn = [x.numpy() for x in xh]
+        wn, hn = wh.numpy(), hh.numpy()
+        wout, hout = torch.empty_like(wh).pin_memory(), torch.empty_like(hh).pin_memory()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        rec2 = ctx2.run(xn, wn, hn, cfg2, E.TimingMode.none)
+        if world == 1:
+            rec2 = ctx2.run(xn[0], wn, hn, cfg2, E.TimingMode.none)
+            fre = rec2.final_relative_error()
+        else:
+            ctx2.load_sharded(xn[0], xn[1])
+            ctx2.begin(wn, hn, cfg2)
+            ctx2.step(args.steps)
+            rr = ctx2.sync()
+            ctx2.end(wout.data_ptr(), hout.data_ptr())
+            fre = rr[-1].relative_error
         t1 = time.perf_counter()
         wall = t1 - t0
         if world > 1:
             t = torch.tensor([wall], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        e2e = {"value": world * args.steps / wall, "unit": UNIT,
-               "h2d_bytes_per_step": int((M * N + M * R + R * N) * 8),
-               "d2h_bytes_per_step": int((M * R + R * N) * 8 + (args.steps + 1) * 56),
-               "step": f"one enmf_gpu_run_dense call: X/W0/H0 host->device, {args.steps} outer iterations, "
-                       f"W/H/records device->host", "seconds": wall,
-               "final_relative_error": rec2.final_relative_error()}
+            ctx2.finalize()
         ctx2.close()
+        xb = sum(x.numel() for x in xh) * 8
+        e2e = {"value": args.steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": int(xb + (wh.numel() + hh.numel()) * 8),
+               "d2h_bytes_per_step": int((wh.numel() + hh.numel()) * 8 + (args.steps + 1) * 56),
+               "step": (f"one enmf_gpu_run_dense call: X/W0/H0 host->device, {args.steps} outer iterations, "
+                        f"W/H/records device->host" if world == 1 else
+                        f"per rank: X column+row blocks and factor shards host->device, {args.steps} outer "
+                        f"iterations, factor shards/records device->host"),
+               "seconds": wall, "final_relative_error": fre}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -314,16 +379,19 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": iter_ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch generator on device)",
+                "warmup": args.warmup, "ms_per_step": iter_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded torch generators on device, tile-wise)",
                 "config": config_block(args, world),
-                "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma (W_yᵀX / X·Tᵀ, 2·r·m·n flop per launch)",
+                "roofline": {"bound": "tensor",
+                             "kernel": "gemm_f64_dmma (W_yᵀX / X·Tᵀ, 2·r·m·n/P flop per launch)",
                              "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SRC,
-                             "gemm_ms": gemm_ms,
+                             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": args.traffic,
+                             "peak_source": FP64_PEAK_SRC, "gemm_ms": gemm_ms,
                              "iteration": {"flops_alg": flops_alg, "t_roof_ms": t_roof_ms,
                                            "frac": t_roof_ms / iter_ms,
-                                           "note": "t_roof = (4mnr + 2(m+n)r²) / FP64 peak; HALS sweeps excluded"},
+                                           "note": "t_roof = (4mnr + 2(m+n)r²)/P / FP64 peak; HALS sweeps "
+                                                   "excluded"},
                              "phases_ms": phases[-1]},
                 "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
                 "sweeps": {"h_mean": statistics.mean(sweeps_h) if sweeps_h else None,
@@ -342,6 +410,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=64)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per GEMM launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -81,7 +81,7 @@ struct enmf_gpu_ctx {
   const double* x = nullptr;
   size_t m = 0, n = 0;
   // factors and products
-  DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch;
+  DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch, Gf;
   DBuf<double> partials, gain_part, terms, ddpart, dd;
   DBuf<int> part_nf, flags;
   DBuf<unsigned> counters;
@@ -171,6 +171,9 @@ void set_attrs_once() {
   big((const void*)gemm::gemm_f64_dmma_s<true, 2, true>, gemm::st::SMEM_BYTES);
   big((const void*)gemm::gemm_f64_dmma_s<true, 1, false>, gemm::st::SMEM_BYTES);
   big((const void*)gemm::gemm_f64_dmma_s<true, 1, true>, gemm::st::SMEM_BYTES);
+  big((const void*)hals::sweep_ws<32>, hals::ws_smem_bytes<32>());
+  big((const void*)hals::sweep_ws<64>, hals::ws_smem_bytes<64>());
+  big((const void*)hals::sweep_ws<128>, hals::ws_smem_bytes<128>());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -353,7 +356,7 @@ int hals_variant() {
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
       : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : 11;  // default t14u2
+      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "" ? 50 : 11;  // default: ws
   }
   return v;
 }
@@ -387,6 +390,21 @@ void attrs_sweep_cv() {
                           hals::cv_smem_bytes<64>()));
   CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<128, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           hals::cv_smem_bytes<128>()));
+}
+
+template <int R_, bool PROF = false, int SKIP = 0>
+void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  const long ntiles = ((long)a.N + 7) / 8;
+  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 15) / 16));
+  if (PROF) {
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute((const void*)hals::sweep_ws<R_, true, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              hals::ws_smem_bytes<R_>()));
+      attr = true;
+    }
+  }
+  hals::sweep_ws<R_, PROF, SKIP><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 
 template <int R_, int NW>
@@ -518,6 +536,16 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     launch_sweep_cv<128, 2, 14, 3>(c, s, a);
   } else if (hals_variant() == 46) {   // timing experiment: same, one warp per CTA (no contention)
     launch_sweep_cv<128, 2, 1, 3>(c, s, a);
+  } else if (hals_variant() == 51) {   // timing experiment: per-warp cycle profile into a.terms
+    launch_sweep_ws<128, true>(c, s, a);
+  } else if (hals_variant() == 52) {
+    launch_sweep_ws<128, true, 1>(c, s, a);
+  } else if (hals_variant() == 53) {
+    launch_sweep_ws<128, true, 2>(c, s, a);
+  } else if (hals_variant() == 50) {
+    if (r <= 32) launch_sweep_ws<32>(c, s, a);
+    else if (r <= 64) launch_sweep_ws<64>(c, s, a);
+    else launch_sweep_ws<128>(c, s, a);
   } else if (hals_variant() == 30) {
     launch_sweep_la_r<14>(c, s, a);
   } else if (hals_variant() == 31) {
@@ -695,6 +723,20 @@ void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
   if (p) CU(cudaEventRecord(p->ev[phase], s));
 }
 
+// sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
+void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
+  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 53)) return;
+  constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
+  c->Gf.ensure(3 * kGf);
+  double* gf = c->Gf.p + slot * kGf;
+  if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+  else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+  else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+  CUK();
+  c->launches++;
+  a.Gf = gf;
+}
+
 void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, int solver, const double* G,
                    const double* Cm, const double* Hin, double* Hout, int rows_n, int max_sweeps, DevState* st,
                    cudaGraphConditionalHandle cond, int mode, Prof* prof, const DistHost* D = nullptr,
@@ -712,6 +754,7 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     hals::reset_ctl<<<1, 1, 0, s>>>(a.ctl, st);
     CUK();
     c->launches++;
+    ws_prepare(c, s, a, pl.prec, side);
     if (mode == INNER_CAPTURE) {
       capture_while(c, s, cond, [&](cudaStream_t bs) { hals_body(c, bs, a, pl.prec); });
     } else {

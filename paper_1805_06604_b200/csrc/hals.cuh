@@ -47,6 +47,7 @@ struct Args {
   unsigned long long cond;  // cudaGraphConditionalHandle (0 = none)
   int use_cond;
   const dist::View* dv;     // multi-GPU: all-reduce the sweep gain across ranks (nullable)
+  const double* Gf;         // sweep_ws: Gram in A-fragment order (ws_prep)
 };
 
 ENMF_DEV void set_cond(const Args& a, unsigned v) {
@@ -1253,6 +1254,298 @@ __global__ void __launch_bounds__(NW * 32, 1) sweep_rl(Args a, int ntiles) {
   const double bg = block_reduce_sum_any(gain, red);
   nf = __syncthreads_or(nf);
   last_block_reduce_n<NTH>(a, bg, nf, red);
+}
+
+// ---- paired-warp tensor-core sweep (default) ----------------------------------
+//
+// Every SM sub-partition runs one PAIR of warps over its own 32 columns:
+//   * the product warp issues the DMMAs of the block products
+//         S_b = G[b-rows, :] · H        (A = Gram fragment in registers, B = H in smem)
+//   * the row warp owns one column per lane and finishes the 8 rows of block b
+//     sequentially (nnls.hpp:117-148 per row), entirely in registers, writing the
+//     new rows straight into the H tile.
+// The two phases strictly alternate (named-barrier hand-offs, bar.arrive by the
+// producer of a tile, bar.sync by its consumer): measured on B200
+// (tools/probe/pipe_probe.cu, profiles/r01_latency_probes.txt), scalar FP64
+// instructions on a sub-partition whose DMMA pipe is streaming are starved
+// (~75 cycles per independent op, ~500 per dependent op), so the row chain runs
+// while the sub-partition's DMMA pipe is idle and takes ~0.3 K cycles instead of
+// ~1.7 K when overlapped.  Diagonal blocks enter the DMMA with their lower triangle
+// (diagonal included) zeroed, so the row warp only subtracts
+// sum_{j<k in block} G_kj h_new_j.
+//
+// Gram fragments come pre-arranged by ws_prep (once per inner solve): Gf holds,
+// for row block b and k-step pair s2, the two A-fragment values of every lane
+// contiguously, so a lane fetches two k-steps with one 16-byte load, and the
+// fragments of block b+1 stream into the registers freed by block b.  The H tile
+// is stored with 16-byte chunks holding columns (c, c+8) and an XOR swizzle per
+// row, so each lane reads the B fragments of its 4 column tiles with two
+// conflict-free 16-byte loads per k-step.
+constexpr int WS_SLD = 40;   // S tile row stride: conflict-free 16-byte fragment stores
+
+template <int RMAX>
+constexpr int ws_smem_bytes() {
+  return (4 * (RMAX * 32 + 8 * WS_SLD) + (RMAX / 8) * 64 + RMAX) * 8;
+}
+
+// position of (row k, column c) in a swizzled 32-column tile
+ENMF_DEV int ws_pos(int k, int c) {
+  const int sw = ((k & 1) << 2) | ((k >> 1) & 1);
+  return k * 32 + 2 * ((2 * (c & 7) + (c >> 4)) ^ sw) + ((c >> 3) & 1);
+}
+
+ENMF_DEV void nb_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
+ENMF_DEV void nb_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" ::"r"(id) : "memory"); }
+
+ENMF_DEV double pos_part_ws(double t) {
+  const long long b = __double_as_longlong(t);
+  return (b > 0 && b <= 0x7FF0000000000000LL) ? t : 0.0;   // t > 0 (NaN -> 0, as `t > 0 ? t : 0`)
+}
+
+// Gf[((b·KS/2 + s2)·32 + lane)·2 + e] = G[8b + lane/4][4(2·s2+e) + lane%4], zero outside r×r,
+// on/below the diagonal inside diagonal blocks, and — for odd b — in the columns of block
+// b-1, whose fragments go to Gf[RMAX² + ...] instead (the "tail" of the paired product).
+template <int RMAX>
+__global__ void ws_prep(const double* G, int r, double* Gf, const DevState* st, const HalsCtl* ctl) {
+  if ((st && !dev_active(st)) || !ctl->cont) return;
+  constexpr int KS = RMAX / 4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < RMAX * RMAX; i += gridDim.x * blockDim.x) {
+    const int e = i & 1, lane = (i >> 1) & 31, s2 = (i >> 6) % (KS / 2), b = (i >> 6) / (KS / 2);
+    const int s = 2 * s2 + e, gi = lane >> 2, gt = lane & 3;
+    const int row = 8 * b + gi, col = 4 * s + gt;
+    double v = 0.0;
+    if (row < r && col < r && !((s >> 1) == b && col - 8 * b <= gi)) v = G[(long)row * r + col];
+    const bool tail = (b & 1) && s2 == b - 1;
+    Gf[i] = tail ? 0.0 : v;
+    if (tail) Gf[RMAX * RMAX + (b >> 1) * 64 + lane * 2 + e] = v;
+  }
+}
+
+// B fragments of k-steps (2j, 2j+1) — rows 8j..8j+7 — for the NT column tiles of a pair
+template <int NT>
+ENMF_DEV void ws_ldb(const double* Hs, int j, int gt, int bx0, int bx1, double2 (&p)[4]) {
+  const int k0 = 8 * j + gt, k1 = k0 + 4;
+  p[0] = *reinterpret_cast<const double2*>(Hs + k0 * 32 + bx0);
+  if (NT > 2) p[1] = *reinterpret_cast<const double2*>(Hs + k0 * 32 + bx1);
+  p[2] = *reinterpret_cast<const double2*>(Hs + k1 * 32 + bx0);
+  if (NT > 2) p[3] = *reinterpret_cast<const double2*>(Hs + k1 * 32 + bx1);
+}
+
+// acc[t] += a0 · B(k-step 2j) + a1 · B(k-step 2j+1) for the NT tiles
+template <int NT>
+ENMF_DEV void ws_mma2(double (&acc)[4][2], double a0, double a1, const double2 (&p)[4]) {
+  dmma884(acc[0][0], acc[0][1], a0, p[0].x);
+  if (NT > 1) dmma884(acc[1][0], acc[1][1], a0, p[0].y);
+  if (NT > 2) dmma884(acc[2][0], acc[2][1], a0, p[1].x);
+  if (NT > 3) dmma884(acc[3][0], acc[3][1], a0, p[1].y);
+  dmma884(acc[0][0], acc[0][1], a1, p[2].x);
+  if (NT > 1) dmma884(acc[1][0], acc[1][1], a1, p[2].y);
+  if (NT > 2) dmma884(acc[2][0], acc[2][1], a1, p[3].x);
+  if (NT > 3) dmma884(acc[3][0], acc[3][1], a1, p[3].y);
+}
+
+ENMF_DEV void ws_store_s(double* Ss, int gi, int gt, const double (&acc)[4][2]) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    *reinterpret_cast<double2*>(Ss + gi * WS_SLD + t * 8 + 2 * gt) = make_double2(acc[t][0], acc[t][1]);
+}
+
+// The product warp's part of one round: row blocks in pairs (b, b+1).  One pass
+// over the H tile feeds both products — S_b over every row block and S_{b+1}
+// over every block but b — so each B fragment is loaded once for two A
+// fragments; S_{b+1} then gets block b's new rows (its "tail") once the row warp
+// has solved block b.  The Gram fragments of the next pair are fetched while the
+// row warp works (DMMA pipe idle).
+template <int KS, int NB, int NT, bool PROF, int SKIP>
+ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf, int gi, int gt, int bx0, int bx1,
+                                int idS, int idH, long long* pw) {
+  double A0[KS], A1[KS];
+#pragma unroll
+  for (int s = 0; s < KS; s += 2) {
+    const double2 f0 = gf[(s / 2) * 32];
+    const double2 f1 = gf[(KS / 2 + s / 2) * 32];
+    A0[s] = f0.x; A0[s + 1] = f0.y;
+    A1[s] = f1.x; A1[s + 1] = f1.y;
+  }
+#pragma unroll 1
+  for (int b = 0; b < NB; b += 2) {
+    if (b > 0) nb_sync(idH);                // rows of block b-1 are final in the tile
+    const long long c1 = PROF ? clock64() : 0;
+    double acc0[4][2], acc1[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc0[t][0] = acc0[t][1] = acc1[t][0] = acc1[t][1] = 0.0;
+    if (SKIP != 2) {
+#pragma unroll
+      for (int j = 0; j < KS / 2; ++j) {   // (block b's fragments of A1 are zero: see ws_prep)
+        double2 p[4];
+        ws_ldb<NT>(Hs, j, gt, bx0, bx1, p);
+        ws_mma2<NT>(acc0, A0[2 * j], A0[2 * j + 1], p);
+        ws_mma2<NT>(acc1, A1[2 * j], A1[2 * j + 1], p);
+      }
+    }
+    ws_store_s(Ss, gi, gt, acc0);
+    nb_arrive(idS);                          // S_b ready: the row warp solves block b
+    if (PROF) pw[2] += clock64() - c1;
+    // while it does: this pair's tail fragments and the next pair's Gram fragments
+    const double2 tl = gf[(16 * KS * KS + (b >> 1) * 64) / 2];   // Gf tails (ws_prep)
+    if (b + 2 < NB) {
+#pragma unroll
+      for (int s = 0; s < KS; s += 2) {
+        const double2 f0 = gf[(((b + 2) * KS / 2) + s / 2) * 32];
+        const double2 f1 = gf[(((b + 3) * KS / 2) + s / 2) * 32];
+        A0[s] = f0.x; A0[s + 1] = f0.y;
+        A1[s] = f1.x; A1[s + 1] = f1.y;
+      }
+    }
+    nb_sync(idH);                            // block b solved
+    const long long c2 = PROF ? clock64() : 0;
+    if (SKIP != 2) {
+      double2 p[4];
+      ws_ldb<NT>(Hs, b, gt, bx0, bx1, p);
+      ws_mma2<NT>(acc1, tl.x, tl.y, p);
+    }
+    ws_store_s(Ss, gi, gt, acc1);
+    nb_arrive(idS);                          // S_{b+1} ready
+    if (PROF) pw[2] += clock64() - c2;
+  }
+}
+
+// PROF (timing experiment): per-warp cycles [barrier wait, tile load, total, DMMA / row phase] into a.terms;
+// SKIP (timing experiment, wrong results): 1 = row warps skip the row pass, 2 = product warps skip the DMMAs
+template <int RMAX, bool PROF = false, int SKIP = 0>
+__global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
+  constexpr int NB = RMAX / 8;
+  constexpr int KS = RMAX / 4;
+  const long long tk0 = PROF ? clock64() : 0;
+  long long pw[3] = {0, 0, 0};
+  if (sweep_skipped(a)) return;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[256 + 33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp & 3;
+  const bool producer = warp < 4;
+  double* Hs = sm + pair * (RMAX * 32);
+  double* Ss = sm + 4 * RMAX * 32 + pair * 8 * WS_SLD;
+  double* Gdb = sm + 4 * (RMAX * 32 + 8 * WS_SLD);   // diagonal blocks [NB][8][8]
+  double* Gi = Gdb + NB * 64;                         // 1 / G[k][k]
+  const int r = a.r;
+  for (int e = threadIdx.x; e < NB * 64; e += 256) {
+    const int b = e >> 6, k = 8 * b + ((e >> 3) & 7), c = 8 * b + (e & 7);
+    Gdb[e] = (k < r && c < r) ? a.G[(long)k * r + c] : (k == c ? 1.0 : 0.0);
+  }
+  for (int k = threadIdx.x; k < RMAX; k += 256) Gi[k] = k < r ? __ddiv_rn(1.0, a.G[(long)k * r + k]) : 1.0;
+  __syncthreads();
+
+  const int idS = 1 + pair, idH = 5 + pair, idP = 9 + pair;
+  const long P = (long)gridDim.x * 4, q = (long)blockIdx.x * 4 + pair;
+  const long tq0 = q * ntiles / P, cnt = (q + 1) * ntiles / P - tq0;
+  const int rounds = (int)((cnt + 3) / 4);
+  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
+  double gain = 0.0;
+  int nf = 0;
+  const int gi = lane >> 2, gt = lane & 3;
+  // this lane's two 16-byte B-fragment chunks (tiles 0,1 and 2,3) within a row k with k & 3 == gt
+  const int swz = ((gt & 1) << 2) | (gt >> 1);
+  const int bx0 = 2 * ((2 * gi) ^ swz), bx1 = 2 * ((2 * gi + 1) ^ swz);
+  const double2* gf = reinterpret_cast<const double2*>(a.Gf) + lane;
+
+  for (int rd = 0; rd < rounds; ++rd) {
+    const long ta = tq0 + (long)rd * cnt / rounds;
+    const int nt = (int)(tq0 + (long)(rd + 1) * cnt / rounds - ta);
+    const long col0 = ta * 8;
+    const long long tl0 = PROF ? clock64() : 0;
+    // stage this round's 32 columns of H (zero outside r × N and past nt tiles)
+    nb_sync(idP);                           // previous round done with the tiles
+    {
+      const int c = lane;
+      const long col = col0 + c;
+      const bool okc = c < nt * 8 && col < a.N;
+      const double* sp = src + col;
+      for (int k = producer ? 0 : 1; k < RMAX; k += 2) {
+        const bool ok = okc && k < r;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(Hs + ws_pos(k, c));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
+                     "l"(ok ? sp + (long)k * a.ld : src), "r"(ok ? 8 : 0));
+      }
+      asm volatile("cp.async.wait_all;\n" ::);
+    }
+    nb_sync(idP);
+    if (PROF) pw[1] += clock64() - tl0;
+
+    if (producer) {
+      switch (nt) {
+        case 4: ws_producer_round<KS, NB, 4, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
+        case 3: ws_producer_round<KS, NB, 3, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
+        case 2: ws_producer_round<KS, NB, 2, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
+        default: ws_producer_round<KS, NB, 1, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
+      }
+    } else {
+      const long col = col0 + lane;
+      const bool valid = lane < nt * 8 && col < a.N;
+      const int rv = valid ? r : 0;         // rows this lane loads / stores
+      const double* cp = a.C + col;
+      double* hp = a.H + col;
+      double cn[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cn[i] = i < rv ? cp[(long)i * a.ld] : 0.0;
+#pragma unroll 1
+      for (int b = 0; b < NB; ++b) {
+        double bb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) bb[i] = cn[i];
+        if (b + 1 < NB) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int k = 8 * (b + 1) + i;
+            cn[i] = k < rv ? cp[(long)k * a.ld] : 0.0;
+          }
+        }
+        const long long c0 = PROF ? clock64() : 0;
+        nb_sync(idS);
+        const long long c1 = PROF ? clock64() : 0;
+        if (PROF) pw[0] += c1 - c0;
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          bb[i] = __dsub_rn(bb[i], Ss[i * WS_SLD + lane]);
+          x[i] = Hs[ws_pos(8 * b + i, lane)];
+        }
+        const double* gd = Gdb + b * 64;
+        const double* gi8 = Gi + 8 * b;
+        double hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < (SKIP == 1 ? 0 : 8); ++i) {
+          const double t = __dmul_rn(bb[i], gi8[i]);
+          const double h = pos_part_ws(t);
+          hv[i] = h;
+#pragma unroll
+          for (int l = i + 1; l < 8; ++l) bb[l] = fma(-gd[l * 8 + i], h, bb[l]);
+          Hs[ws_pos(8 * b + i, lane)] = h;
+          const double o = __dsub_rn(x[i], t), n = __dsub_rn(h, t);
+          gain = fma(gd[i * 9], __dsub_rn(__dmul_rn(o, o), __dmul_rn(n, n)), gain);
+        }
+        if (b + 1 < NB) nb_arrive(idH);
+        if (PROF) pw[2] += clock64() - c1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (8 * b + i < rv) {
+            hp[(long)(8 * b + i) * a.ld] = hv[i];
+            nf |= !isfinite(hv[i]);
+          }
+        }
+      }
+    }
+  }
+  if (PROF && lane == 0) {
+    double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 4;
+    o[0] = (double)pw[0];
+    o[1] = (double)pw[1];
+    o[2] = (double)(clock64() - tk0);
+    o[3] = (double)pw[2];
+  }
+  const double bg = block_reduce_sum_any(gain, red);
+  nf = __syncthreads_or(nf);
+  last_block_reduce_n<256>(a, bg, nf, red);
 }
 
 // ---- bitwise-faithful sweep (hals_row_update_impl order) -----------------
