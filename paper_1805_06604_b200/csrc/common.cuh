@@ -22,7 +22,7 @@ struct HalsCtl {
   int nonfinite;         // last sweep wrote a non-finite value
   int degenerate;        // index+1 of a degenerate Gram diagonal (0 = none)
   unsigned arrive;       // block-arrival counter for the last-block reduction
-  int pad;
+  unsigned epoch;        // persistent sweep kernel: number of sweeps decided
 };
 
 // Device-resident run state: BetaSchedule (engine.hpp:63-70), err_prev, the

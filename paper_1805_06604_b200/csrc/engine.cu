@@ -174,6 +174,9 @@ void set_attrs_once() {
   big((const void*)hals::sweep_ws<32>, hals::ws_smem_bytes<32>());
   big((const void*)hals::sweep_ws<64>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128>, hals::ws_smem_bytes<128>());
+  big((const void*)hals::sweep_ws<32, false, 0, true>, hals::ws_smem_bytes<32>());
+  big((const void*)hals::sweep_ws<64, false, 0, true>, hals::ws_smem_bytes<64>());
+  big((const void*)hals::sweep_ws<128, false, 0, true>, hals::ws_smem_bytes<128>());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -356,7 +359,7 @@ int hals_variant() {
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
       : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "" ? 50 : 11;  // default: ws
+      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "" ? 54 : 11;  // default: ws
   }
   return v;
 }
@@ -392,10 +395,25 @@ void attrs_sweep_cv() {
                           hals::cv_smem_bytes<128>()));
 }
 
-template <int R_, bool PROF = false, int SKIP = 0>
+template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
 void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
   const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 15) / 16));
+  if (PERSIST) {
+    // every CTA must be resident for the grid-wide decision between sweeps
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = hals::ws_smem_bytes<R_>();
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&lc, hals::sweep_ws<R_, false, 0, true>, a, ntiles));
+    return;
+  }
   if (PROF) {
     static bool attr = false;
     if (!attr) {
@@ -491,6 +509,9 @@ void launch_sweep_p(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
 }
 bool hals_use_fma() { return hals_variant() == 1; }
 
+// The persistent sweep kernel runs a whole inner solve in one launch.
+bool hals_persistent(int prec, int r) { return prec != PREC_EXACT && r <= 128 && hals_variant() == 54; }
+
 void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   const int r = a.r;
   if (prec == PREC_EXACT || r > 128) {
@@ -542,6 +563,10 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     launch_sweep_ws<128, true, 1>(c, s, a);
   } else if (hals_variant() == 53) {
     launch_sweep_ws<128, true, 2>(c, s, a);
+  } else if (hals_variant() == 54) {
+    if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
+    else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
+    else launch_sweep_ws<128, false, 0, true>(c, s, a);
   } else if (hals_variant() == 50) {
     if (r <= 32) launch_sweep_ws<32>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64>(c, s, a);
@@ -725,7 +750,7 @@ void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
 
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
 void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
-  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 53)) return;
+  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 54)) return;
   constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
   c->Gf.ensure(3 * kGf);
   double* gf = c->Gf.p + slot * kGf;
@@ -756,7 +781,12 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     c->launches++;
     ws_prepare(c, s, a, pl.prec, side);
     if (mode == INNER_CAPTURE) {
-      capture_while(c, s, cond, [&](cudaStream_t bs) { hals_body(c, bs, a, pl.prec); });
+      if (hals_persistent(pl.prec, pl.r)) {
+        a.use_cond = 0;                       // one launch runs every sweep
+        hals_body(c, s, a, pl.prec);
+      } else {
+        capture_while(c, s, cond, [&](cudaStream_t bs) { hals_body(c, bs, a, pl.prec); });
+      }
     } else {
       // host-driven: one sweep per launch, flag read back after each (profiling / no-graph path)
       cudaEvent_t e0, e1;
@@ -1081,7 +1111,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   se->dev_factors = dev_factors;
   se->m = m; se->n = n; se->r = r; se->K = K;
   se->ml = ml; se->nl = nl;
-  se->kps = (pl.prec == PREC_EXACT || r > 128) ? 2 : 1;
+  se->kps = (pl.prec == PREC_EXACT || r > 128) ? 2 : hals_persistent(pl.prec, (int)r) ? 0 : 1;
   const Layout L = make_layout(c, pl);
 
   // ||X||^2 (linalg.hpp:160-171) and e(0) (engine.hpp:487-503)
@@ -1121,9 +1151,10 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   if (K > 0) {
     CU(cudaGraphCreate(&se->graph, 0));
     cudaGraphConditionalHandle ch = 0, cw = 0;
-    if (pl.inner_h == ENMF_INNER_HALS)
+    const bool persist = hals_persistent(pl.prec, pl.r);
+    if (pl.inner_h == ENMF_INNER_HALS && !persist)
       CU(cudaGraphConditionalHandleCreate(&ch, se->graph, 1, cudaGraphCondAssignDefault));
-    if (pl.inner_w == ENMF_INNER_HALS)
+    if (pl.inner_w == ENMF_INNER_HALS && !persist)
       CU(cudaGraphConditionalHandleCreate(&cw, se->graph, 1, cudaGraphCondAssignDefault));
     const unsigned long long before = c->launches;
     CU(cudaStreamBeginCaptureToGraph(s, se->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));

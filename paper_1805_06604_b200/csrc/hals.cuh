@@ -1285,7 +1285,7 @@ constexpr int WS_SLD = 40;   // S tile row stride: conflict-free 16-byte fragmen
 
 template <int RMAX>
 constexpr int ws_smem_bytes() {
-  return (4 * (RMAX * 32 + 8 * WS_SLD) + (RMAX / 8) * 64 + RMAX) * 8;
+  return (4 * (RMAX * 32 + 8 * WS_SLD) + (RMAX / 8) * 48) * 8;
 }
 
 // position of (row k, column c) in a swizzled 32-column tile
@@ -1412,7 +1412,14 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
 
 // PROF (timing experiment): per-warp cycles [barrier wait, tile load, total, DMMA / row phase] into a.terms;
 // SKIP (timing experiment, wrong results): 1 = row warps skip the row pass, 2 = product warps skip the DMMAs
-template <int RMAX, bool PROF = false, int SKIP = 0>
+// PERSIST: one launch runs every sweep of the solve.  Between sweeps the CTAs
+// meet at a grid-wide decision point (the last CTA to arrive sums the per-CTA
+// gains in fixed order, applies the stall rule — after the cross-GPU gain
+// exchange when sharded — and publishes it through ctl->epoch), and the rounds
+// alternate direction so the tile a pair finished a sweep with is the one it
+// starts the next sweep with, already in shared memory.  Requires all CTAs to be
+// co-resident (cooperative launch, one CTA per SM).
+template <int RMAX, bool PROF = false, int SKIP = 0, bool PERSIST = false>
 __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   constexpr int NB = RMAX / 8;
   constexpr int KS = RMAX / 4;
@@ -1426,14 +1433,25 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   const bool producer = warp < 4;
   double* Hs = sm + pair * (RMAX * 32);
   double* Ss = sm + 4 * RMAX * 32 + pair * 8 * WS_SLD;
-  double* Gdb = sm + 4 * (RMAX * 32 + 8 * WS_SLD);   // diagonal blocks [NB][8][8]
-  double* Gi = Gdb + NB * 64;                         // 1 / G[k][k]
+  // per row block: lower triangle G[8b+l][8b+i] (i < l) at l(l-1)/2 + i, G_kk/2 at 28 + l,
+  // 1/G_kk at 36 + l (padding rows: unit diagonal)
+  double* Gc = sm + 4 * (RMAX * 32 + 8 * WS_SLD);
   const int r = a.r;
-  for (int e = threadIdx.x; e < NB * 64; e += 256) {
-    const int b = e >> 6, k = 8 * b + ((e >> 3) & 7), c = 8 * b + (e & 7);
-    Gdb[e] = (k < r && c < r) ? a.G[(long)k * r + c] : (k == c ? 1.0 : 0.0);
+  for (int e = threadIdx.x; e < NB * 48; e += 256) {
+    const int b = e / 48, j = e % 48;
+    double v = 0.0;
+    if (j < 28) {
+      int l = 1;
+      while (l * (l + 1) / 2 <= j) ++l;
+      const int i = j - l * (l - 1) / 2, k = 8 * b + l, c = 8 * b + i;
+      v = (k < r && c < r) ? a.G[(long)k * r + c] : 0.0;
+    } else if (j < 44) {
+      const int k = 8 * b + ((j - 28) & 7);
+      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
+      v = j < 36 ? __dmul_rn(0.5, d) : __ddiv_rn(1.0, d);
+    }
+    Gc[e] = v;
   }
-  for (int k = threadIdx.x; k < RMAX; k += 256) Gi[k] = k < r ? __ddiv_rn(1.0, a.G[(long)k * r + k]) : 1.0;
   __syncthreads();
 
   const int idS = 1 + pair, idH = 5 + pair, idP = 9 + pair;
@@ -1443,20 +1461,27 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
   double gain = 0.0;
   int nf = 0;
+  __shared__ int s_flag;
   const int gi = lane >> 2, gt = lane & 3;
   // this lane's two 16-byte B-fragment chunks (tiles 0,1 and 2,3) within a row k with k & 3 == gt
   const int swz = ((gt & 1) << 2) | (gt >> 1);
   const int bx0 = 2 * ((2 * gi) ^ swz), bx1 = 2 * ((2 * gi + 1) ^ swz);
   const double2* gf = reinterpret_cast<const double2*>(a.Gf) + lane;
+  int hoff[4];                              // swizzled position of column `lane` in a row k, by k & 3
+#pragma unroll
+  for (int j = 0; j < 4; ++j) hoff[j] = ws_pos(j, lane) - j * 32;
 
-  for (int rd = 0; rd < rounds; ++rd) {
+  for (int sw = 0;; ++sw) {
+  for (int i = 0; i < rounds; ++i) {
+    const int rd = (PERSIST && (sw & 1)) ? rounds - 1 - i : i;
     const long ta = tq0 + (long)rd * cnt / rounds;
     const int nt = (int)(tq0 + (long)(rd + 1) * cnt / rounds - ta);
     const long col0 = ta * 8;
     const long long tl0 = PROF ? clock64() : 0;
-    // stage this round's 32 columns of H (zero outside r × N and past nt tiles)
+    // stage this round's 32 columns of H (zero outside r × N and past nt tiles);
+    // persistent: the first round of a later sweep is still in shared memory
     nb_sync(idP);                           // previous round done with the tiles
-    {
+    if (!(PERSIST && sw > 0 && i == 0)) {
       const int c = lane;
       const long col = col0 + c;
       const bool okc = c < nt * 8 && col < a.N;
@@ -1488,6 +1513,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
       double cn[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) cn[i] = i < rv ? cp[(long)i * a.ld] : 0.0;
+      long long hmax = 0;                   // largest bit pattern stored (h >= 0: +inf is the only non-finite)
 #pragma unroll 1
       for (int b = 0; b < NB; ++b) {
         double bb[8];
@@ -1500,29 +1526,40 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
             cn[i] = k < rv ? cp[(long)k * a.ld] : 0.0;
           }
         }
+        // this block's lower triangle, half diagonal and inverse diagonal (broadcast loads)
+        double gc[48];
+        {
+          const double2* gb = reinterpret_cast<const double2*>(Gc + b * 48);
+#pragma unroll
+          for (int j = 0; j < 22; ++j) {
+            const double2 v = gb[j];
+            gc[2 * j] = v.x;
+            gc[2 * j + 1] = v.y;
+          }
+        }
         const long long c0 = PROF ? clock64() : 0;
         nb_sync(idS);
         const long long c1 = PROF ? clock64() : 0;
         if (PROF) pw[0] += c1 - c0;
+        double* hrow = Hs + 8 * b * 32;
         double x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           bb[i] = __dsub_rn(bb[i], Ss[i * WS_SLD + lane]);
-          x[i] = Hs[ws_pos(8 * b + i, lane)];
+          x[i] = hrow[i * 32 + hoff[i & 3]];
         }
-        const double* gd = Gdb + b * 64;
-        const double* gi8 = Gi + 8 * b;
         double hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int i = 0; i < (SKIP == 1 ? 0 : 8); ++i) {
-          const double t = __dmul_rn(bb[i], gi8[i]);
+          const double t = __dmul_rn(bb[i], gc[36 + i]);
           const double h = pos_part_ws(t);
           hv[i] = h;
 #pragma unroll
-          for (int l = i + 1; l < 8; ++l) bb[l] = fma(-gd[l * 8 + i], h, bb[l]);
-          Hs[ws_pos(8 * b + i, lane)] = h;
-          const double o = __dsub_rn(x[i], t), n = __dsub_rn(h, t);
-          gain = fma(gd[i * 9], __dsub_rn(__dmul_rn(o, o), __dmul_rn(n, n)), gain);
+          for (int l = i + 1; l < 8; ++l) bb[l] = fma(-gc[l * (l - 1) / 2 + i], h, bb[l]);
+          hrow[i * 32 + hoff[i & 3]] = h;
+          // G_kk((x-t)² - (h-t)²) = (x-h)(G_kk(x+h) - 2b_k), accumulated halved
+          const double u = __dsub_rn(x[i], h), v = __dadd_rn(x[i], h);
+          gain = fma(u, fma(gc[28 + i], v, -bb[i]), gain);
         }
         if (b + 1 < NB) nb_arrive(idH);
         if (PROF) pw[2] += clock64() - c1;
@@ -1530,11 +1567,58 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
         for (int i = 0; i < 8; ++i) {
           if (8 * b + i < rv) {
             hp[(long)(8 * b + i) * a.ld] = hv[i];
-            nf |= !isfinite(hv[i]);
+            const long long hb = __double_as_longlong(hv[i]);
+            hmax = hb > hmax ? hb : hmax;
           }
         }
       }
+      nf |= hmax >= 0x7FF0000000000000LL;
     }
+  }
+  if (!PERSIST) break;
+  // ---- grid-wide end of sweep `sw`: stall rule on the total gain ----
+  {
+    const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
+    const int bnf = __syncthreads_or(nf);
+    if (threadIdx.x == 0) {
+      a.part[blockIdx.x] = bg;
+      a.part_nf[blockIdx.x] = bnf;
+      __threadfence();
+      const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
+      s_flag = prev == (unsigned)(sw + 1) * gridDim.x - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_flag) {                           // last CTA: fixed-order total
+      __threadfence();
+      double v = 0.0;
+      int f = 0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) {
+        v = __dadd_rn(v, __ldcg(a.part + b));
+        f |= __ldcg(a.part_nf + b);
+      }
+      double total = block_reduce_sum_any(v, red);
+      f = __syncthreads_or(f);
+      if (threadIdx.x == 0) {
+        if (a.dv) dist::allreduce_gain(*a.dv, total, f, &total, &f);
+        finish_sweep(a, total, f);
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(&a.ctl->epoch), "r"((unsigned)(sw + 1))
+                     : "memory");
+      }
+    }
+    if (threadIdx.x == 0) {
+      unsigned e;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->epoch) : "memory");
+      } while (e < (unsigned)(sw + 1));
+      s_flag = *(volatile int*)&a.ctl->cont;
+    }
+    __syncthreads();
+    if (!s_flag) break;
+    gain = 0.0;
+    nf = 0;
+    src = a.H;
+  }
   }
   if (PROF && lane == 0) {
     double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 4;
@@ -1543,9 +1627,11 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
     o[2] = (double)(clock64() - tk0);
     o[3] = (double)pw[2];
   }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<256>(a, bg, nf, red);
+  if (!PERSIST) {
+    const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
+    nf = __syncthreads_or(nf);
+    last_block_reduce_n<256>(a, bg, nf, red);
+  }
 }
 
 // ---- bitwise-faithful sweep (hals_row_update_impl order) -----------------
@@ -1608,6 +1694,7 @@ __global__ void reset_ctl(HalsCtl* c, const DevState* st) {
   c->cont = 1;
   c->nonfinite = 0;
   c->arrive = 0;
+  c->epoch = 0;
 }
 
 }  // namespace hals
