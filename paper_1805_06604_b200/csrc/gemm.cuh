@@ -226,14 +226,20 @@ __global__ void __launch_bounds__(WMW * 4 * 32, 1) gemm_f64_dmma(Params p) {
 // CTA waiting at its k-block barrier no longer drains the SM's DMMA pipe
 // (the 128×128 single-CTA kernel above tops out at 79% DMMA-pipe activity,
 // profiles/r01_gemm_ncu.txt).
+// Tiles are stored unpadded with an XOR swizzle (16 KB per stage, 4 stages, still
+// three CTAs per SM): K-major element (row, k) at row·BK + (k ^ 4·(row & 3)),
+// N-major element (k, n) at k·BN + (n ^ nswz(k)); both keep 16-byte chunks whole
+// and make the 8-byte fragment loads conflict-free.
 namespace st {
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NTH = 128;
-constexpr int LDA_S = BK + 4;
-constexpr int LDB_N = BN + 4;
-constexpr int LDB_K = BK + 4;
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 4, NTH = 128;
+constexpr int LDA_S = BK;
+constexpr int LDB_N = BN;
+constexpr int LDB_K = BK;
 constexpr int A_STAGE = BM * LDA_S;
 constexpr int B_STAGE = (BN * LDB_K > BK * LDB_N) ? BN * LDB_K : BK * LDB_N;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(double);
+ENMF_DEV int kswz(int row) { return 4 * (row & 3); }
+ENMF_DEV int nswz(int k) { return 4 * (k & 1) + 8 * ((k >> 1) & 1); }
 }  // namespace st
 
 template <int VEC, int BKk, int NTHk>
@@ -246,8 +252,9 @@ ENMF_DEV void st_load_kmajor(double* s, int lds, const double* g, long ld, int r
     int valid = 0;
     if (gr < rows_valid && gk < K) valid = (K - gk >= VEC) ? VEC : (K - gk);
     const double* src = valid ? g + (long)gr * ld + gk : g;
-    if (VEC == 2) cp_async16(s + row * lds + col, src, valid * 8);
-    else cp_async8(s + row * lds + col, src, valid * 8);
+    double* d = s + row * lds + (col ^ st::kswz(row));
+    if (VEC == 2) cp_async16(d, src, valid * 8);
+    else cp_async8(d, src, valid * 8);
   }
 }
 template <int VEC>
@@ -259,8 +266,9 @@ ENMF_DEV void st_load_nmajor(double* s, const double* g, long ld, int k0, int K,
     int valid = 0;
     if (gk < K && gn < N) valid = (N - gn >= VEC) ? VEC : (N - gn);
     const double* src = valid ? g + (long)gk * ld + gn : g;
-    if (VEC == 2) cp_async16(s + row * st::LDB_N + col, src, valid * 8);
-    else cp_async8(s + row * st::LDB_N + col, src, valid * 8);
+    double* d = s + row * st::LDB_N + (col ^ st::nswz(row));
+    if (VEC == 2) cp_async16(d, src, valid * 8);
+    else cp_async8(d, src, valid * 8);
   }
 }
 
@@ -289,7 +297,33 @@ __global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_s(Params p) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // Interior tiles (the whole tile in range, K a multiple of BK, 16-byte rows): every
+  // thread's four 16-byte chunks per operand have fixed addresses up to the k offset.
+  const bool full = VEC == 2 && m0 + BM <= p.M && n0 + BN <= p.N && (p.K % BK) == 0;
+  const double* fa = p.A + (long)(m0 + (tid >> 3)) * p.lda + (long)kb0 * BK + (tid & 7) * 2;
+  const int sa = (tid >> 3) * LDA_S + (((tid & 7) * 2) ^ st::kswz(tid >> 3));
+  const double* fb = B_KMAJOR ? p.B + (long)(n0 + (tid >> 3)) * p.ldb + (long)kb0 * BK + (tid & 7) * 2
+                              : p.B + (long)(kb0 * BK + (tid >> 5)) * p.ldb + n0 + (tid & 31) * 2;
+  const int sb = B_KMAJOR ? (tid >> 3) * LDB_K + (((tid & 7) * 2) ^ st::kswz(tid >> 3))
+                          : (tid >> 5) * LDB_N + (((tid & 31) * 2) ^ st::nswz(tid >> 5));
   auto issue = [&](int kb, int stage) {
+    if (full) {
+      double* da = As + stage * A_STAGE + sa;
+      double* db = Bs + stage * B_STAGE + sb;
+      const double* ga = fa + (long)kb * BK;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cp_async16(da + i * 16 * LDA_S, ga + (long)i * 16 * p.lda, 16);
+      if (B_KMAJOR) {
+        const double* gb = fb + (long)kb * BK;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp_async16(db + i * 16 * LDB_K, gb + (long)i * 16 * p.ldb, 16);
+      } else {
+        const double* gb = fb + (long)kb * BK * p.ldb;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp_async16(db + i * 4 * LDB_N, gb + (long)i * 4 * p.ldb, 16);
+      }
+      return;
+    }
     const int k0 = (kb0 + kb) * BK;
     st_load_kmajor<VEC, BK, NTH>(As + stage * A_STAGE, LDA_S, p.A, p.lda, p.M, m0, k0, p.K, BM);
     if (B_KMAJOR) st_load_kmajor<VEC, BK, NTH>(Bs + stage * B_STAGE, LDB_K, p.B, p.ldb, p.N, n0, k0, p.K, BN);
@@ -308,16 +342,18 @@ __global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_s(Params p) {
       if (nxt < nk) issue(nxt, nxt % STAGES);
       cp_commit();
     }
-    const double* as = As + (kb % STAGES) * A_STAGE + (wm * 32 + g) * LDA_S + t;
+    // rows wm·32 + mi·8 + g (K-major) share row & 3 = g & 3; N-major k-rows kk·4 + t share k & 3 = t
+    const double* as = As + (kb % STAGES) * A_STAGE + (wm * 32 + g) * LDA_S;
     const double* bs = Bs + (kb % STAGES) * B_STAGE;
     double a[2][4], b[2][4];
     auto load_frag = [&](int kk, int buf) {
+      const int kq = 4 * (kk ^ (g & 3)) + t;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = as[mi * 8 * LDA_S + kk * 4];
+      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = as[mi * 8 * LDA_S + kq];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
-        if (B_KMAJOR) b[buf][ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kk * 4 + t];
-        else b[buf][ni] = bs[(kk * 4 + t) * LDB_N + wn * 32 + ni * 8 + g];
+        if (B_KMAJOR) b[buf][ni] = bs[(wn * 32 + ni * 8 + g) * LDB_K + kq];
+        else b[buf][ni] = bs[(kk * 4 + t) * LDB_N + ((wn * 32 + ni * 8 + g) ^ st::nswz(t))];
       }
     };
     load_frag(0, 0);
