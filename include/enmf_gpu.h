@@ -135,6 +135,11 @@ int enmf_gpu_run_csr(enmf_gpu_ctx* ctx, const uint64_t* offsets, const uint64_t*
                      const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
                      size_t* n_iters, double* w_out, double* h_out, double* norm_x);
 
+/* Upload a CSR X (validated as SparseMatrix::validate, matrix.hpp:226-251) for
+ * enmf_gpu_solve / enmf_gpu_begin; keeps a CSC copy on the device for W_yᵀX. */
+int enmf_gpu_load_csr(enmf_gpu_ctx* ctx, const uint64_t* offsets, const uint64_t* col_idx,
+                      const double* vals, size_t m, size_t n, size_t nnz);
+
 /* ---- resident-data API (bench / repeated solves on one X) -------------------
  * Upload X once (from host or from a device pointer), then solve from device
  * or host factors.  *_device pointers are CUDA device pointers. */

@@ -63,7 +63,7 @@ EXPORTS = [
     "enmf_gpu_active_set_solve", "enmf_gpu_begin", "enmf_gpu_step", "enmf_gpu_step_profiled",
     "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream",
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
-    "enmf_gpu_dist_finalize",
+    "enmf_gpu_dist_finalize", "enmf_gpu_load_csr",
 ]
 
 _lib = None
@@ -95,6 +95,7 @@ def load() -> C.CDLL:
     L.enmf_gpu_run_dense.argtypes = [vp, dp, sz, sz, dp, dp] + run_tail
     L.enmf_gpu_run_csr.argtypes = [vp, dp, dp, dp, sz, sz, sz, dp, dp] + run_tail
     L.enmf_gpu_load_dense.argtypes = [vp, dp, sz, sz, C.c_int]
+    L.enmf_gpu_load_csr.argtypes = [vp, dp, dp, dp, sz, sz, sz]
     L.enmf_gpu_solve.argtypes = [vp, dp, dp, sz, C.c_int, C.POINTER(CConfig), C.POINTER(CIter), sz,
                                  C.POINTER(sz), dp, dp, C.POINTER(C.c_double)]
     L.enmf_gpu_set_precision.argtypes = [vp, C.c_int]

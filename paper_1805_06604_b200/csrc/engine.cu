@@ -28,6 +28,7 @@
 #include "gemm.cuh"
 #include "hals.cuh"
 #include "misc.cuh"
+#include "sparse.cuh"
 
 namespace {
 
@@ -80,6 +81,12 @@ struct enmf_gpu_ctx {
   DBuf<double> x_own;
   const double* x = nullptr;
   size_t m = 0, n = 0;
+  // CSR data matrix (enmf_gpu_load_csr): CSR for X·Tᵀ, CSC copy for W_yᵀX
+  bool sparse = false;
+  size_t nnz = 0;
+  DBuf<long long> csr_ptr, csc_ptr;
+  DBuf<int> csr_idx, csc_idx;
+  DBuf<double> csr_val, csc_val, rowmaj;
   // factors and products
   DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch, Gf;
   DBuf<double> partials, gain_part, terms, ddpart, dd;
@@ -359,7 +366,7 @@ int hals_variant() {
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
       : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "" ? 54 : 11;  // default: ws
+      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "" ? 54 : 11;  // default: ws
   }
   return v;
 }
@@ -399,6 +406,14 @@ template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
 void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
   const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 15) / 16));
+  if (PROF) {
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute((const void*)hals::sweep_ws<R_, true, SKIP, PERSIST>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, hals::ws_smem_bytes<R_>()));
+      attr = true;
+    }
+  }
   if (PERSIST) {
     // every CTA must be resident for the grid-wide decision between sweeps
     cudaLaunchConfig_t lc = {};
@@ -411,16 +426,8 @@ void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&lc, hals::sweep_ws<R_, false, 0, true>, a, ntiles));
+    CU(cudaLaunchKernelEx(&lc, hals::sweep_ws<R_, PROF, SKIP, true>, a, ntiles));
     return;
-  }
-  if (PROF) {
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute((const void*)hals::sweep_ws<R_, true, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              hals::ws_smem_bytes<R_>()));
-      attr = true;
-    }
   }
   hals::sweep_ws<R_, PROF, SKIP><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
@@ -563,6 +570,12 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     launch_sweep_ws<128, true, 1>(c, s, a);
   } else if (hals_variant() == 53) {
     launch_sweep_ws<128, true, 2>(c, s, a);
+  } else if (hals_variant() == 55) {   // timing experiments (persistent): profile, no row pass, no DMMA
+    launch_sweep_ws<128, true, 0, true>(c, s, a);
+  } else if (hals_variant() == 56) {
+    launch_sweep_ws<128, true, 1, true>(c, s, a);
+  } else if (hals_variant() == 57) {
+    launch_sweep_ws<128, true, 2, true>(c, s, a);
   } else if (hals_variant() == 54) {
     if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
@@ -748,9 +761,44 @@ void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
   if (p) CU(cudaEventRecord(p->ev[phase], s));
 }
 
+// CSR products (sparse.cuh): the r-major factor is transposed into the row-major
+// scratch, then gathered once per stored entry in the reference's order.
+void sparse_gather(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const long long* ptr, const int* idx,
+                   const double* val, long lines, const double* Frm, int r, double* out, const DevState* st) {
+  const long warps = std::max<long>(1, lines);
+  const unsigned grid = (unsigned)std::min<long>((warps + 7) / 8, (long)c->sms * 16);
+  if (exact) sparse::gather_lines<true><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
+  else sparse::gather_lines<false><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
+  CUK();
+  c->launches++;
+}
+
+void transpose_launch(enmf_gpu_ctx* c, cudaStream_t s, const double* in, double* out, long rows, long cols) {
+  dim3 tb(32, 8), tg((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  misc::transpose<<<tg, tb, 0, s>>>(in, out, (int)rows, (int)cols);
+  CUK();
+  c->launches++;
+}
+
+// (X·Tᵀ)ᵀ (r×m) for CSR X, T r×n  (linalg.hpp:127-146)
+void sparse_xht(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* Tm, int r, double* out,
+                const DevState* st) {
+  c->rowmaj.ensure(std::max(c->m, c->n) * (size_t)r);
+  transpose_launch(c, s, Tm, c->rowmaj.p, r, (long)c->n);
+  sparse_gather(c, s, exact, c->csr_ptr.p, c->csr_idx.p, c->csr_val.p, (long)c->m, c->rowmaj.p, r, out, st);
+}
+
+// W_yᵀX (r×n) for CSR X (through the CSC copy), W_yᵀ r×m  (linalg.hpp:86-104)
+void sparse_wx(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* WyT, int r, double* out,
+               const DevState* st) {
+  c->rowmaj.ensure(std::max(c->m, c->n) * (size_t)r);
+  transpose_launch(c, s, WyT, c->rowmaj.p, r, (long)c->m);
+  sparse_gather(c, s, exact, c->csc_ptr.p, c->csc_idx.p, c->csc_val.p, (long)c->n, c->rowmaj.p, r, out, st);
+}
+
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
 void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
-  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 54)) return;
+  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 57)) return;
   constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
   c->Gf.ensure(3 * kGf);
   double* gf = c->Gf.p + slot * kGf;
@@ -902,7 +950,9 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   dist_allreduce(c, s, L, c->GH.p, r * r, st);
   fixup(c->WyT.p, ml, L.row0, m, 0, c->GH.p, 0);
   mark(c, s, prof, 1);
-  if (pl.prec == PREC_EXACT) {
+  if (c->sparse) {
+    sparse_wx(c, s, pl.prec == PREC_EXACT, c->WyT.p, r, c->CH.p, st);
+  } else if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
     c->launches++;
@@ -932,7 +982,9 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   fixup(T, nl, L.col0, n, 1, c->GW.p, 1);
   mark(c, s, prof, 5);
   auto cross_xht = [&](const double* Tm, double* out) {
-    if (pl.prec == PREC_EXACT) {
+    if (c->sparse) {
+      sparse_xht(c, s, pl.prec == PREC_EXACT, Tm, r, out, st);
+    } else if (pl.prec == PREC_EXACT) {
       gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
       CUK();
       c->launches++;
@@ -1011,7 +1063,8 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   close_session(c);
   validate_cfg(cfg);
   const DistHost* D = (c->dist && c->dist->ready) ? c->dist : nullptr;
-  if (!D && !c->x) throw Fail{ENMF_INVALID_ARGUMENT, "run: no data matrix loaded"};
+  if (!D && !c->x && !c->sparse) throw Fail{ENMF_INVALID_ARGUMENT, "run: no data matrix loaded"};
+  if (D && c->sparse) throw Fail{ENMF_INVALID_ARGUMENT, "run: the sharded engine takes dense data only"};
   if (D && (!D->xc || !D->xr)) throw Fail{ENMF_INVALID_ARGUMENT, "run: no sharded data loaded"};
   if (D && cfg->precision == PREC_EXACT)
     throw Fail{ENMF_INVALID_ARGUMENT, "the bitwise-faithful precision is single-GPU only"};
@@ -1103,7 +1156,8 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   pl.inner_h = cfg->inner_h; pl.inner_w = cfg->inner_w; pl.hp = cfg->hp;
   pl.extrap = cfg->extrapolation_enabled ? 1 : 0;
   pl.literal = cfg->literal_hp1_order ? 1 : 0;
-  const double setup = (double)m * (double)n * (double)r;  // setup_flop_estimate (engine.hpp:242-244)
+  // setup_flop_estimate (engine.hpp:242-248): m·n·r dense, nnz·r sparse
+  const double setup = c->sparse ? (double)c->nnz * (double)r : (double)m * (double)n * (double)r;
   pl.max_sweeps_h = derive_sweeps(cfg, setup, n, r);
   pl.max_sweeps_w = derive_sweeps(cfg, setup, m, r);
   pl.stall = cfg->inner_stall_fraction;
@@ -1115,8 +1169,9 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   const Layout L = make_layout(c, pl);
 
   // ||X||^2 (linalg.hpp:160-171) and e(0) (engine.hpp:487-503)
-  const double* xnorm = D ? D->xr : c->x;   // multi-GPU: the row blocks partition X
-  const long xs = (long)ml * n;
+  // (CSR: the stored values in storage order, linalg.hpp:167-171)
+  const double* xnorm = c->sparse ? c->csr_val.p : D ? D->xr : c->x;   // multi-GPU: the row blocks partition X
+  const long xs = c->sparse ? (long)c->nnz : (long)ml * n;
   if (pl.prec == PREC_EXACT) {
     misc::neumaier_exact<<<1, 32, 0, s>>>(xnorm, nullptr, xs, 0, 0, 0, c->dd.p + 2, nullptr);
     c->launches++;
@@ -1134,7 +1189,9 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   dist_allreduce(c, s, L, c->GW.p, (int)(r * r), st);
   dist_gather(c, s, L, c->H.p, (int)r, 1, pl, st);       // H0 replica for X·H0ᵀ
   dist_gather(c, s, L, c->WT.p, (int)r, 0, pl, st);      // W0ᵀ replica for iteration 1's W_yᵀX
-  if (pl.prec == PREC_EXACT) {
+  if (c->sparse) {
+    sparse_xht(c, s, pl.prec == PREC_EXACT, c->H.p, (int)r, c->P.p, st);
+  } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);
     CUK();

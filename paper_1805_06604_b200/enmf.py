@@ -265,6 +265,39 @@ class Context:
                                             C.byref(nit), _p(w), _p(h), C.byref(nx)))
         return RunRecord(_records(iters, min(nit.value, cap)), FactorPair(w, h), nx.value)
 
+    def run_csr(self, offsets, col_idx, vals, m: int, n: int, w0, h0, cfg: SolverConfig,
+                timing: TimingMode = TimingMode.wall) -> RunRecord:
+        """enmf::run<SparseMatrix> (engine.hpp:447-521 with linalg.hpp:86-104,127-146,167-171).
+        offsets (m+1) / col_idx (nnz) as uint64, vals (nnz) float64: the SparseMatrix CSR arrays."""
+        self.load_csr(offsets, col_idx, vals, m, n)
+        return self._solve_host(w0, h0, m, n, cfg, timing)
+
+    def load_csr(self, offsets, col_idx, vals, m: int, n: int) -> None:
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.uint64)
+        v = _f64(vals, "vals")
+        if off.shape != (m + 1,) or ci.shape != v.shape:
+            raise InvalidArgument("SparseMatrix: inconsistent compressed storage")
+        _check(self._lib.enmf_gpu_load_csr(self._h, off.ctypes.data, ci.ctypes.data, v.ctypes.data, m, n, v.size))
+
+    def _solve_host(self, w0, h0, m, n, cfg: SolverConfig, timing: TimingMode) -> RunRecord:
+        w0, h0 = _f64(w0, "w0"), _f64(h0, "h0")
+        r = w0.shape[1]
+        if w0.shape[1] != h0.shape[0]:
+            raise InvalidArgument("run: factor inner dimensions disagree")
+        if w0.shape[0] != m or h0.shape[1] != n:
+            raise InvalidArgument("run: factor shapes do not match the data matrix")
+        c = cfg.to_c(timing)
+        cap = int(cfg.max_outer_iterations) + 1
+        iters = (L.CIter * cap)()
+        nit = C.c_size_t(0)
+        w = np.empty((m, r))
+        h = np.empty((r, n))
+        nx = C.c_double(0)
+        _check(self._lib.enmf_gpu_solve(self._h, _p(w0), _p(h0), r, 0, C.byref(c), iters, cap, C.byref(nit),
+                                        _p(w), _p(h), C.byref(nx)))
+        return RunRecord(_records(iters, min(nit.value, cap)), FactorPair(w, h), nx.value)
+
     def load_device(self, x_ptr: int, m: int, n: int) -> None:
         """Borrow a device-resident X (e.g. torch.Tensor.data_ptr())."""
         _check(self._lib.enmf_gpu_load_dense(self._h, C.c_void_p(x_ptr), m, n, 1))
@@ -403,6 +436,12 @@ def default_context() -> Context:
 def run(x, w0, h0, cfg: SolverConfig, timing: TimingMode = TimingMode.wall) -> RunRecord:
     """enmf::run (engine.hpp:447-521) on the calling thread's GPU context."""
     return default_context().run(x, w0, h0, cfg, timing)
+
+
+def run_csr(offsets, col_idx, vals, m, n, w0, h0, cfg: SolverConfig,
+            timing: TimingMode = TimingMode.wall) -> RunRecord:
+    """enmf::run<SparseMatrix> on the calling thread's GPU context."""
+    return default_context().run_csr(offsets, col_idx, vals, m, n, w0, h0, cfg, timing)
 
 
 def gram(a):

@@ -33,8 +33,36 @@ def save_run(R, tag, x, w0, h0, cfg, meta):
     meta[tag]["restarts"] = int(rec["restarted"].sum())
 
 
+def csr_fixtures(R, meta):
+    """C4-shaped CSR (gen_docs: lognormal document lengths, Zipf term ids, tf·idf, L2 columns)
+    at 300×120, r=6, through enmf::run<SparseMatrix> (linalg.hpp:86-146)."""
+    gen = Oracle("port")       # data generator only (orc_gen_docs); the runs are the reference's
+    off, cidx, vals = gen.gen_docs(300, 120, 4)
+    m, n, r = 300, 120, 6
+    w0, h0 = R.random_init(m, n, r, 9)
+    np.savez_compressed(os.path.join(OUT, "csr_inputs.npz"), off=off, cidx=cidx, vals=vals, w0=w0, h0=h0,
+                        m=m, n=n)
+    for name in ["e-ahals-hp3", "e-anls-hp1"]:
+        cfg = preset(name, max_outer_iterations=40)
+        rec, w, h, nx = R.run_csr(off, cidx, vals, m, n, w0, h0, cfg)
+        tag = f"csr_{name}"
+        np.savez_compressed(os.path.join(OUT, f"{tag}.npz"), error=rec["error"],
+                            relative_error=rec["relative_error"], beta=rec["beta"],
+                            restarted=rec["restarted"], w=w, h=h, norm_x=nx)
+        meta[tag] = {k: getattr(cfg, k) for k, _ in cfg._fields_}
+        meta[tag]["final_relative_error"] = float(rec["relative_error"][-1])
+
+
 def main():
     R = Oracle("reference")
+    if len(sys.argv) > 1 and sys.argv[1] == "--csr-only":
+        with open(os.path.join(OUT, "golden.json")) as f:
+            meta = json.load(f)
+        csr_fixtures(R, meta)
+        with open(os.path.join(OUT, "golden.json"), "w") as f:
+            json.dump(meta, f, indent=1, sort_keys=True, default=float)
+        print("wrote CSR fixtures")
+        return
     meta = {}
     # Config 1 (BASELINE.json configs[0]): gen_lowrank(200,200,20,seed=1), random_init(...,seed=2), 200 iterations.
     x = R.gen_lowrank(200, 200, 20, 1)
@@ -78,6 +106,7 @@ def main():
     ha, _ = R.active_set_solve(G, Cm, np.abs(h0k))
     np.savez_compressed(os.path.join(OUT, "kernels.npz"), w=wk, x=xk, gram=G, cross=Cm,
                         xht=R.cross_xht(xk, g.random((12, 30))), h0=h0k, hals=hh, bpp=ha)
+    csr_fixtures(R, meta)
     # Known answers quoted in SURVEY.md §6.2 for config 1 (hp3 / hp1).
     meta["known_answers"] = {"c1_e-ahals-hp3_final_relative_error": 7.8674950787740083e-4,
                              "c1_e-ahals-hp1_final_relative_error": 1.2721814731209598e-3,

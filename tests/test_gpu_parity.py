@@ -339,3 +339,53 @@ def test_sharded_engine_world1_matches_single(ctx, port, alg, shape):
     assert np.max(np.abs(e - es) / es) <= 1e-9
     assert np.max(np.abs(w - single.factors.w)) <= 1e-6 * np.max(np.abs(single.factors.w))
     assert np.max(np.abs(h - single.factors.h)) <= 1e-6 * np.max(np.abs(single.factors.h))
+
+
+# ------------------------------------------------------------ CSR
+def _csr_inputs(golden):
+    inp = golden.load("csr_inputs")
+    return inp["off"], inp["cidx"], inp["vals"], int(inp["m"]), int(inp["n"]), inp["w0"], inp["h0"]
+
+
+@pytest.mark.parametrize("name", ["e-ahals-hp3", "e-anls-hp1"])
+def test_csr_exact_mode_bitwise_vs_reference(ctx, golden, name):
+    """enmf::run<SparseMatrix> (linalg.hpp:86-146): the CSR gathers in the reference's order."""
+    off, cidx, vals, m, n, w0, h0 = _csr_inputs(golden)
+    rec = ctx.run_csr(off, cidx, vals, m, n, w0, h0, _cfg(name, 40, E.Precision.fp64_exact), E.TimingMode.none)
+    assert_bitwise(rec, golden.load(f"csr_{name}"))
+
+
+@pytest.mark.parametrize("name", ["e-ahals-hp3", "e-anls-hp1"])
+def test_csr_fast_mode_parity(ctx, golden, name):
+    off, cidx, vals, m, n, w0, h0 = _csr_inputs(golden)
+    g = golden.load(f"csr_{name}")
+    rec = ctx.run_csr(off, cidx, vals, m, n, w0, h0, _cfg(name, 40), E.TimingMode.none)
+    assert_parity(rec, g["error"], g["restarted"], g["w"], g["h"], float(g["norm_x"]))
+
+
+def test_c4_shaped_csr_parity(ctx, port):
+    """BASELINE config 4 shape at 1/4 scale (7500×2500 documents, r=20, E-A-HALS hp3): vs the oracle."""
+    m, n, r = 7500, 2500, 20
+    off, cidx, vals = port.gen_docs(m, n, 11)
+    w0, h0 = port.random_init(m, n, r, 12)
+    ref = port.run_csr(off, cidx, vals, m, n, w0, h0, preset("e-ahals-hp3", max_outer_iterations=10))
+    rec = ctx.run_csr(off, cidx, vals, m, n, w0, h0, _cfg("e-ahals-hp3", 10), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+
+
+def test_csr_validation_errors(ctx):
+    """SparseMatrix::validate (matrix.hpp:226-251): same failures, InvalidArgument."""
+    w0 = np.ones((3, 2))
+    h0 = np.ones((2, 4))
+    cfg = _cfg("e-ahals-hp3", 2)
+    bad = [
+        (np.array([0, 2, 1, 3], np.uint64), np.array([0, 1, 2], np.uint64), np.ones(3)),   # offsets decrease
+        (np.array([0, 1, 2, 3], np.uint64), np.array([0, 7, 2], np.uint64), np.ones(3)),   # column out of range
+        (np.array([0, 2, 2, 3], np.uint64), np.array([1, 1, 2], np.uint64), np.ones(3)),   # not increasing in a row
+        (np.array([0, 1, 2, 3], np.uint64), np.array([0, 1, 2], np.uint64), np.array([1.0, np.nan, 1.0])),
+        (np.array([0, 1, 2, 4], np.uint64), np.array([0, 1, 2], np.uint64), np.ones(3)),   # offsets[m] != nnz
+    ]
+    for off, ci, v in bad:
+        with pytest.raises(E.InvalidArgument):
+            ctx.run_csr(off, ci, v, 3, 4, w0, h0, cfg, E.TimingMode.none)

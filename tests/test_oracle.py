@@ -182,3 +182,15 @@ def test_port_csr_vs_reference(port, ref):
     b = ref.run_csr(off, cidx, vals, m, n, w0, h0, cfg)
     assert np.array_equal(a[0]["error"], b[0]["error"])
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("name", ["e-ahals-hp3", "e-anls-hp1"])
+def test_port_csr_vs_golden(port, golden, name):
+    """The C restatement's CSR path is bitwise the reference's (fixtures from the reference)."""
+    inp = golden.load("csr_inputs")
+    g = golden.load(f"csr_{name}")
+    rec, w, h, nx = port.run_csr(inp["off"], inp["cidx"], inp["vals"], int(inp["m"]), int(inp["n"]),
+                                 inp["w0"], inp["h0"], preset(name, max_outer_iterations=40))
+    assert np.array_equal(rec["error"], g["error"])
+    assert np.array_equal(rec["restarted"].astype(np.int32), g["restarted"].astype(np.int32))
+    assert np.array_equal(w, g["w"]) and np.array_equal(h, g["h"]) and nx == float(g["norm_x"])
