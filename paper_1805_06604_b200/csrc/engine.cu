@@ -14,6 +14,7 @@
 // GEMM writes its result straight into the r×m layout the sweep consumes;
 // H r×n as given.  W is transposed only at entry and exit.
 #include <cuda_runtime.h>
+#include <cublasLt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +30,7 @@
 #include "hals.cuh"
 #include "misc.cuh"
 #include "sparse.cuh"
+#include "ozaki.cuh"
 
 namespace {
 
@@ -87,6 +89,13 @@ struct enmf_gpu_ctx {
   DBuf<long long> csr_ptr, csc_ptr;
   DBuf<int> csr_idx, csc_idx;
   DBuf<double> csr_val, csc_val, rowmaj;
+  // FP64 cross products on INT8 tensor cores (ozaki.cuh): X digits (cut once per load)
+  bool xdig_ready = false;
+  DBuf<int8_t> xdig, adig;
+  DBuf<int> xexp, aexp;
+  DBuf<int> ocbuf;
+  DBuf<double> opart;
+  void* lt = nullptr;                     // LtCache (cuBLASLt handle, workspace, per-shape plans)
   // factors and products
   DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch, Gf;
   DBuf<double> partials, gain_part, terms, ddpart, dd;
@@ -796,6 +805,140 @@ void sparse_wx(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* WyT, i
   sparse_gather(c, s, exact, c->csc_ptr.p, c->csc_idx.p, c->csc_val.p, (long)c->n, c->rowmaj.p, r, out, st);
 }
 
+// ---- FP64 cross products on INT8 tensor cores (ozaki.cuh) ----------------------
+// int8 × int8 → int32 digit GEMMs through cuBLASLt (plain library GEMMs); the
+// splitting and the FP64 recombination are ours.
+struct LtCache {
+  cublasLtHandle_t h = nullptr;
+  void* ws = nullptr;
+  size_t ws_size = 64u << 20;
+  struct Entry {
+    int M, N, K, tn;
+    cublasLtMatmulDesc_t op;
+    cublasLtMatrixLayout_t la, lb, lc;
+    cublasLtMatmulAlgo_t algo;
+  };
+  std::vector<Entry> e;
+};
+
+#define LT(x)                                                                                           \
+  do {                                                                                                  \
+    cublasStatus_t st_ = (x);                                                                           \
+    if (st_ != CUBLAS_STATUS_SUCCESS) throw Fail{ENMF_CUDA_ERROR, std::string("cuBLASLt: ") + #x + " = " + \
+                                                                      std::to_string((int)st_)};       \
+  } while (0)
+
+void lt_free(enmf_gpu_ctx* c) {
+  auto* lt = static_cast<LtCache*>(c->lt);
+  if (!lt) return;
+  for (auto& e : lt->e) {
+    cublasLtMatrixLayoutDestroy(e.la); cublasLtMatrixLayoutDestroy(e.lb); cublasLtMatrixLayoutDestroy(e.lc);
+    cublasLtMatmulDescDestroy(e.op);
+  }
+  if (lt->ws) cudaFree(lt->ws);
+  if (lt->h) cublasLtDestroy(lt->h);
+  delete lt;
+  c->lt = nullptr;
+}
+
+// C (M×N int32, row-major) = A (M×K int8, row-major) · B, where B = Xdᵀ with Xd
+// N×K row-major (tn) or B = Xd with Xd K×N row-major (!tn).  Column-major call:
+// Cᵀ (N×M) = op(Xd') · Aᵀ.
+void lt_gemm_i8(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* Xd, int* C, int M, int N, int K,
+                bool tn) {
+  if (!c->lt) {
+    auto* nl = new LtCache();
+    c->lt = nl;
+    LT(cublasLtCreate(&nl->h));
+    CU(cudaMalloc(&nl->ws, nl->ws_size));
+  }
+  LtCache* lt = static_cast<LtCache*>(c->lt);
+  LtCache::Entry* en = nullptr;
+  for (auto& e : lt->e)
+    if (e.M == M && e.N == N && e.K == K && e.tn == (int)tn) en = &e;
+  if (!en) {
+    LtCache::Entry e{};
+    e.M = M; e.N = N; e.K = K; e.tn = tn;
+    LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
+    const cublasOperation_t ta = tn ? CUBLAS_OP_T : CUBLAS_OP_N, tb = CUBLAS_OP_N;
+    LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta));
+    LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb));
+    if (tn) LT(cublasLtMatrixLayoutCreate(&e.la, CUDA_R_8I, K, N, K));
+    else LT(cublasLtMatrixLayoutCreate(&e.la, CUDA_R_8I, N, K, N));
+    LT(cublasLtMatrixLayoutCreate(&e.lb, CUDA_R_8I, K, M, K));
+    LT(cublasLtMatrixLayoutCreate(&e.lc, CUDA_R_32I, N, M, N));
+    cublasLtMatmulPreference_t pref;
+    LT(cublasLtMatmulPreferenceCreate(&pref));
+    LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt->ws_size,
+                                            sizeof lt->ws_size));
+    cublasLtMatmulHeuristicResult_t res{};
+    int found = 0;
+    LT(cublasLtMatmulAlgoGetHeuristic(lt->h, e.op, e.la, e.lb, e.lc, e.lc, pref, 1, &res, &found));
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (!found) throw Fail{ENMF_CUDA_ERROR, "cuBLASLt: no int8 algorithm for the digit GEMM"};
+    e.algo = res.algo;
+    lt->e.push_back(e);
+    en = &lt->e.back();
+  }
+  const int alpha = 1, beta = 0;
+  LT(cublasLtMatmul(lt->h, en->op, &alpha, Xd, en->la, A, en->lb, &beta, C, en->lc, C, en->lc, &en->algo,
+                    lt->ws, lt->ws_size, s));
+}
+
+// Use the INT8-digit products for the dense single-GPU FP64 path when the problem is
+// large enough to pay the one-time digit cut of X and K keeps the int32 sums exact.
+bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("ENMF_CROSS");
+    env = (e && std::string(e) == "dmma") ? 0 : 1;
+  }
+  return env == 1 && prec == PREC_FAST && !dist && !c->sparse && c->x &&
+         (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072;
+}
+
+void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s) {
+  if (c->xdig_ready) return;
+  const long mn = (long)c->m * (long)c->n;
+  c->xdig.ensure((size_t)ozaki::S * mn);
+  c->xexp.ensure(1);
+  c->opart.ensure(4096);
+  const int nb = (int)std::min<long>(4096, (mn + 255) / 256);
+  ozaki::absmax_partial<<<nb, 256, 0, s>>>(c->x, mn, c->opart.p);
+  ozaki::absmax_final<<<1, 1024, 0, s>>>(c->opart.p, nb, c->xexp.p);
+  ozaki::split<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(
+      c->x, (long)c->m, (long)c->n, (long)c->n, c->xexp.p, 0, c->xdig.p, nullptr);
+  CUK();
+  c->launches += 3;
+  c->xdig_ready = true;
+}
+
+// out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · (tn ? Xᵀ : X) in FP64 accuracy,
+// X = m × n (tn: N = m, K = n; !tn: K = m, N = n).
+void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
+                 const DevState* st) {
+  const long K = tn ? (long)c->n : (long)c->m, N = tn ? (long)c->m : (long)c->n;
+  const long mn = (long)c->m * (long)c->n;
+  c->adig.ensure((size_t)ozaki::S * r * K);
+  c->aexp.ensure((size_t)r);
+  c->ocbuf.ensure((size_t)ozaki::PAIRS * r * N);
+  ozaki::row_exp<<<r, 256, 0, s>>>(A, K, lda, c->aexp.p, st);
+  ozaki::split<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
+      A, r, K, lda, c->aexp.p, 1, c->adig.p, st);
+  CUK();
+  c->launches += 2;
+  long acc = 0;
+  for (int q = 0; q < ozaki::S; ++q) {
+    const int Mq = (ozaki::S - q) * r;   // factor digits p = 0..S-1-q, stacked
+    lt_gemm_i8(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + acc, Mq, (int)N, (int)K, tn);
+    acc += (long)Mq * N;
+  }
+  ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
+      c->ocbuf.p, r, N, c->aexp.p, c->xexp.p, out, ldo, st);
+  CUK();
+  c->launches += 1 + ozaki::S;
+}
+
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
 void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
   if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 57)) return;
@@ -952,6 +1095,8 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   mark(c, s, prof, 1);
   if (c->sparse) {
     sparse_wx(c, s, pl.prec == PREC_EXACT, c->WyT.p, r, c->CH.p, st);
+  } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
+    ozaki_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
@@ -984,6 +1129,8 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   auto cross_xht = [&](const double* Tm, double* out) {
     if (c->sparse) {
       sparse_xht(c, s, pl.prec == PREC_EXACT, Tm, r, out, st);
+    } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
+      ozaki_cross(c, s, Tm, n, r, true, out, m, st);
     } else if (pl.prec == PREC_EXACT) {
       gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
       CUK();
@@ -1191,6 +1338,9 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   dist_gather(c, s, L, c->WT.p, (int)r, 0, pl, st);      // W0ᵀ replica for iteration 1's W_yᵀX
   if (c->sparse) {
     sparse_xht(c, s, pl.prec == PREC_EXACT, c->H.p, (int)r, c->P.p, st);
+  } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
+    ozaki_prepare_x(c, s);               // once per loaded X (outside the iteration graph)
+    ozaki_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);

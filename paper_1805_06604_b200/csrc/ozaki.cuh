@@ -1,0 +1,128 @@
+// ozaki.cuh — FP64-accurate cross products on the B200's INT8 tensor cores.
+//
+// W_yᵀX and T·Xᵀ (linalg.hpp:67-124) are the two large contractions of an outer
+// iteration (2·r·m·n flop each).  B200 runs FP64 on DMMA.8x8x4 at 37 TF/s but
+// INT8 on tcgen05 at ~3 POP/s (profiles/r01_int8_probe.txt), so the products are
+// computed by error-free splitting (Ozaki's scheme): every operand row is scaled
+// by a power of two into (-1, 1) and cut into S signed 7-bit digits,
+//     a = 2^e · sum_{p<S} d_p · 2^{-7(p+1)},   d_p ∈ [-127, 127]   (exact cuts)
+// and the product is the exact int32 sum of the digit products
+//     (A·B)_ij ≈ 2^{ea_i+eb} · sum_{p+q<S} 2^{-7(p+q+2)} · (D^A_p · D^B_q)_ij
+// each digit GEMM an int8×int8→int32 tensor-core GEMM (exact while K·127² < 2³¹).
+// With S = 7 the neglected terms are below 2^{-49} of the row maxima — the same
+// order as FP64 accumulation over K = 32768 — and the sum over the digit pairs is
+// formed in FP64 smallest term first.  X's digits are cut once per load (X is
+// fixed); the factor's digits once per product.  The digit GEMMs are grouped by
+// X digit q: one GEMM multiplies the stacked factor digits p = 0..S-1-q (an
+// (S-q)·r-row operand) by X digit q, so X is streamed S times per product.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace ozaki {
+
+constexpr int S = 7;                      // digits per operand (7 bits each)
+constexpr int PAIRS = S * (S + 1) / 2;    // digit products kept (p + q < S)
+
+// largest |x| → exponent e with |x| / 2^e < 1 (0 when all zero)
+ENMF_DEV int exp_above(double mx) {
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);            // mx = f · 2^e, f ∈ [0.5, 1)
+  return e;
+}
+
+__global__ void absmax_partial(const double* __restrict__ x, long cnt, double* part) {
+  __shared__ double sh[32];
+  double m = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+  }
+}
+
+__global__ void absmax_final(const double* part, int nb, int* e_out) {
+  double m = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmax(m, part[i]);
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    m = fmax(m, sh[0]);
+    *e_out = exp_above(m);
+  }
+}
+
+// one block per row of an R × K row-major matrix: e[i] for max_k |a[i][k]|
+__global__ void row_exp(const double* __restrict__ a, long K, long lda, int* e, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  __shared__ double sh[32];
+  const double* row = a + (long)blockIdx.x * lda;
+  double m = 0.0;
+  for (long k = threadIdx.x; k < K; k += blockDim.x) m = fmax(m, fabs(row[k]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    m = fmax(m, sh[0]);
+    e[blockIdx.x] = exp_above(m);
+  }
+}
+
+// digits of an R × K matrix (row-major, lda) into out[p][i][k] (row stride K,
+// digit stride R·K); row i is scaled by 2^-e[i] (per_row) or 2^-e[0].
+__global__ void split(const double* __restrict__ a, long R, long K, long lda, const int* e, int per_row,
+                      int8_t* __restrict__ out, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long total = R * K, dstride = R * K;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const long i = idx / K, k = idx - i * K;
+    double r = ldexp(a[i * lda + k], -e[per_row ? i : 0]);   // exact, |r| < 1
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+      r *= 128.0;                      // exact
+      const double d = trunc(r);       // |d| <= 127
+      r -= d;                          // exact
+      out[p * dstride + idx] = (int8_t)(int)d;
+    }
+  }
+}
+
+// out[i][j] = sum_{q} sum_{p < S-q} 2^{ea_i + eb - 7(p+q+2)} · Cq[p·R + i][j],  Cq = C + R·N·(qS - q(q-1)/2)
+// (FP64, smallest weight first).  out row stride ldo.
+__global__ void combine(const int* __restrict__ C, long R, long N, const int* ea, const int* eb,
+                        double* __restrict__ out, long ldo, const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long total = R * N;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const long i = idx / N, j = idx - i * N;
+    const int base = ea[i] + eb[0];
+    double acc = 0.0;
+#pragma unroll
+    for (int w = S - 1; w >= 0; --w) {            // w = p + q, weight 2^{-7(w+2)}
+      double part = 0.0;                         // sum of the exact int32 terms of this weight
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int p = w - q;
+        if (p < 0 || p >= S - q) continue;
+        const long off = R * N * (long)(q * S - q * (q - 1) / 2);   // GEMM q output: (S-q)·R rows
+        part += (double)C[off + (p * R + i) * N + j];                // |part| < 2^34: exact in FP64
+      }
+      acc += ldexp(part, base - 7 * (w + 2));
+    }
+    out[i * ldo + j] = acc;
+  }
+}
+
+}  // namespace ozaki

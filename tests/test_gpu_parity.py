@@ -389,3 +389,19 @@ def test_csr_validation_errors(ctx):
     for off, ci, v in bad:
         with pytest.raises(E.InvalidArgument):
             ctx.run_csr(off, ci, v, 3, 4, w0, h0, cfg, E.TimingMode.none)
+
+
+def test_int8_digit_cross_products_parity(ctx, port):
+    """FP64 cross products on the INT8 tensor cores (ozaki.cuh), taken for dense single-GPU
+    problems with m·n >= 2^24: 4096² r=64 C5-like data, 6 iterations vs the oracle
+    (identical restarts, errors within 1e-9, factors within 1e-6)."""
+    m = n = 4096
+    r = 64
+    rng = np.random.default_rng(21)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, 22)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=6))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 6), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
