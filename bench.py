@@ -45,6 +45,8 @@ METRIC = "E-A-HALS outer iters/sec + % roofline, 32768² r=128, 1/2/4/8 B200"
 UNIT = "outer_iters/s"
 FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.txt)
 FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry)"
+INT8_PEAK_TOPS = 3216.0      # best cuBLASLt int8 GEMM measured on this pool's B200 (profiles/r01_int8_probe.txt)
+INT8_PEAK_SRC = "measured cuBLASLt int8 GEMM, M=1024 K=N=32768 (profiles/r01_int8_probe.txt); nominal dense 4500"
 
 
 def cfg_c5(iters):
@@ -312,10 +314,15 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         ctx.finalize()
     ctx.close()
-    gemm_ms = statistics.mean([(p["cross_wx"] + p["cross_xht"]) / 2 for p in phases])
-    # per-launch algorithmic flops: 2·r·m·n on one GPU, 2·r·m·n/P on each rank when sharded
-    gemm_flops = 2.0 * R * M * N / world
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    # dominant kernel: the persistent HALS sweep kernel (one launch per inner solve), timed per
+    # phase with CUDA events on the engine stream; algorithmic work 2·r²·N per sweep
+    ph = phases[-1]
+    nh, mw = (N // world, M // world)
+    sweep_ms = ph["update_h"] + ph["update_w"]
+    sweep_flops = 2.0 * R * R * (nh * ph["sweeps_h"] + mw * ph["sweeps_w"])
+    achieved = sweep_flops / (sweep_ms * 1e-3) / 1e12
+    cross_ms = statistics.mean([(p["cross_wx"] + p["cross_xht"]) / 2 for p in phases])
+    cross_flops = 2.0 * R * M * N / world
     iter_ms = ms / args.steps
     flops_alg = 4.0 * M * N * R + 2.0 * (M + N) * R * R
     t_roof_ms = flops_alg / world / (FP64_PEAK_TFLOPS * 1e12) * 1e3
@@ -384,14 +391,22 @@ def run_ours(args, rank, world, local_rank):
                 "data": "synthetic (seeded torch generators on device, tile-wise)",
                 "config": config_block(args, world),
                 "roofline": {"bound": "tensor",
-                             "kernel": "gemm_f64_dmma (W_yᵀX / X·Tᵀ, 2·r·m·n/P flop per launch)",
+                             "kernel": "hals::sweep_ws (persistent FP64 DMMA HALS sweeps, one launch per "
+                                       "inner solve; 2·r²·N flop per sweep)",
                              "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                              "frac": achieved / FP64_PEAK_TFLOPS, "traffic": args.traffic,
-                             "peak_source": FP64_PEAK_SRC, "gemm_ms": gemm_ms,
+                             "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
+                             "cross_products": {
+                                 "kernel": "FP64-accurate W_yᵀX / X·Tᵀ: 7-digit INT8 splitting, 7 int8 digit "
+                                           "GEMMs (cuBLASLt) + FP64 recombination (ozaki.cuh)",
+                                 "ms": cross_ms, "fp64_equiv_tflops": cross_flops / (cross_ms * 1e-3) / 1e12,
+                                 "int8_tops": 28 * cross_flops / (cross_ms * 1e-3) / 1e12,
+                                 "int8_peak_tops": INT8_PEAK_TOPS, "int8_peak_source": INT8_PEAK_SRC},
                              "iteration": {"flops_alg": flops_alg, "t_roof_ms": t_roof_ms,
                                            "frac": t_roof_ms / iter_ms,
-                                           "note": "t_roof = (4mnr + 2(m+n)r²)/P / FP64 peak; HALS sweeps "
-                                                   "excluded"},
+                                           "note": "t_roof = (4mnr + 2(m+n)r²)/P at the FP64 DMMA peak; HALS "
+                                                   "sweeps excluded; the cross products run on INT8 tensor "
+                                                   "cores, which is how frac can pass what FP64 DMMA allows"},
                              "phases_ms": phases[-1]},
                 "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
                 "sweeps": {"h_mean": statistics.mean(sweeps_h) if sweeps_h else None,

@@ -921,20 +921,29 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   const long mn = (long)c->m * (long)c->n;
   c->adig.ensure((size_t)ozaki::S * r * K);
   c->aexp.ensure((size_t)r);
-  c->ocbuf.ensure((size_t)ozaki::PAIRS * r * N);
+  // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
+  // are slow below 256 rows with an N-contiguous B, so short stacks are padded with further
+  // (unused) digits there
+  ozaki::Offsets off{};
+  int Mq[ozaki::S];
+  long acc = 0;
+  for (int q = 0; q < ozaki::S; ++q) {
+    Mq[q] = (ozaki::S - q) * r;
+    if (!tn && Mq[q] < 256) Mq[q] = std::min(256, ozaki::S * r);
+    off.q[q] = acc;
+    acc += (long)Mq[q] * N;
+  }
+  // one size for both products of this (m, n, r): no reallocation between captured launches
+  c->ocbuf.ensure(std::max((size_t)acc, ((size_t)ozaki::PAIRS * r + 256) * std::max(c->m, c->n)));
   ozaki::row_exp<<<r, 256, 0, s>>>(A, K, lda, c->aexp.p, st);
   ozaki::split<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
       A, r, K, lda, c->aexp.p, 1, c->adig.p, st);
   CUK();
   c->launches += 2;
-  long acc = 0;
-  for (int q = 0; q < ozaki::S; ++q) {
-    const int Mq = (ozaki::S - q) * r;   // factor digits p = 0..S-1-q, stacked
-    lt_gemm_i8(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + acc, Mq, (int)N, (int)K, tn);
-    acc += (long)Mq * N;
-  }
+  for (int q = 0; q < ozaki::S; ++q)
+    lt_gemm_i8(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn);
   ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
-      c->ocbuf.p, r, N, c->aexp.p, c->xexp.p, out, ldo, st);
+      c->ocbuf.p, off, r, N, c->aexp.p, c->xexp.p, out, ldo, st);
   CUK();
   c->launches += 1 + ozaki::S;
 }

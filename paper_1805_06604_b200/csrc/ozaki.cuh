@@ -99,9 +99,11 @@ __global__ void split(const double* __restrict__ a, long R, long K, long lda, co
   }
 }
 
-// out[i][j] = sum_{q} sum_{p < S-q} 2^{ea_i + eb - 7(p+q+2)} · Cq[p·R + i][j],  Cq = C + R·N·(qS - q(q-1)/2)
+// out[i][j] = sum_{q} sum_{p < S-q} 2^{ea_i + eb - 7(p+q+2)} · Cq[p·R + i][j],  Cq = C + off.q[q]
 // (FP64, smallest weight first).  out row stride ldo.
-__global__ void combine(const int* __restrict__ C, long R, long N, const int* ea, const int* eb,
+struct Offsets { long q[S]; };   // start of digit GEMM q's output (its rows p·R + i, p < S - q)
+
+__global__ void combine(const int* __restrict__ C, Offsets off, long R, long N, const int* ea, const int* eb,
                         double* __restrict__ out, long ldo, const DevState* st) {
   if (st && !dev_active(st)) return;
   const long total = R * N;
@@ -116,8 +118,7 @@ __global__ void combine(const int* __restrict__ C, long R, long N, const int* ea
       for (int q = 0; q < S; ++q) {
         const int p = w - q;
         if (p < 0 || p >= S - q) continue;
-        const long off = R * N * (long)(q * S - q * (q - 1) / 2);   // GEMM q output: (S-q)·R rows
-        part += (double)C[off + (p * R + i) * N + j];                // |part| < 2^34: exact in FP64
+        part += (double)C[off.q[q] + (p * R + i) * N + j];   // |part| < 2^34: exact in FP64
       }
       acc += ldexp(part, base - 7 * (w + 2));
     }

@@ -1,15 +1,17 @@
 #!/bin/bash
-# One GPU call: tests, smoke, bench, ncu launch list + one full capture of the GEMM.
+# One GPU call: tests, smoke, bench, ncu launch list + full captures of the dominant kernels.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 if [ "${NCU:-1}" = "1" ]; then
   CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
-  $CMD > gpurun_out/plain.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:gemm_f64 -s 2 -c 2 -o gpurun_out/prof_gemm $CMD > gpurun_out/ncu_full.log 2>&1
-  echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+  timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_ws -s 2 -c 1 -o gpurun_out/prof_sweep $CMD > gpurun_out/ncu_sweep.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cutlass|gemm|Kernel" -s 20 -c 3 -o gpurun_out/prof_i8 $CMD > gpurun_out/ncu_i8.log 2>&1
+  echo "ncu rc=$?" >> gpurun_out/ncu_i8.log
 fi
