@@ -375,7 +375,7 @@ int hals_variant() {
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
       : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "" ? 54 : 11;  // default: ws
+      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58 : s == "" ? 54 : 11;  // default: ws
   }
   return v;
 }
@@ -585,6 +585,8 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     launch_sweep_ws<128, true, 1, true>(c, s, a);
   } else if (hals_variant() == 57) {
     launch_sweep_ws<128, true, 2, true>(c, s, a);
+  } else if (hals_variant() == 58) {
+    launch_sweep_ws<128, true, 3, true>(c, s, a);
   } else if (hals_variant() == 54) {
     if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
@@ -950,7 +952,7 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
 
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
 void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
-  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 57)) return;
+  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 58)) return;
   constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
   c->Gf.ensure(3 * kGf);
   double* gf = c->Gf.p + slot * kGf;

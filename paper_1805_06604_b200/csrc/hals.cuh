@@ -1295,6 +1295,15 @@ ENMF_DEV int ws_pos(int k, int c) {
 }
 
 ENMF_DEV void nb_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
+// clock64 after a shared-memory load that the hardware cannot issue before the preceding
+// barrier resolves (bar.sync defers its blocking; timing experiments only)
+ENMF_DEV long long clock_after_smem(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];\n" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  long long t;
+  asm volatile("{ .reg .pred q; setp.eq.f64 q, %1, %1; mov.u64 %0, %%clock64; }\n" : "=l"(t) : "d"(v) : "memory");
+  return t;
+}
 ENMF_DEV void nb_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" ::"r"(id) : "memory"); }
 
 ENMF_DEV double pos_part_ws(double t) {
@@ -1369,12 +1378,14 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
   }
 #pragma unroll 1
   for (int b = 0; b < NB; b += 2) {
+    const long long c0 = PROF ? clock64() : 0;
     if (b > 0) nb_sync(idH);                // rows of block b-1 are final in the tile
-    const long long c1 = PROF ? clock64() : 0;
+    const long long c1 = PROF ? clock_after_smem(Ss) : 0;
+    if (PROF) pw[0] += c1 - c0;
     double acc0[4][2], acc1[4][2];
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc0[t][0] = acc0[t][1] = acc1[t][0] = acc1[t][1] = 0.0;
-    if (SKIP != 2) {
+    if (!(SKIP & 2)) {
 #pragma unroll
       for (int j = 0; j < KS / 2; ++j) {   // (block b's fragments of A1 are zero: see ws_prep)
         double2 p[4];
@@ -1397,9 +1408,11 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
         A1[s] = f1.x; A1[s + 1] = f1.y;
       }
     }
+    const long long c3 = PROF ? clock64() : 0;
     nb_sync(idH);                            // block b solved
-    const long long c2 = PROF ? clock64() : 0;
-    if (SKIP != 2) {
+    const long long c2 = PROF ? clock_after_smem(Ss) : 0;
+    if (PROF) pw[0] += c2 - c3;
+    if (!(SKIP & 2)) {
       double2 p[4];
       ws_ldb<NT>(Hs, b, gt, bx0, bx1, p);
       ws_mma2<NT>(acc1, tl.x, tl.y, p);
@@ -1424,7 +1437,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   constexpr int NB = RMAX / 8;
   constexpr int KS = RMAX / 4;
   const long long tk0 = PROF ? clock64() : 0;
-  long long pw[3] = {0, 0, 0};
+  long long pw[4] = {0, 0, 0, 0};
   if (sweep_skipped(a)) return;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[256 + 33];
@@ -1462,6 +1475,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   double gain = 0.0;
   int nf = 0;
   __shared__ int s_flag;
+  double first_total = 0.0;                 // persistent: the first sweep's total gain (stall rule)
   const int gi = lane >> 2, gt = lane & 3;
   // this lane's two 16-byte B-fragment chunks (tiles 0,1 and 2,3) within a row k with k & 3 == gt
   const int swz = ((gt & 1) << 2) | (gt >> 1);
@@ -1539,7 +1553,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
         }
         const long long c0 = PROF ? clock64() : 0;
         nb_sync(idS);
-        const long long c1 = PROF ? clock64() : 0;
+        const long long c1 = PROF ? clock_after_smem(Ss + lane) : 0;
         if (PROF) pw[0] += c1 - c0;
         double* hrow = Hs + 8 * b * 32;
         double x[8];
@@ -1550,7 +1564,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
         }
         double hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < (SKIP == 1 ? 0 : 8); ++i) {
+        for (int i = 0; i < ((SKIP & 1) ? 0 : 8); ++i) {
           const double t = __dmul_rn(bb[i], gc[36 + i]);
           const double h = pos_part_ws(t);
           hv[i] = h;
@@ -1577,43 +1591,72 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   }
   if (!PERSIST) break;
   // ---- grid-wide end of sweep `sw`: stall rule on the total gain ----
+  const long long tg0 = PROF ? clock64() : 0;
   {
     const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
     const int bnf = __syncthreads_or(nf);
+    const unsigned target = (unsigned)(sw + 1) * gridDim.x;
     if (threadIdx.x == 0) {
       a.part[blockIdx.x] = bg;
       a.part_nf[blockIdx.x] = bnf;
       __threadfence();
       const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
-      s_flag = prev == (unsigned)(sw + 1) * gridDim.x - 1 ? 1 : 0;
+      s_flag = prev == target - 1 ? 1 : 0;   // this CTA arrived last (used when sharded)
     }
-    __syncthreads();
-    if (s_flag) {                           // last CTA: fixed-order total
-      __threadfence();
+    if (!a.dv) {
+      // every CTA forms the same fixed-order total itself once all partials are in
+      if (threadIdx.x == 0) {
+        unsigned e;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
+        } while (e < target);
+      }
+      __syncthreads();
       double v = 0.0;
       int f = 0;
       for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) {
         v = __dadd_rn(v, __ldcg(a.part + b));
         f |= __ldcg(a.part_nf + b);
       }
-      double total = block_reduce_sum_any(v, red);
+      const double total = block_reduce_sum_any(v, red);
       f = __syncthreads_or(f);
-      if (threadIdx.x == 0) {
-        if (a.dv) dist::allreduce_gain(*a.dv, total, f, &total, &f);
-        finish_sweep(a, total, f);
+      if (sw == 0) first_total = total;
+      const bool stop = (sw + 1 >= a.max_sweeps) ||
+                        (total <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
+      if (blockIdx.x == 0 && threadIdx.x == 0) finish_sweep(a, total, f);   // bookkeeping (same rule)
+      s_flag = stop ? 0 : 1;
+    } else {
+      // sharded: the last CTA exchanges the gain with the other ranks and publishes the decision
+      __syncthreads();
+      if (s_flag) {
         __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(&a.ctl->epoch), "r"((unsigned)(sw + 1))
-                     : "memory");
+        double v = 0.0;
+        int f = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) {
+          v = __dadd_rn(v, __ldcg(a.part + b));
+          f |= __ldcg(a.part_nf + b);
+        }
+        double total = block_reduce_sum_any(v, red);
+        f = __syncthreads_or(f);
+        if (threadIdx.x == 0) {
+          dist::allreduce_gain(*a.dv, total, f, &total, &f);
+          finish_sweep(a, total, f);
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(&a.ctl->epoch), "r"((unsigned)(sw + 1))
+                       : "memory");
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned e;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->epoch) : "memory");
+        } while (e < (unsigned)(sw + 1));
+        s_flag = *(volatile int*)&a.ctl->cont;
       }
     }
-    if (threadIdx.x == 0) {
-      unsigned e;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->epoch) : "memory");
-      } while (e < (unsigned)(sw + 1));
-      s_flag = *(volatile int*)&a.ctl->cont;
-    }
     __syncthreads();
+    if (PROF) pw[3] += clock64() - tg0;
     if (!s_flag) break;
     gain = 0.0;
     nf = 0;
@@ -1621,11 +1664,12 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   }
   }
   if (PROF && lane == 0) {
-    double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 4;
+    double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 8;
     o[0] = (double)pw[0];
     o[1] = (double)pw[1];
     o[2] = (double)(clock64() - tk0);
     o[3] = (double)pw[2];
+    o[4] = (double)pw[3];
   }
   if (!PERSIST) {
     const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
