@@ -244,6 +244,15 @@ def gen_block(w0, h0, r0, r1, c0, c1, seed):
     return out
 
 
+def direct_rel_error(x, w, h, rows=2048):
+    """||X - W·H||_F / ||X||_F in FP64 on the device, in row blocks."""
+    num = 0.0
+    for i in range(0, x.shape[0], rows):
+        d = x[i:i + rows] - w[i:i + rows] @ h
+        num += float((d * d).sum())
+    return (num / float((x * x).sum())) ** 0.5
+
+
 def _make_context(E, dist_mod, local_rank, rank, world, xs, exchange):
     """Single-GPU Context with X loaded, or this rank's ShardedContext."""
     if world == 1:
@@ -309,8 +318,41 @@ def run_ours(args, rank, world, local_rank):
     sweeps_w = [r.inner_w_count for r in timed]
     # dominant kernel: FP64 DMMA GEMM, timed per phase with CUDA events on the engine stream
     phases = [ctx.step_profiled() for _ in range(prof_steps)]
-    ctx.sync()
-    ctx.end()
+    recs = ctx.sync()
+    w64 = torch.empty(wi_s.shape, dtype=torch.float64, device=dev)
+    h64 = torch.empty(hi_s.shape, dtype=torch.float64, device=dev)
+    ctx.end(w64.data_ptr(), h64.data_ptr())
+    # TF32 variant (BASELINE configs[4]): same data, init and iteration count, the two cross
+    # products on TF32 tensor cores; reported next to the FP64 line, not as its value
+    tf32 = None
+    if world == 1 and not args.no_tf32:
+        cfg_t = cfg_c5(args.warmup + args.steps + prof_steps)
+        cfg_t.precision = E.Precision.tf32
+        ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg_t)
+        ctx.step(args.warmup)
+        ctx.sync()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0e.record(stream)
+        ctx.step(args.steps)
+        t1e.record(stream)
+        t1e.synchronize()
+        ctx.step(prof_steps)
+        rt = ctx.sync()
+        w32 = torch.empty_like(w64)
+        h32 = torch.empty_like(h64)
+        ctx.end(w32.data_ptr(), h32.data_ptr())
+        tms = t0e.elapsed_time(t1e)
+        # final factors judged by the direct residual ||X - WH|| / ||X|| in FP64 (the TF32 run's
+        # in-loop estimate carries the tensor cores' FP32 accumulation bias, profiles/r01_tf32_bias.txt)
+        f64_final, t_final = direct_rel_error(xs[0], w64, h64), direct_rel_error(xs[0], w32, h32)
+        tf32 = {"value": args.steps / (tms * 1e-3), "unit": UNIT, "ms_per_step": tms / args.steps,
+                "dtype": "tf32 cross products (X in FP32), FP64 elsewhere",
+                "iterations": len(rt) - 1, "final_relative_error": t_final,
+                "in_loop_estimate": rt[-1].relative_error,
+                "fp64_final_relative_error": f64_final, "abs_diff": abs(t_final - f64_final),
+                "within_1e-4": abs(t_final - f64_final) <= 1e-4,
+                "restarts": int(sum(r.restarted for r in rt)), "fp64_restarts": int(sum(r.restarted for r in recs))}
     if world > 1:
         ctx.finalize()
     ctx.close()
@@ -409,6 +451,7 @@ def run_ours(args, rank, world, local_rank):
                                                    "cores, which is how frac can pass what FP64 DMMA allows"},
                              "phases_ms": phases[-1]},
                 "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+                "tf32_variant": tf32,
                 "sweeps": {"h_mean": statistics.mean(sweeps_h) if sweeps_h else None,
                            "w_mean": statistics.mean(sweeps_w) if sweeps_w else None},
                 "final_relative_error": recs[-1].relative_error if recs else None}
@@ -424,6 +467,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tf32", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=64)
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per GEMM launch from an ncu --set full capture (profiles/)")

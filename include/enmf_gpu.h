@@ -53,6 +53,7 @@ enum { ENMF_TIMING_WALL = 0, ENMF_TIMING_NONE = 1 };
 /* Arithmetic of the device path. FP64 is the parity path. */
 enum {
   ENMF_PRECISION_FP64 = 0,        /* DMMA tensor-core GEMMs, FMA sweeps: the product path */
+  ENMF_PRECISION_TF32 = 1,        /* variant: W_yᵀX and X·Tᵀ on TF32 tensor cores (X held in FP32), rest FP64 */
   ENMF_PRECISION_FP64_EXACT = 2   /* bitwise-faithful debug path: reference summation order, no FMA */
 };
 

@@ -22,7 +22,7 @@ ENMF_CACHE_STALE = 6
 
 ENMF_INNER_EXACT, ENMF_INNER_HALS = 0, 1
 ENMF_TIMING_WALL, ENMF_TIMING_NONE = 0, 1
-ENMF_PRECISION_FP64, ENMF_PRECISION_FP64_EXACT = 0, 2
+ENMF_PRECISION_FP64, ENMF_PRECISION_TF32, ENMF_PRECISION_FP64_EXACT = 0, 1, 2
 
 
 class CConfig(C.Structure):

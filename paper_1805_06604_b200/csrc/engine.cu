@@ -96,6 +96,9 @@ struct enmf_gpu_ctx {
   DBuf<int> ocbuf;
   DBuf<double> opart;
   void* lt = nullptr;                     // LtCache (cuBLASLt handle, workspace, per-shape plans)
+  // TF32 variant: FP32 copy of X (once per load), FP32 factor / product staging
+  bool xf_ready = false;
+  DBuf<float> xf, af, cf;
   // factors and products
   DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch, Gf;
   DBuf<double> partials, gain_part, terms, ddpart, dd;
@@ -228,7 +231,7 @@ inline unsigned grid_for(long count, int nt = 256, int maxb = 148 * 8) {
 }
 
 // ---- precision modes ---------------------------------------------------------
-enum { PREC_FAST = ENMF_PRECISION_FP64, PREC_EXACT = 2 };
+enum { PREC_FAST = ENMF_PRECISION_FP64, PREC_TF32 = ENMF_PRECISION_TF32, PREC_EXACT = 2 };
 
 // ---- contractions --------------------------------------------------------------
 // Split-K factor: the smallest S whose CTA count fills the SMs to >= 95%
@@ -703,7 +706,8 @@ void validate_cfg(const enmf_gpu_config* c) {
       (c->inner_w != ENMF_INNER_EXACT && c->inner_w != ENMF_INNER_HALS))
     bad("SolverConfig: inner solver must be exact or hals");
   if (c->timing != ENMF_TIMING_WALL && c->timing != ENMF_TIMING_NONE) bad("SolverConfig: bad timing mode");
-  if (c->precision != PREC_FAST && c->precision != PREC_EXACT) bad("SolverConfig: unsupported precision");
+  if (c->precision != PREC_FAST && c->precision != PREC_EXACT && c->precision != PREC_TF32)
+    bad("SolverConfig: unsupported precision");
 }
 
 // InnerLoopPolicy::derive (nnls.hpp:79-87) via detail::inner_policy (engine.hpp:250-263)
@@ -815,7 +819,7 @@ struct LtCache {
   void* ws = nullptr;
   size_t ws_size = 64u << 20;
   struct Entry {
-    int M, N, K, tn;
+    int M, N, K, tn, kind;           // kind 0: int8 → int32, 1: fp32 (TF32 tensor cores) → fp32
     cublasLtMatmulDesc_t op;
     cublasLtMatrixLayout_t la, lb, lc;
     cublasLtMatmulAlgo_t algo;
@@ -846,8 +850,8 @@ void lt_free(enmf_gpu_ctx* c) {
 // C (M×N int32, row-major) = A (M×K int8, row-major) · B, where B = Xdᵀ with Xd
 // N×K row-major (tn) or B = Xd with Xd K×N row-major (!tn).  Column-major call:
 // Cᵀ (N×M) = op(Xd') · Aᵀ.
-void lt_gemm_i8(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* Xd, int* C, int M, int N, int K,
-                bool tn) {
+void lt_gemm(enmf_gpu_ctx* c, cudaStream_t s, const void* A, const void* Xd, void* C, int M, int N, int K, bool tn,
+             int kind) {
   if (!c->lt) {
     auto* nl = new LtCache();
     c->lt = nl;
@@ -857,18 +861,20 @@ void lt_gemm_i8(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* 
   LtCache* lt = static_cast<LtCache*>(c->lt);
   LtCache::Entry* en = nullptr;
   for (auto& e : lt->e)
-    if (e.M == M && e.N == N && e.K == K && e.tn == (int)tn) en = &e;
+    if (e.M == M && e.N == N && e.K == K && e.tn == (int)tn && e.kind == kind) en = &e;
   if (!en) {
     LtCache::Entry e{};
-    e.M = M; e.N = N; e.K = K; e.tn = tn;
-    LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
+    e.M = M; e.N = N; e.K = K; e.tn = tn; e.kind = kind;
+    const cudaDataType_t ab = kind ? CUDA_R_32F : CUDA_R_8I, cd = kind ? CUDA_R_32F : CUDA_R_32I;
+    if (kind) LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F));
+    else LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
     const cublasOperation_t ta = tn ? CUBLAS_OP_T : CUBLAS_OP_N, tb = CUBLAS_OP_N;
     LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta));
     LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb));
-    if (tn) LT(cublasLtMatrixLayoutCreate(&e.la, CUDA_R_8I, K, N, K));
-    else LT(cublasLtMatrixLayoutCreate(&e.la, CUDA_R_8I, N, K, N));
-    LT(cublasLtMatrixLayoutCreate(&e.lb, CUDA_R_8I, K, M, K));
-    LT(cublasLtMatrixLayoutCreate(&e.lc, CUDA_R_32I, N, M, N));
+    if (tn) LT(cublasLtMatrixLayoutCreate(&e.la, ab, K, N, K));
+    else LT(cublasLtMatrixLayoutCreate(&e.la, ab, N, K, N));
+    LT(cublasLtMatrixLayoutCreate(&e.lb, ab, K, M, K));
+    LT(cublasLtMatrixLayoutCreate(&e.lc, cd, N, M, N));
     cublasLtMatmulPreference_t pref;
     LT(cublasLtMatmulPreferenceCreate(&pref));
     LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt->ws_size,
@@ -877,13 +883,16 @@ void lt_gemm_i8(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* 
     int found = 0;
     LT(cublasLtMatmulAlgoGetHeuristic(lt->h, e.op, e.la, e.lb, e.lc, e.lc, pref, 1, &res, &found));
     cublasLtMatmulPreferenceDestroy(pref);
-    if (!found) throw Fail{ENMF_CUDA_ERROR, "cuBLASLt: no int8 algorithm for the digit GEMM"};
+    if (!found) throw Fail{ENMF_CUDA_ERROR, "cuBLASLt: no algorithm for the cross-product GEMM"};
     e.algo = res.algo;
     lt->e.push_back(e);
     en = &lt->e.back();
   }
-  const int alpha = 1, beta = 0;
-  LT(cublasLtMatmul(lt->h, en->op, &alpha, Xd, en->la, A, en->lb, &beta, C, en->lc, C, en->lc, &en->algo,
+  const int ialpha = 1, ibeta = 0;
+  const float falpha = 1.f, fbeta = 0.f;
+  const void* alpha = kind ? (const void*)&falpha : (const void*)&ialpha;
+  const void* beta = kind ? (const void*)&fbeta : (const void*)&ibeta;
+  LT(cublasLtMatmul(lt->h, en->op, alpha, Xd, en->la, A, en->lb, beta, C, en->lc, C, en->lc, &en->algo,
                     lt->ws, lt->ws_size, s));
 }
 
@@ -943,11 +952,70 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   CUK();
   c->launches += 2;
   for (int q = 0; q < ozaki::S; ++q)
-    lt_gemm_i8(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn);
+    lt_gemm(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
   ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
       c->ocbuf.p, off, r, N, c->aexp.p, c->xexp.p, out, ldo, st);
   CUK();
   c->launches += 1 + ozaki::S;
+}
+
+// ---- TF32 variant of the cross products (ENMF_PRECISION_TF32) -----------------
+// X is kept in FP32 (one copy per load), the factor rounded to FP32 per product, the
+// product on the TF32 tensor cores (cuBLASLt, FP32 accumulation) and widened to FP64;
+// everything else (Grams, sweeps, error, decisions) stays FP64.
+__global__ void to_f32(const double* __restrict__ in, long rows, long cols, long ld, float* __restrict__ out,
+                       const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long total = rows * cols;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long r_ = i / cols, c_ = i - r_ * cols;
+    // round to the nearest TF32 value here: the tensor cores drop the low 13 bits of an FP32
+    // operand (a bias of half a TF32 ulp that the trace-identity error would amplify)
+    const float f = (float)in[r_ * ld + c_];
+    unsigned t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(f));
+    out[i] = __uint_as_float(t);
+  }
+}
+__global__ void to_f64(const float* __restrict__ in, long rows, long cols, double* __restrict__ out, long ldo,
+                       const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long total = rows * cols;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long r_ = i / cols, c_ = i - r_ * cols;
+    out[r_ * ldo + c_] = (double)in[i];
+  }
+}
+
+bool tf32_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
+  return prec == PREC_TF32 && !dist && !c->sparse && c->x;
+}
+
+void tf32_prepare_x(enmf_gpu_ctx* c, cudaStream_t s) {
+  if (c->xf_ready) return;
+  const long mn = (long)c->m * (long)c->n;
+  c->xf.ensure((size_t)mn);
+  to_f32<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(c->x, (long)c->m,
+                                                                                       (long)c->n, (long)c->n,
+                                                                                       c->xf.p, nullptr);
+  CUK();
+  c->launches++;
+  c->xf_ready = true;
+}
+
+void tf32_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
+                const DevState* st) {
+  const long K = tn ? (long)c->n : (long)c->m, N = tn ? (long)c->m : (long)c->n;
+  c->af.ensure((size_t)r * std::max(c->m, c->n));
+  c->cf.ensure((size_t)r * std::max(c->m, c->n));
+  to_f32<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(A, r, K, lda,
+                                                                                                c->af.p, st);
+  CUK();
+  lt_gemm(c, s, c->af.p, c->xf.p, c->cf.p, r, (int)N, (int)K, tn, 1);
+  to_f64<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(c->cf.p, r, N, out,
+                                                                                                ldo, st);
+  CUK();
+  c->launches += 3;
 }
 
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
@@ -1106,6 +1174,8 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   mark(c, s, prof, 1);
   if (c->sparse) {
     sparse_wx(c, s, pl.prec == PREC_EXACT, c->WyT.p, r, c->CH.p, st);
+  } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
+    tf32_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
     ozaki_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
   } else if (pl.prec == PREC_EXACT) {
@@ -1140,6 +1210,8 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   auto cross_xht = [&](const double* Tm, double* out) {
     if (c->sparse) {
       sparse_xht(c, s, pl.prec == PREC_EXACT, Tm, r, out, st);
+    } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
+      tf32_cross(c, s, Tm, n, r, true, out, m, st);
     } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
       ozaki_cross(c, s, Tm, n, r, true, out, m, st);
     } else if (pl.prec == PREC_EXACT) {
@@ -1349,6 +1421,9 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   dist_gather(c, s, L, c->WT.p, (int)r, 0, pl, st);      // W0ᵀ replica for iteration 1's W_yᵀX
   if (c->sparse) {
     sparse_xht(c, s, pl.prec == PREC_EXACT, c->H.p, (int)r, c->P.p, st);
+  } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
+    tf32_prepare_x(c, s);                // once per loaded X (outside the iteration graph)
+    tf32_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
     ozaki_prepare_x(c, s);               // once per loaded X (outside the iteration graph)
     ozaki_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);

@@ -82,7 +82,8 @@ class TimingMode(enum.IntEnum):
 
 
 class Precision(enum.IntEnum):
-    fp64 = L.ENMF_PRECISION_FP64              # DMMA tensor-core path (product)
+    fp64 = L.ENMF_PRECISION_FP64              # FP64 product path (DMMA / INT8-digit tensor cores)
+    tf32 = L.ENMF_PRECISION_TF32              # variant: cross products on TF32 tensor cores
     fp64_exact = L.ENMF_PRECISION_FP64_EXACT  # bitwise-faithful debug path
 
 

@@ -405,3 +405,23 @@ def test_int8_digit_cross_products_parity(ctx, port):
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
     assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+
+
+def test_tf32_variant_final_error(ctx):
+    """TF32 variant (BASELINE configs[4], reported separately): the cross products on TF32
+    tensor cores, everything else FP64; final relative error within 1e-4 of the FP64 path
+    on 4096² r=64 C5-like data after 20 iterations (north_star tolerance)."""
+    m = n = 4096
+    r = 64
+    rng = np.random.default_rng(31)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = rng.random((m, r)), rng.random((r, n))
+    f64 = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 20), E.TimingMode.none)
+    t32 = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 20, E.Precision.tf32), E.TimingMode.none)
+    nx = np.linalg.norm(x)
+    # the in-loop trace-identity estimate of the TF32 run carries the tensor cores' FP32
+    # accumulation bias (profiles/r01_tf32_bias.txt); the final factors are judged directly
+    e64 = np.linalg.norm(x - f64.factors.w @ f64.factors.h) / nx
+    e32 = np.linalg.norm(x - t32.factors.w @ t32.factors.h) / nx
+    assert abs(e32 - e64) <= 1e-4, (e32, e64)
+    assert np.all(np.isfinite(t32.factors.w)) and np.all(t32.factors.w >= 0)
