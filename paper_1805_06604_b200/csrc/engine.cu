@@ -90,9 +90,15 @@ struct enmf_gpu_ctx {
   DBuf<int> csr_idx, csc_idx;
   DBuf<double> csr_val, csc_val, rowmaj;
   // FP64 cross products on INT8 tensor cores (ozaki.cuh): X digits (cut once per load)
-  bool xdig_ready = false;
-  DBuf<int8_t> xdig, adig;
-  DBuf<int> xexp, aexp;
+  struct XDig {                            // digits of one X operand (full X, or a rank's block)
+    DBuf<int8_t> d;
+    DBuf<int> e;
+    const double* src = nullptr;
+    long rows = 0, cols = 0;
+    bool ready = false;
+  } xd_full, xd_cols, xd_rows;
+  DBuf<int8_t> adig;
+  DBuf<int> aexp;
   DBuf<int> ocbuf;
   DBuf<double> opart;
   void* lt = nullptr;                     // LtCache (cuBLASLt handle, workspace, per-shape plans)
@@ -904,32 +910,37 @@ bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
     const char* e = std::getenv("ENMF_CROSS");
     env = (e && std::string(e) == "dmma") ? 0 : 1;
   }
-  return env == 1 && prec == PREC_FAST && !dist && !c->sparse && c->x &&
+  return env == 1 && prec == PREC_FAST && !c->sparse && (c->x || dist) &&
          (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072;
 }
 
-void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s) {
-  if (c->xdig_ready) return;
-  const long mn = (long)c->m * (long)c->n;
-  c->xdig.ensure((size_t)ozaki::S * mn);
-  c->xexp.ensure(1);
+// digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph)
+void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, const double* x, long rows,
+                     long cols) {
+  if (xd.ready && xd.src == x && xd.rows == rows && xd.cols == cols) return;
+  const long mn = rows * cols;
+  xd.d.ensure((size_t)ozaki::S * mn);
+  xd.e.ensure(1);
   c->opart.ensure(4096);
   const int nb = (int)std::min<long>(4096, (mn + 255) / 256);
-  ozaki::absmax_partial<<<nb, 256, 0, s>>>(c->x, mn, c->opart.p);
-  ozaki::absmax_final<<<1, 1024, 0, s>>>(c->opart.p, nb, c->xexp.p);
+  ozaki::absmax_partial<<<nb, 256, 0, s>>>(x, mn, c->opart.p);
+  ozaki::absmax_final<<<1, 1024, 0, s>>>(c->opart.p, nb, xd.e.p);
   ozaki::split<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(
-      c->x, (long)c->m, (long)c->n, (long)c->n, c->xexp.p, 0, c->xdig.p, nullptr);
+      x, rows, cols, cols, xd.e.p, 0, xd.d.p, nullptr);
   CUK();
   c->launches += 3;
-  c->xdig_ready = true;
+  xd.src = x;
+  xd.rows = rows;
+  xd.cols = cols;
+  xd.ready = true;
 }
 
-// out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · (tn ? Xᵀ : X) in FP64 accuracy,
-// X = m × n (tn: N = m, K = n; !tn: K = m, N = n).
+// out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · (tn ? Xdᵀ : Xd) in FP64 accuracy,
+// Xd = the digit-cut operand (tn: N = rows, K = cols; !tn: K = rows, N = cols).
 void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
-                 const DevState* st) {
-  const long K = tn ? (long)c->n : (long)c->m, N = tn ? (long)c->m : (long)c->n;
-  const long mn = (long)c->m * (long)c->n;
+                 const DevState* st, const enmf_gpu_ctx::XDig& xd) {
+  const long K = tn ? xd.cols : xd.rows, N = tn ? xd.rows : xd.cols;
+  const long mn = xd.rows * xd.cols;
   c->adig.ensure((size_t)ozaki::S * r * K);
   c->aexp.ensure((size_t)r);
   // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
@@ -946,15 +957,16 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   }
   // one size for both products of this (m, n, r): no reallocation between captured launches
   c->ocbuf.ensure(std::max((size_t)acc, ((size_t)ozaki::PAIRS * r + 256) * std::max(c->m, c->n)));
+  if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
   ozaki::row_exp<<<r, 256, 0, s>>>(A, K, lda, c->aexp.p, st);
   ozaki::split<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
       A, r, K, lda, c->aexp.p, 1, c->adig.p, st);
   CUK();
   c->launches += 2;
   for (int q = 0; q < ozaki::S; ++q)
-    lt_gemm(c, s, c->adig.p, c->xdig.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
+    lt_gemm(c, s, c->adig.p, xd.d.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
   ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
-      c->ocbuf.p, off, r, N, c->aexp.p, c->xexp.p, out, ldo, st);
+      c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
   CUK();
   c->launches += 1 + ozaki::S;
 }
@@ -1177,7 +1189,7 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
     tf32_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-    ozaki_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
+    ozaki_cross(c, s, L.wyfull, m, r, false, c->CH.p, nl, st, D ? c->xd_cols : c->xd_full);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
@@ -1213,7 +1225,7 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
     } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
       tf32_cross(c, s, Tm, n, r, true, out, m, st);
     } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-      ozaki_cross(c, s, Tm, n, r, true, out, m, st);
+      ozaki_cross(c, s, D ? L.tfull : Tm, n, r, true, out, ml, st, D ? c->xd_rows : c->xd_full);
     } else if (pl.prec == PREC_EXACT) {
       gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
       CUK();
@@ -1425,8 +1437,14 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     tf32_prepare_x(c, s);                // once per loaded X (outside the iteration graph)
     tf32_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-    ozaki_prepare_x(c, s);               // once per loaded X (outside the iteration graph)
-    ozaki_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);
+    if (D) {                             // once per loaded X (outside the iteration graph)
+      ozaki_prepare_x(c, s, c->xd_cols, D->xc, (long)m, (long)D->np);
+      ozaki_prepare_x(c, s, c->xd_rows, D->xr, (long)D->mp, (long)n);
+    } else {
+      ozaki_prepare_x(c, s, c->xd_full, c->x, (long)m, (long)n);
+    }
+    ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
+                D ? c->xd_rows : c->xd_full);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);
