@@ -8,6 +8,6 @@ from .enmf import (  # noqa: F401
     BetaSchedule, CacheStale, Context, DEFAULT_ALGORITHMS, DegenerateColumn, DeviceError, FactorPair,
     InnerSolver, InvalidArgument, IterationRecord, NoConvergence, NonFiniteIterate, Precision, RunRecord,
     SolverConfig, TimingMode, active_set_solve, algorithm_config, cross_wx, cross_xht, default_context,
-    fast_error, frob_norm_sq, gram, hals_solve, run, run_csr, update_beta,
+    fast_error, frob_norm_sq, gram, hals_solve, run, run_batch, run_csr, update_beta,
 )
 from ._lib import LIB_PATH, load as load_library  # noqa: F401

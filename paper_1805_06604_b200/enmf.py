@@ -439,6 +439,42 @@ def run(x, w0, h0, cfg: SolverConfig, timing: TimingMode = TimingMode.wall) -> R
     return default_context().run(x, w0, h0, cfg, timing)
 
 
+def run_batch(problems, cfg: SolverConfig, timing: TimingMode = TimingMode.none, streams: int = 8,
+              device: int = -1) -> List[RunRecord]:
+    """Many independent dense runs in flight together — the paper protocol's dataset × init
+    grid that the reference runs on a host thread pool (run_suite, bench.hpp:233-294).
+
+    `problems` is a sequence of (x, w0, h0).  Up to `streams` contexts, each with its own
+    CUDA stream and iteration graph, take a problem each; all K iterations of every context
+    are enqueued before any result is read, so the GPU overlaps the small launch-bound runs.
+    Every run is computed exactly as `run` would compute it on its own."""
+    problems = list(problems)
+    pool = [Context(device) for _ in range(max(1, min(streams, len(problems))))]
+    out: List[RunRecord] = []
+    try:
+        for start in range(0, len(problems), len(pool)):
+            chunk = problems[start:start + len(pool)]
+            live = []
+            for ctx, (x, w0, h0) in zip(pool, chunk):
+                x, w0, h0 = _f64(x, "x"), _f64(w0, "w0"), _f64(h0, "h0")
+                if w0.shape[0] != x.shape[0] or h0.shape[1] != x.shape[1] or w0.shape[1] != h0.shape[0]:
+                    raise InvalidArgument("run: factor shapes do not match the data matrix")
+                ctx.load(x)
+                ctx.begin(w0, h0, cfg, timing)
+                ctx.step(int(cfg.max_outer_iterations))
+                live.append((ctx, x.shape, w0.shape[1]))
+            for ctx, (m, n), r in live:
+                recs = ctx.sync()
+                w = np.empty((m, r))
+                h = np.empty((r, n))
+                nx = ctx.end(w.ctypes.data, h.ctypes.data)
+                out.append(RunRecord(recs, FactorPair(w, h), nx))
+    finally:
+        for ctx in pool:
+            ctx.close()
+    return out
+
+
 def run_csr(offsets, col_idx, vals, m, n, w0, h0, cfg: SolverConfig,
             timing: TimingMode = TimingMode.wall) -> RunRecord:
     """enmf::run<SparseMatrix> on the calling thread's GPU context."""

@@ -426,3 +426,17 @@ def test_tf32_variant_final_error(ctx):
     e32 = np.linalg.norm(x - t32.factors.w @ t32.factors.h) / nx
     assert abs(e32 - e64) <= 1e-4, (e32, e64)
     assert np.all(np.isfinite(t32.factors.w)) and np.all(t32.factors.w >= 0)
+
+
+def test_run_batch_matches_single_runs(ctx, golden):
+    """run_batch (the paper protocol's many small runs in flight together) computes every run
+    exactly as a single run does: bitwise-identical records and factors."""
+    inp = golden.load("c1_inputs")
+    rng = np.random.default_rng(3)
+    probs = [(inp["x"], rng.random((200, 20)), rng.random((20, 200))) for _ in range(6)]
+    cfg = _cfg("e-ahals-hp3", 60)
+    batch = E.run_batch(probs, cfg, streams=4)
+    for (x, w0, h0), rb in zip(probs, batch):
+        rs = ctx.run(x, w0, h0, cfg, E.TimingMode.none)
+        assert np.array_equal(rb.column("error"), rs.column("error"))
+        assert np.array_equal(rb.factors.w, rs.factors.w) and np.array_equal(rb.factors.h, rs.factors.h)
