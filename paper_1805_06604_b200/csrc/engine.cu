@@ -910,8 +910,11 @@ bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
     const char* e = std::getenv("ENMF_CROSS");
     env = (e && std::string(e) == "dmma") ? 0 : 1;
   }
+  // (cuBLASLt's int8 kernels need 16-aligned leading dimensions: m, n and, when sharded, the
+  // rank's row / column block sizes multiples of 16)
   return env == 1 && prec == PREC_FAST && !c->sparse && (c->x || dist) &&
-         (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072;
+         (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072 &&
+         c->m % 16 == 0 && c->n % 16 == 0 && (!dist || (c->dist->mp % 16 == 0 && c->dist->np % 16 == 0));
 }
 
 // digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph)

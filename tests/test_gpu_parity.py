@@ -440,3 +440,19 @@ def test_run_batch_matches_single_runs(ctx, golden):
         rs = ctx.run(x, w0, h0, cfg, E.TimingMode.none)
         assert np.array_equal(rb.column("error"), rs.column("error"))
         assert np.array_equal(rb.factors.w, rs.factors.w) and np.array_equal(rb.factors.h, rs.factors.h)
+
+
+@pytest.mark.parametrize("shape", [(3001, 2999, 100), (517, 4403, 72), (4097, 4101, 33), (4096, 4112, 33)])
+def test_ragged_shapes_parity(ctx, port, shape):
+    """Odd m, n and r that fill no tile, row block or digit stack exactly (sweep padding rows,
+    partial column tiles; 4096×4112 r=33 takes the INT8-digit products with an odd digit stack,
+    4097×4101 falls back to the DMMA GEMM): E-A-HALS hp3 vs the oracle."""
+    m, n, r = shape
+    rng = np.random.default_rng(m + n + r)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, 4)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=5))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 5), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
