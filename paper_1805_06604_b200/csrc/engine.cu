@@ -885,44 +885,12 @@ void lt_gemm(enmf_gpu_ctx* c, cudaStream_t s, const void* A, const void* Xd, voi
     LT(cublasLtMatmulPreferenceCreate(&pref));
     LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt->ws_size,
                                             sizeof lt->ws_size));
-    cublasLtMatmulHeuristicResult_t res[8] = {};
+    cublasLtMatmulHeuristicResult_t res[1] = {};
     int found = 0;
-    LT(cublasLtMatmulAlgoGetHeuristic(lt->h, e.op, e.la, e.lb, e.lc, e.lc, pref, 8, res, &found));
+    LT(cublasLtMatmulAlgoGetHeuristic(lt->h, e.op, e.la, e.lb, e.lc, e.lc, pref, 1, res, &found));
     cublasLtMatmulPreferenceDestroy(pref);
     if (!found) throw Fail{ENMF_CUDA_ERROR, "cuBLASLt: no algorithm for the cross-product GEMM"};
     e.algo = res[0].algo;
-    // outside stream capture: time the candidates once on the real operands, keep the fastest
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CU(cudaStreamIsCapturing(s, &cap));
-    if (found > 1 && cap == cudaStreamCaptureStatusNone) {
-      const int ia = 1, ib = 0;
-      const float fa = 1.f, fb = 0.f;
-      const void* al = kind ? (const void*)&fa : (const void*)&ia;
-      const void* be = kind ? (const void*)&fb : (const void*)&ib;
-      cudaEvent_t t0, t1;
-      CU(cudaEventCreate(&t0));
-      CU(cudaEventCreate(&t1));
-      float best = 1e30f;
-      for (int i = 0; i < found; ++i) {
-        if (cublasLtMatmul(lt->h, e.op, al, Xd, e.la, A, e.lb, be, C, e.lc, C, e.lc, &res[i].algo, lt->ws,
-                           lt->ws_size, s) != CUBLAS_STATUS_SUCCESS)
-          continue;
-        CU(cudaEventRecord(t0, s));
-        for (int rep = 0; rep < 2; ++rep)
-          LT(cublasLtMatmul(lt->h, e.op, al, Xd, e.la, A, e.lb, be, C, e.lc, C, e.lc, &res[i].algo, lt->ws,
-                            lt->ws_size, s));
-        CU(cudaEventRecord(t1, s));
-        CU(cudaEventSynchronize(t1));
-        float ms = 0.f;
-        CU(cudaEventElapsedTime(&ms, t0, t1));
-        if (ms < best) {
-          best = ms;
-          e.algo = res[i].algo;
-        }
-      }
-      cudaEventDestroy(t0);
-      cudaEventDestroy(t1);
-    }
     lt->e.push_back(e);
     en = &lt->e.back();
   }
@@ -1480,10 +1448,6 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     }
     ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
                 D ? c->xd_rows : c->xd_full);
-    // the W_yᵀX shapes once here too (result unused: iteration 1 recomputes C_H), so that their
-    // cuBLASLt plans are chosen outside the iteration graph's capture
-    ozaki_cross(c, s, D ? L.wyfull : c->WT.p, (long)m, (int)r, false, c->CH.p, (long)nl, st,
-                D ? c->xd_cols : c->xd_full);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);
