@@ -548,6 +548,83 @@ def run_c4(args):
     return 0
 
 
+def gen_dense_config(which, seed):
+    """BASELINE configs[1] (C2) / configs[2] (C3) as seeded numpy data (same descriptions as the
+    oracle's generators, not their streams)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    if which == "c2":   # image-shaped: 10304 pixels × 400 images, r = 40, 70%-sparse W0, |N(0,.01²)|, rescaled
+        m, n, r = 10304, 400, 40
+        w = rng.random((m, r)) * (rng.random((m, r)) >= 0.7)
+        x = w @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+        x /= x.max()
+        return x, r, "e-ahals-hp3", 500
+    m = n = 2000
+    r = 30
+    x = rng.random((m, r)) @ rng.random((r, n))
+    x = np.maximum(x + 0.05 * x.mean() * rng.standard_normal((m, n)), 0.0)
+    return x, r, "e-anls-hp1", 100
+
+
+def run_dense_config(args):
+    import numpy as np
+    import torch
+    import paper_1805_06604_b200 as E
+    x, r, alg, iters = gen_dense_config(args.workload, 505)
+    m, n = x.shape
+    rng = np.random.default_rng(506)
+    w0, h0 = rng.random((m, r)), rng.random((r, n))
+    steps = min(args.steps, iters)
+    cfg = E.algorithm_config(alg)
+    cfg.max_outer_iterations = args.warmup + steps
+    ctx = E.Context(0)
+    ctx.load(x)
+    ctx.begin(w0, h0, cfg)
+    ctx.step(args.warmup)
+    ctx.sync()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", 0))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    ctx.step(steps)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    recs = ctx.sync()
+    ctx.end()
+    cfg2 = E.algorithm_config(alg)
+    cfg2.max_outer_iterations = iters
+    t0 = time.perf_counter()
+    rec2 = ctx.run(x, w0, h0, cfg2, E.TimingMode.none)
+    wall = time.perf_counter() - t0
+    ctx.close()
+    cpu = None
+    if not args.no_cpu:
+        from oracle.oracle import Oracle, preset
+        orc = Oracle("reference")
+        k = 5 if args.workload == "c2" else 2
+        t0 = time.perf_counter()
+        orc.run_dense(x, w0, h0, preset(alg, max_outer_iterations=k))
+        t1 = time.perf_counter()
+        orc.run_dense(x, w0, h0, preset(alg, max_outer_iterations=0))
+        t2 = time.perf_counter()
+        cpu = {"value": k / max((t1 - t0) - (t2 - t1), 1e-9), "unit": UNIT, "cores": 1, "kind": "reference",
+               "sample": f"{k} outer iterations of enmf::run on the same matrix (setup subtracted via a "
+                         f"0-iteration run); one run is single-threaded in the reference"}
+    line = {"metric": f"{alg} outer iters/sec, {args.workload.upper()} {m}×{n} r={r}",
+            "value": steps / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded numpy, BASELINE.json description)",
+            "config": {"workload": f"{args.workload.upper()}: BASELINE.json configs[{1 if args.workload == 'c2' else 2}]",
+                       "m": m, "n": n, "r": r, "algorithm": alg},
+            "e2e": {"value": iters / wall, "unit": UNIT, "seconds": wall, "iterations": iters,
+                    "h2d_bytes_per_step": int((m * n + (m + n) * r) * 8),
+                    "d2h_bytes_per_step": int((m + n) * r * 8)},
+            "cpu_baseline": cpu, "final_relative_error": rec2.final_relative_error()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -557,8 +634,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tf32", action="store_true")
-    ap.add_argument("--workload", default="c5", choices=["c5", "c4"],
-                    help="c5: the headline (default); c4: the CSR document matrix (extra line)")
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4"],
+                    help="c5: the headline (default); c2 / c3 / c4: the other BASELINE configs (extra lines)")
     ap.add_argument("--cpu-threads", type=int, default=64)
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per GEMM launch from an ncu --set full capture (profiles/)")
@@ -572,6 +649,8 @@ def main():
         return run_reference(args, rank, world)
     if args.workload == "c4":
         return run_c4(args)
+    if args.workload in ("c2", "c3"):
+        return run_dense_config(args)
     if world > 1:
         import torch
         import torch.distributed as dist
