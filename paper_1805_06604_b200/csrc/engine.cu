@@ -95,8 +95,9 @@ struct enmf_gpu_ctx {
     DBuf<int> e;
     const double* src = nullptr;
     long rows = 0, cols = 0;
-    bool ready = false;
-  } xd_full, xd_cols, xd_rows;
+    bool ready = false, by_row = false;
+    int levels = 7;                        // digit levels used (ozaki::combine's S)
+  } xd_xt, xd_x, xd_cols, xd_rows;          // one GPU: X scaled per row (T·Xᵀ) / per column (W_yᵀX)
   DBuf<int8_t> adig;
   DBuf<int> aexp;
   DBuf<int> ocbuf;
@@ -917,21 +918,39 @@ bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
          c->m % 16 == 0 && c->n % 16 == 0 && (!dist || (c->dist->mp % 16 == 0 && c->dist->np % 16 == 0));
 }
 
-// digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph)
+// digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph).
+// by_row: one exponent per X row (the operand of T·Xᵀ, whose output columns are X's rows);
+// otherwise one per X column (W_yᵀX) — so the product's precision follows each output
+// column's own scale, not X's global maximum.
 void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, const double* x, long rows,
-                     long cols) {
-  if (xd.ready && xd.src == x && xd.rows == rows && xd.cols == cols) return;
+                     long cols, bool by_row) {
+  if (xd.ready && xd.src == x && xd.rows == rows && xd.cols == cols && xd.by_row == by_row) return;
   const long mn = rows * cols;
-  xd.d.ensure((size_t)ozaki::S * mn);
-  xd.e.ensure(1);
-  c->opart.ensure(4096);
-  const int nb = (int)std::min<long>(4096, (mn + 255) / 256);
-  ozaki::absmax_partial<<<nb, 256, 0, s>>>(x, mn, c->opart.p);
-  ozaki::absmax_final<<<1, 1024, 0, s>>>(c->opart.p, nb, xd.e.p);
-  ozaki::split<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(
-      x, rows, cols, cols, xd.e.p, 0, xd.d.p, nullptr);
+  xd.d.ensure((size_t)ozaki::SMAX * mn);
+  xd.e.ensure((size_t)(by_row ? rows : cols));
+  // digit levels: the neglected terms of level S scale with K·max|a|·max|b| / |sum a·b|; the
+  // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
+  // along it stands in for both operands: 7 levels when it is at most 2.5, else 8
+  c->opart.ensure(1);
+  CU(cudaMemsetAsync(c->opart.p, 0, sizeof(double), s));
+  auto* rb = reinterpret_cast<unsigned long long*>(c->opart.p);
+  if (by_row) ozaki::row_range<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, rb);
+  else ozaki::col_range<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(x, rows, cols,
+                                                                                                     cols, rb);
   CUK();
-  c->launches += 3;
+  double ratio = 0.0;
+  CU(cudaMemcpyAsync(&ratio, c->opart.p, sizeof ratio, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  xd.levels = ratio <= 2.5 ? 7 : 8;
+  c->launches++;
+  if (by_row) ozaki::row_exp<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, xd.e.p, nullptr);
+  else ozaki::col_exp<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(x, rows, cols,
+                                                                                                   cols, xd.e.p);
+  ozaki::split<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(
+      x, rows, cols, cols, xd.e.p, by_row ? 1 : 2, xd.d.p, nullptr);
+  CUK();
+  c->launches += 2;
+  xd.by_row = by_row;
   xd.src = x;
   xd.rows = rows;
   xd.cols = cols;
@@ -944,34 +963,36 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
                  const DevState* st, const enmf_gpu_ctx::XDig& xd) {
   const long K = tn ? xd.cols : xd.rows, N = tn ? xd.rows : xd.cols;
   const long mn = xd.rows * xd.cols;
-  c->adig.ensure((size_t)ozaki::S * r * K);
+  const int S = xd.levels;
+  c->adig.ensure((size_t)ozaki::SMAX * r * K);
   c->aexp.ensure((size_t)r);
   // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
   // are slow below 256 rows with an N-contiguous B, so short stacks are padded with further
   // (unused) digits there
   ozaki::Offsets off{};
-  int Mq[ozaki::S];
+  int Mq[ozaki::SMAX];
   long acc = 0;
-  for (int q = 0; q < ozaki::S; ++q) {
-    Mq[q] = (ozaki::S - q) * r;
-    if (!tn && Mq[q] < 256) Mq[q] = std::min(256, ozaki::S * r);
+  for (int q = 0; q < S; ++q) {
+    Mq[q] = (S - q) * r;
+    if (!tn && Mq[q] < 256) Mq[q] = std::min(256, ozaki::SMAX * r);
     off.q[q] = acc;
     acc += (long)Mq[q] * N;
   }
   // one size for both products of this (m, n, r): no reallocation between captured launches
-  c->ocbuf.ensure(std::max((size_t)acc, ((size_t)ozaki::PAIRS * r + 256) * std::max(c->m, c->n)));
+  c->ocbuf.ensure(std::max((size_t)acc, ((size_t)(ozaki::SMAX * (ozaki::SMAX + 1) / 2) * r + 256) *
+                                            std::max(c->m, c->n)));
   if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
   ozaki::row_exp<<<r, 256, 0, s>>>(A, K, lda, c->aexp.p, st);
   ozaki::split<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
       A, r, K, lda, c->aexp.p, 1, c->adig.p, st);
   CUK();
   c->launches += 2;
-  for (int q = 0; q < ozaki::S; ++q)
+  for (int q = 0; q < S; ++q)
     lt_gemm(c, s, c->adig.p, xd.d.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
   ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
-      c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
+      c->ocbuf.p, off, S, r, N, c->aexp.p, xd.e.p, out, ldo, st);
   CUK();
-  c->launches += 1 + ozaki::S;
+  c->launches += 1 + S;
 }
 
 // ---- TF32 variant of the cross products (ENMF_PRECISION_TF32) -----------------
@@ -1192,7 +1213,7 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
   } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
     tf32_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-    ozaki_cross(c, s, L.wyfull, m, r, false, c->CH.p, nl, st, D ? c->xd_cols : c->xd_full);
+    ozaki_cross(c, s, L.wyfull, m, r, false, c->CH.p, nl, st, D ? c->xd_cols : c->xd_x);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
@@ -1228,7 +1249,7 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
     } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
       tf32_cross(c, s, Tm, n, r, true, out, m, st);
     } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-      ozaki_cross(c, s, D ? L.tfull : Tm, n, r, true, out, ml, st, D ? c->xd_rows : c->xd_full);
+      ozaki_cross(c, s, D ? L.tfull : Tm, n, r, true, out, ml, st, D ? c->xd_rows : c->xd_xt);
     } else if (pl.prec == PREC_EXACT) {
       gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
       CUK();
@@ -1441,13 +1462,14 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     tf32_cross(c, s, c->H.p, (long)n, (int)r, true, c->P.p, (long)m, st);
   } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
     if (D) {                             // once per loaded X (outside the iteration graph)
-      ozaki_prepare_x(c, s, c->xd_cols, D->xc, (long)m, (long)D->np);
-      ozaki_prepare_x(c, s, c->xd_rows, D->xr, (long)D->mp, (long)n);
+      ozaki_prepare_x(c, s, c->xd_cols, D->xc, (long)m, (long)D->np, false);
+      ozaki_prepare_x(c, s, c->xd_rows, D->xr, (long)D->mp, (long)n, true);
     } else {
-      ozaki_prepare_x(c, s, c->xd_full, c->x, (long)m, (long)n);
+      ozaki_prepare_x(c, s, c->xd_x, c->x, (long)m, (long)n, false);
+      ozaki_prepare_x(c, s, c->xd_xt, c->x, (long)m, (long)n, true);
     }
     ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
-                D ? c->xd_rows : c->xd_full);
+                D ? c->xd_rows : c->xd_xt);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);

@@ -23,8 +23,9 @@
 
 namespace ozaki {
 
-constexpr int S = 7;                      // digits per operand (7 bits each)
-constexpr int PAIRS = S * (S + 1) / 2;    // digit products kept (p + q < S)
+constexpr int SMAX = 8;                   // digits cut per operand (7 bits each)
+// digit levels kept, S ∈ {7, 8}: products d_p·d_q with p + q < S (S(S+1)/2 of them).  7 levels
+// for X with a narrow per-row / per-column dynamic range, 8 otherwise (see ozaki_levels)
 
 // largest |x| → exponent e with |x| / 2^e < 1 (0 when all zero)
 ENMF_DEV int exp_above(double mx) {
@@ -80,17 +81,70 @@ __global__ void row_exp(const double* __restrict__ a, long K, long lda, int* e, 
   }
 }
 
+// e[k] for max_i |a[i][k]| of an R × K row-major matrix (thread per column, coalesced rows)
+__global__ void col_exp(const double* __restrict__ a, long R, long K, long lda, int* e) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
+    double m = 0.0;
+    for (long i = 0; i < R; ++i) m = fmax(m, fabs(a[i * lda + k]));
+    e[k] = exp_above(m);
+  }
+}
+
+// Dynamic range of an R × K row-major matrix along K: ratio[0] = max over rows of
+// max_k |a| / mean_k |a| (rows with a zero sum are skipped).  One block per row.
+__global__ void row_range(const double* __restrict__ a, long K, long lda, unsigned long long* ratio_bits) {
+  __shared__ double smax[32], ssum[32];
+  const double* row = a + (long)blockIdx.x * lda;
+  double m = 0.0, t = 0.0;
+  for (long k = threadIdx.x; k < K; k += blockDim.x) {
+    const double v = fabs(row[k]);
+    m = fmax(m, v);
+    t += v;
+  }
+  for (int o = 16; o; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  if ((threadIdx.x & 31) == 0) { smax[threadIdx.x >> 5] = m; ssum[threadIdx.x >> 5] = t; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tt = 0.0;
+    m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      m = fmax(m, smax[w]);
+      tt += ssum[w];
+    }
+    if (tt > 0.0) {
+      const double ratio = m * (double)K / tt;      // positive: the bit pattern orders like the value
+      atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(ratio));
+    }
+  }
+}
+// Same along the rows: thread per column.
+__global__ void col_range(const double* __restrict__ a, long R, long K, long lda, unsigned long long* ratio_bits) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
+    double m = 0.0, t = 0.0;
+    for (long i = 0; i < R; ++i) {
+      const double v = fabs(a[i * lda + k]);
+      m = fmax(m, v);
+      t += v;
+    }
+    if (t > 0.0) atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(m * (double)R / t));
+  }
+}
+
 // digits of an R × K matrix (row-major, lda) into out[p][i][k] (row stride K,
 // digit stride R·K); row i is scaled by 2^-e[i] (per_row) or 2^-e[0].
-__global__ void split(const double* __restrict__ a, long R, long K, long lda, const int* e, int per_row,
+// scale: 0 = one exponent e[0], 1 = per row e[i], 2 = per column e[k]; SMAX digits
+__global__ void split(const double* __restrict__ a, long R, long K, long lda, const int* e, int scale,
                       int8_t* __restrict__ out, const DevState* st) {
   if (st && !dev_active(st)) return;
   const long total = R * K, dstride = R * K;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
     const long i = idx / K, k = idx - i * K;
-    double r = ldexp(a[i * lda + k], -e[per_row ? i : 0]);   // exact, |r| < 1
+    double r = ldexp(a[i * lda + k], -e[scale == 1 ? i : scale == 2 ? k : 0]);   // exact, |r| < 1
 #pragma unroll
-    for (int p = 0; p < S; ++p) {
+    for (int p = 0; p < SMAX; ++p) {
       r *= 128.0;                      // exact
       const double d = trunc(r);       // |d| <= 127
       r -= d;                          // exact
@@ -101,23 +155,25 @@ __global__ void split(const double* __restrict__ a, long R, long K, long lda, co
 
 // out[i][j] = sum_{q} sum_{p < S-q} 2^{ea_i + eb - 7(p+q+2)} · Cq[p·R + i][j],  Cq = C + off.q[q]
 // (FP64, smallest weight first).  out row stride ldo.
-struct Offsets { long q[S]; };   // start of digit GEMM q's output (its rows p·R + i, p < S - q)
+struct Offsets { long q[SMAX]; };   // start of digit GEMM q's output (its rows p·R + i, p < S - q)
 
-__global__ void combine(const int* __restrict__ C, Offsets off, long R, long N, const int* ea, const int* eb,
-                        double* __restrict__ out, long ldo, const DevState* st) {
+// eb: the X digits' exponents, per output column j (X scaled per row for T·Xᵀ, per column for W_yᵀX)
+__global__ void combine(const int* __restrict__ C, Offsets off, int S, long R, long N, const int* ea,
+                        const int* eb, double* __restrict__ out, long ldo, const DevState* st) {
   if (st && !dev_active(st)) return;
   const long total = R * N;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
     const long i = idx / N, j = idx - i * N;
-    const int base = ea[i] + eb[0];
+    const int base = ea[i] + eb[j];
     double acc = 0.0;
 #pragma unroll
-    for (int w = S - 1; w >= 0; --w) {            // w = p + q, weight 2^{-7(w+2)}
+    for (int w = SMAX - 1; w >= 0; --w) {         // w = p + q, weight 2^{-7(w+2)}
+      if (w >= S) continue;
       double part = 0.0;                         // sum of the exact int32 terms of this weight
 #pragma unroll
-      for (int q = 0; q < S; ++q) {
+      for (int q = 0; q < SMAX; ++q) {
         const int p = w - q;
-        if (p < 0 || p >= S - q) continue;
+        if (p < 0 || q >= S) continue;
         part += (double)C[off.q[q] + (p * R + i) * N + j];   // |part| < 2^34: exact in FP64
       }
       acc += ldexp(part, base - 7 * (w + 2));

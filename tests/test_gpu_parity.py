@@ -456,3 +456,20 @@ def test_ragged_shapes_parity(ctx, port, shape):
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
     assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+
+
+def test_int8_digit_products_wide_dynamic_range(ctx, port):
+    """X with rows and columns scaled over six orders of magnitude (document lengths, image
+    intensities): the INT8-digit products scale X per row (T·Xᵀ) and per column (W_yᵀX), so every
+    output keeps FP64-level relative accuracy; vs the oracle at 4096×4096 r=32."""
+    m = n = 4096
+    r = 32
+    rng = np.random.default_rng(41)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    x *= 10.0 ** rng.uniform(-3, 3, (m, 1))
+    x *= 10.0 ** rng.uniform(-3, 3, (1, n))
+    w0, h0 = port.random_init(m, n, r, 42)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=5))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 5), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
