@@ -930,7 +930,8 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   xd.e.ensure((size_t)(by_row ? rows : cols));
   // digit levels: the neglected terms of level S scale with K·max|a|·max|b| / |sum a·b|; the
   // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
-  // along it stands in for both operands: 7 levels when it is at most 2.5, else 8
+  // along it stands in for both operands: 7 levels up to 2.5, 8 up to 16, beyond that the
+  // product stays on the FP64 DMMA GEMM (levels = 0)
   c->opart.ensure(1);
   CU(cudaMemsetAsync(c->opart.p, 0, sizeof(double), s));
   auto* rb = reinterpret_cast<unsigned long long*>(c->opart.p);
@@ -941,7 +942,7 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   double ratio = 0.0;
   CU(cudaMemcpyAsync(&ratio, c->opart.p, sizeof ratio, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  xd.levels = ratio <= 2.5 ? 7 : 8;
+  xd.levels = ratio <= 2.5 ? 7 : ratio <= 16.0 ? 8 : 0;
   c->launches++;
   if (by_row) ozaki::row_exp<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, xd.e.p, nullptr);
   else ozaki::col_exp<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(x, rows, cols,
@@ -958,12 +959,14 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
 }
 
 // out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · (tn ? Xdᵀ : Xd) in FP64 accuracy,
-// Xd = the digit-cut operand (tn: N = rows, K = cols; !tn: K = rows, N = cols).
-void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
+// Xd = the digit-cut operand (tn: N = rows, K = cols; !tn: K = rows, N = cols).  Returns false
+// (nothing enqueued) when X's dynamic range puts this product on the DMMA GEMM instead.
+bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
                  const DevState* st, const enmf_gpu_ctx::XDig& xd) {
   const long K = tn ? xd.cols : xd.rows, N = tn ? xd.rows : xd.cols;
   const long mn = xd.rows * xd.cols;
   const int S = xd.levels;
+  if (S == 0) return false;
   c->adig.ensure((size_t)ozaki::SMAX * r * K);
   c->aexp.ensure((size_t)r);
   // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
@@ -993,6 +996,7 @@ void ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
       c->ocbuf.p, off, S, r, N, c->aexp.p, xd.e.p, out, ldo, st);
   CUK();
   c->launches += 1 + S;
+  return true;
 }
 
 // ---- TF32 variant of the cross products (ENMF_PRECISION_TF32) -----------------
@@ -1212,8 +1216,9 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
     sparse_wx(c, s, pl.prec == PREC_EXACT, c->WyT.p, r, c->CH.p, st);
   } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
     tf32_cross(c, s, c->WyT.p, m, r, false, c->CH.p, n, st);
-  } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-    ozaki_cross(c, s, L.wyfull, m, r, false, c->CH.p, nl, st, D ? c->xd_cols : c->xd_x);
+  } else if (ozaki_enabled(c, pl.prec, D != nullptr) &&
+             ozaki_cross(c, s, L.wyfull, m, r, false, c->CH.p, nl, st, D ? c->xd_cols : c->xd_x)) {
+    // on the INT8 tensor cores
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_wx_exact<<<grid_for(hsz, 128, 1 << 30), 128, 0, s>>>(c->WyT.p, c->x, m, n, r, c->CH.p, st);
     CUK();
@@ -1248,8 +1253,9 @@ void enqueue_iteration(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, cudaGrap
       sparse_xht(c, s, pl.prec == PREC_EXACT, Tm, r, out, st);
     } else if (tf32_enabled(c, pl.prec, D != nullptr)) {
       tf32_cross(c, s, Tm, n, r, true, out, m, st);
-    } else if (ozaki_enabled(c, pl.prec, D != nullptr)) {
-      ozaki_cross(c, s, D ? L.tfull : Tm, n, r, true, out, ml, st, D ? c->xd_rows : c->xd_xt);
+    } else if (ozaki_enabled(c, pl.prec, D != nullptr) &&
+               ozaki_cross(c, s, D ? L.tfull : Tm, n, r, true, out, ml, st, D ? c->xd_rows : c->xd_xt)) {
+      // on the INT8 tensor cores
     } else if (pl.prec == PREC_EXACT) {
       gemm::cross_xht_exact<<<grid_for(wsz, 128, 1 << 30), 128, 0, s>>>(c->x, Tm, m, n, r, out, st);
       CUK();
@@ -1468,8 +1474,10 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
       ozaki_prepare_x(c, s, c->xd_x, c->x, (long)m, (long)n, false);
       ozaki_prepare_x(c, s, c->xd_xt, c->x, (long)m, (long)n, true);
     }
-    ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
-                D ? c->xd_rows : c->xd_xt);
+    if (!ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
+                     D ? c->xd_rows : c->xd_xt))
+      gemm_launch(c, s, true, D ? L.tfull : c->H.p, n, L.xrb, L.ld_rb, c->P.p, ml, (int)r, (int)ml, (int)n, false,
+                  st);
   } else if (pl.prec == PREC_EXACT) {
     gemm::cross_xht_exact<<<grid_for((long)wsz, 128, 1 << 30), 128, 0, s>>>(c->x, c->H.p, (int)m, (int)n, (int)r,
                                                                              c->P.p, st);
