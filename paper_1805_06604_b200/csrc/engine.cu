@@ -162,15 +162,6 @@ inline void shard_bounds(size_t len, int rank, int world, size_t* off, size_t* c
 
 namespace {
 
-template <int UB, int NW>
-void attrs_sweep_t();
-template <int NW>
-void attrs_sweep_rl();
-template <int NW>
-void attrs_sweep_la();
-template <int UB, int NW>
-void attrs_sweep_cv();
-
 void set_attrs_once() {
   static bool done = false;
   if (done) return;
@@ -207,26 +198,6 @@ void set_attrs_once() {
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
   big((const void*)hals::sweep_fast<32, 4>, hals::smem_bytes<32, 4>());
-  big((const void*)hals::sweep_dmma<32>, hals::dmma_smem_bytes<32>());
-  big((const void*)hals::sweep_dmma<64>, hals::dmma_smem_bytes<64>());
-  big((const void*)hals::sweep_dmma<128>, hals::dmma_smem_bytes<128>());
-  big((const void*)hals::sweep_dmma_p<32, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<32>());
-  big((const void*)hals::sweep_dmma_p<64, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<64>());
-  big((const void*)hals::sweep_dmma_p<128, 1, hals::kDmmaWarps>, hals::dmma_smem_bytes<128>());
-  big((const void*)hals::sweep_dmma_p<32, 1, 12>, hals::dmma_smem_bytes<32>());
-  big((const void*)hals::sweep_dmma_p<64, 1, 12>, hals::dmma_smem_bytes<64>());
-  big((const void*)hals::sweep_dmma_p<128, 1, 12>, hals::dmma_smem_bytes<128>());
-  attrs_sweep_cv<2, 14>();
-  attrs_sweep_cv<1, 14>();
-  attrs_sweep_cv<2, 12>();
-  attrs_sweep_la<14>();
-  attrs_sweep_la<12>();
-  attrs_sweep_rl<14>();
-  attrs_sweep_rl<12>();
-  attrs_sweep_t<1, 14>();
-  attrs_sweep_t<2, 14>();
-  attrs_sweep_t<2, 12>();
-  attrs_sweep_t<4, 12>();
   big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
   big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
   done = true;
@@ -373,52 +344,18 @@ void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, lon
 }
 
 // ---- inner solvers ------------------------------------------------------------
-// HALS sweep kernel variant: ENMF_HALS_KERNEL=fma selects the CUDA-core
-// register kernel (A/B comparisons); default is the DMMA blocked sweep.
-// 0: persistent DMMA, 14 warps (default); 1: fma; 2: unrolled DMMA (v1);
-// 3: persistent DMMA, 12 warps (168 registers, no spills)
-// 10..13: transposed-tile DMMA sweep (NW, UB) = (14,1), (14,2), (12,2), (12,4)
 int hals_variant() {
+  // ENMF_HALS_KERNEL: "" / "wsp" persistent paired-warp kernel (default), "ws" one launch per
+  // sweep, "fma" CUDA-core kernel, "ws[p]prof*" timing experiments.  Retired variants and their
+  // measurements: profiles/r01_sweep_variants.md.
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("ENMF_HALS_KERNEL");
     const std::string s = e ? e : "";
-    v = s == "fma" ? 1 : s == "dmma1" ? 2 : s == "p12" ? 3 : s == "p14" ? 0 : s == "t14u1" ? 10
-      : s == "t14u2" ? 11 : s == "t12u2" ? 12 : s == "t12u4" ? 13 : s == "rl12" ? 21 : s == "rl14" ? 20
-      : s == "la12" ? 31 : s == "la14" ? 30 : s == "t14u2" ? 11 : s == "cv14u1" ? 41 : s == "cv12u2" ? 42 : s == "skel" ? 43 : s == "nobar" ? 44 : s == "prof" ? 45 : s == "prof1" ? 46 : s == "cv14u2" ? 40 : s == "ws" ? 50 : s == "wsp" ? 54 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53 : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58 : s == "" ? 54 : 11;  // default: ws
+    v = s == "fma" ? 1 : s == "ws" ? 50 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53
+      : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58 : 54;
   }
   return v;
-}
-
-template <int R_, int UB, int NW, int MODE = 0>
-void launch_sweep_cv(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  constexpr int cols = NW * 8;
-  const int ntiles = (a.N + cols - 1) / cols;
-  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<R_, UB, NW, MODE>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, hals::cv_smem_bytes<R_>()));
-    attr = true;
-  }
-  hals::sweep_cv<R_, UB, NW, MODE><<<grid, NW * 32, hals::cv_smem_bytes<R_>(), s>>>(a, ntiles);
-}
-
-template <int UB, int NW>
-void launch_sweep_cv_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  if (a.r <= 32) launch_sweep_cv<32, UB, NW>(c, s, a);
-  else if (a.r <= 64) launch_sweep_cv<64, UB, NW>(c, s, a);
-  else launch_sweep_cv<128, UB, NW>(c, s, a);
-}
-
-template <int UB, int NW>
-void attrs_sweep_cv() {
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<32, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::cv_smem_bytes<32>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<64, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::cv_smem_bytes<64>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_cv<128, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::cv_smem_bytes<128>()));
 }
 
 template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
@@ -451,88 +388,6 @@ void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   hals::sweep_ws<R_, PROF, SKIP><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 
-template <int R_, int NW>
-void launch_sweep_la(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  constexpr int cols = NW * 8;
-  const int ntiles = (a.N + cols - 1) / cols;
-  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-  hals::sweep_la<R_, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
-}
-
-template <int NW>
-void launch_sweep_la_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  if (a.r <= 32) launch_sweep_la<32, NW>(c, s, a);
-  else if (a.r <= 64) launch_sweep_la<64, NW>(c, s, a);
-  else launch_sweep_la<128, NW>(c, s, a);
-}
-
-template <int NW>
-void attrs_sweep_la() {
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<32, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::dmma_smem_bytes<32>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<64, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::dmma_smem_bytes<64>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_la<128, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::dmma_smem_bytes<128>()));
-}
-
-template <int R_, int NW>
-void launch_sweep_rl(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  constexpr int cols = NW * 8;
-  const int ntiles = (a.N + cols - 1) / cols;
-  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-  hals::sweep_rl<R_, NW><<<grid, NW * 32, hals::rl_smem_bytes<R_>(), s>>>(a, ntiles);
-}
-
-template <int NW>
-void launch_sweep_rl_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  if (a.r <= 32) launch_sweep_rl<32, NW>(c, s, a);
-  else if (a.r <= 64) launch_sweep_rl<64, NW>(c, s, a);
-  else launch_sweep_rl<128, NW>(c, s, a);
-}
-
-template <int NW>
-void attrs_sweep_rl() {
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<32, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::rl_smem_bytes<32>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<64, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::rl_smem_bytes<64>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<128, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::rl_smem_bytes<128>()));
-}
-
-template <int R_, int UB, int NW>
-void launch_sweep_t(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  constexpr int cols = NW * 8;
-  const int ntiles = (a.N + cols - 1) / cols;
-  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-  hals::sweep_dmma_t<R_, UB, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
-}
-
-template <int UB, int NW>
-void launch_sweep_t_r(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  if (a.r <= 32) launch_sweep_t<32, UB, NW>(c, s, a);
-  else if (a.r <= 64) launch_sweep_t<64, UB, NW>(c, s, a);
-  else launch_sweep_t<128, UB, NW>(c, s, a);
-}
-
-template <int UB, int NW>
-void attrs_sweep_t() {
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<32, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::dmma_smem_bytes<32>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<64, UB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          hals::dmma_smem_bytes<64>()));
-  CU(cudaFuncSetAttribute((const void*)hals::sweep_dmma_t<128, UB, NW>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, hals::dmma_smem_bytes<128>()));
-}
-
-template <int R_, int NW>
-void launch_sweep_p(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  constexpr int cols = NW * 8;
-  const int ntiles = (a.N + cols - 1) / cols;
-  const unsigned grid = (unsigned)std::min(ntiles, c->sms);
-  hals::sweep_dmma_p<R_, 1, NW><<<grid, NW * 32, hals::dmma_smem_bytes<R_>(), s>>>(a, ntiles);
-}
 bool hals_use_fma() { return hals_variant() == 1; }
 
 // The persistent sweep kernel runs a whole inner solve in one launch.
@@ -548,7 +403,8 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     c->launches += 2;
     return;
   }
-  if (hals_use_fma()) {
+  const int v = hals_variant();
+  if (v == 1) {
 #define SW(S_, T_)                                                                          \
   hals::sweep_fast<S_, T_><<<(a.N + hals::NT / T_ - 1) / (hals::NT / T_), hals::NT,          \
                              hals::smem_bytes<S_, T_>(), s>>>(a)
@@ -557,74 +413,28 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     else if (r <= 64) SW(32, 2);
     else SW(32, 4);
 #undef SW
-  } else if (hals_variant() == 2) {
-    constexpr int cols = hals::kDmmaWarps * 8;
-    const unsigned grid = (unsigned)((a.N + cols - 1) / cols);
-#define SD(R_) hals::sweep_dmma<R_><<<grid, hals::kDmmaWarps * 32, hals::dmma_smem_bytes<R_>(), s>>>(a)
-    if (r <= 32) SD(32);
-    else if (r <= 64) SD(64);
-    else SD(128);
-#undef SD
-  } else if (hals_variant() == 3) {
-    if (r <= 32) launch_sweep_p<32, 12>(c, s, a);
-    else if (r <= 64) launch_sweep_p<64, 12>(c, s, a);
-    else launch_sweep_p<128, 12>(c, s, a);
-  } else if (hals_variant() == 40) {
-    launch_sweep_cv_r<2, 14>(c, s, a);
-  } else if (hals_variant() == 41) {
-    launch_sweep_cv_r<1, 14>(c, s, a);
-  } else if (hals_variant() == 42) {
-    launch_sweep_cv_r<2, 12>(c, s, a);
-  } else if (hals_variant() == 43) {   // timing experiment: skeleton (no row chain; wrong results)
-    launch_sweep_cv<128, 2, 14, 1>(c, s, a);
-  } else if (hals_variant() == 44) {   // timing experiment: no phase barriers
-    launch_sweep_cv<128, 2, 14, 2>(c, s, a);
-  } else if (hals_variant() == 45) {   // timing experiment: per-phase clock64 profile into a.terms
-    launch_sweep_cv<128, 2, 14, 3>(c, s, a);
-  } else if (hals_variant() == 46) {   // timing experiment: same, one warp per CTA (no contention)
-    launch_sweep_cv<128, 2, 1, 3>(c, s, a);
-  } else if (hals_variant() == 51) {   // timing experiment: per-warp cycle profile into a.terms
-    launch_sweep_ws<128, true>(c, s, a);
-  } else if (hals_variant() == 52) {
-    launch_sweep_ws<128, true, 1>(c, s, a);
-  } else if (hals_variant() == 53) {
-    launch_sweep_ws<128, true, 2>(c, s, a);
-  } else if (hals_variant() == 55) {   // timing experiments (persistent): profile, no row pass, no DMMA
-    launch_sweep_ws<128, true, 0, true>(c, s, a);
-  } else if (hals_variant() == 56) {
-    launch_sweep_ws<128, true, 1, true>(c, s, a);
-  } else if (hals_variant() == 57) {
-    launch_sweep_ws<128, true, 2, true>(c, s, a);
-  } else if (hals_variant() == 58) {
-    launch_sweep_ws<128, true, 3, true>(c, s, a);
-  } else if (hals_variant() == 54) {
-    if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
-    else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
-    else launch_sweep_ws<128, false, 0, true>(c, s, a);
-  } else if (hals_variant() == 50) {
+  } else if (v == 50) {                 // one launch per sweep
     if (r <= 32) launch_sweep_ws<32>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64>(c, s, a);
     else launch_sweep_ws<128>(c, s, a);
-  } else if (hals_variant() == 30) {
-    launch_sweep_la_r<14>(c, s, a);
-  } else if (hals_variant() == 31) {
-    launch_sweep_la_r<12>(c, s, a);
-  } else if (hals_variant() == 20) {
-    launch_sweep_rl_r<14>(c, s, a);
-  } else if (hals_variant() == 21) {
-    launch_sweep_rl_r<12>(c, s, a);
-  } else if (hals_variant() == 10) {
-    launch_sweep_t_r<1, 14>(c, s, a);
-  } else if (hals_variant() == 11) {
-    launch_sweep_t_r<2, 14>(c, s, a);
-  } else if (hals_variant() == 12) {
-    launch_sweep_t_r<2, 12>(c, s, a);
-  } else if (hals_variant() == 13) {
-    launch_sweep_t_r<4, 12>(c, s, a);
-  } else {
-    if (r <= 32) launch_sweep_p<32, hals::kDmmaWarps>(c, s, a);
-    else if (r <= 64) launch_sweep_p<64, hals::kDmmaWarps>(c, s, a);
-    else launch_sweep_p<128, hals::kDmmaWarps>(c, s, a);
+  } else if (v == 51) {                 // timing experiments: per-warp cycle profile into a.terms
+    launch_sweep_ws<128, true>(c, s, a);
+  } else if (v == 52) {
+    launch_sweep_ws<128, true, 1>(c, s, a);
+  } else if (v == 53) {
+    launch_sweep_ws<128, true, 2>(c, s, a);
+  } else if (v == 55) {                 // same, persistent: profile, no row pass, no DMMA, neither
+    launch_sweep_ws<128, true, 0, true>(c, s, a);
+  } else if (v == 56) {
+    launch_sweep_ws<128, true, 1, true>(c, s, a);
+  } else if (v == 57) {
+    launch_sweep_ws<128, true, 2, true>(c, s, a);
+  } else if (v == 58) {
+    launch_sweep_ws<128, true, 3, true>(c, s, a);
+  } else {                              // default: persistent, one launch per inner solve
+    if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
+    else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
+    else launch_sweep_ws<128, false, 0, true>(c, s, a);
   }
   CUK();
   c->launches++;

@@ -196,1066 +196,6 @@ __global__ void __launch_bounds__(NT) sweep_fast(Args a) {
   last_block_reduce_n<NT>(a, bg, nf, red);
 }
 
-// ---- tensor-core sweep: blocked Gauss-Seidel on DMMA ----------------------
-//
-// The r rows are processed in blocks of 8.  For block K = [k0, k0+8) and the 8
-// columns a warp owns,
-//     S = G[K, :] · H            (DMMA m8n8k4 over j, 4 independent accumulators)
-// uses the current H (rows < k0 already updated this sweep, rows >= k0 old), so
-//     b_k = C_k - sum_{j != k} G_kj h_j = C_k - S_k + G_kk h_old_k - sum_{i in K, i < k} G_ki (h_new_i - h_old_i)
-// and the 8 rows of the block are then finished sequentially with one shuffle
-// per row to forward the change δ_i.  H lives in registers in the DMMA
-// B-fragment layout: lane (g, t) holds H[4s + t][col g] in slot s.  Per sweep
-// this is r·r·N FMAs on the tensor pipe (the reference's r² per column).
-constexpr int kDmmaWarps = 14;
-
-template <int RMAX>
-constexpr int dmma_smem_bytes() {
-  return RMAX * (RMAX + 4) * 8 + 2 * RMAX * 8;
-}
-
-template <int RMAX>
-__global__ void __launch_bounds__(kDmmaWarps * 32, 1) sweep_dmma(Args a) {
-  constexpr int LDG = RMAX + 4;    // conflict-free A-fragment rows
-  constexpr int SL = RMAX / 4;     // H slots per lane
-  constexpr int NB = RMAX / 8;     // row blocks
-  constexpr int NTH = kDmmaWarps * 32;
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;                 // [RMAX][LDG]
-  double* Gd = sm + RMAX * LDG;    // G_kk (1 for padding rows)
-  double* Gi = Gd + RMAX;          // 1 / G_kk
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
-    const int k = e / RMAX, j = e % RMAX;
-    Gs[k * LDG + j] = (k < r && j < r) ? a.G[k * r + j] : 0.0;
-  }
-  for (int k = threadIdx.x; k < RMAX; k += NTH) {
-    const double d = k < r ? a.G[k * r + k] : 1.0;
-    Gd[k] = d;
-    Gi[k] = __ddiv_rn(1.0, d);
-  }
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const long c0 = ((long)blockIdx.x * kDmmaWarps + warp) * 8;
-  const long colH = c0 + g;                 // column this lane holds in the H layout
-  const bool validH = colH < a.N;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double hreg[SL];
-#pragma unroll
-  for (int s = 0; s < SL; ++s) {
-    const int j = 4 * s + t;
-    hreg[s] = (validH && j < r) ? src[(long)j * a.ld + colH] : 0.0;
-  }
-  // S-layout columns of this lane: c0 + 2t + e
-  const long colS = c0 + 2 * t;
-  const bool v0 = colS < a.N, v1 = colS + 1 < a.N;
-  auto loadC = [&](int k, double& x0, double& x1) {
-    x0 = (k < r && v0) ? a.C[(long)k * a.ld + colS] : 0.0;
-    x1 = (k < r && v1) ? a.C[(long)k * a.ld + colS + 1] : 0.0;
-  };
-  double cn0, cn1;
-  loadC(g, cn0, cn1);
-  double gain = 0.0;
-
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int k0 = 8 * b;
-    const double cc0 = cn0, cc1 = cn1;
-    if (b + 1 < NB) loadC(k0 + 8 + g, cn0, cn1);
-    // S = G[K, :] · H
-    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    const double* ga = Gs + (k0 + g) * LDG + t;
-#pragma unroll
-    for (int s = 0; s < SL; ++s) dmma884(acc[s & 3][0], acc[s & 3][1], ga[4 * s], hreg[s]);
-    const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
-    const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
-    // h_old of (row k0+g, cols colS, colS+1) from the H layout
-    const int srcA0 = (2 * t) * 4 + (g & 3), srcA1 = (2 * t + 1) * 4 + (g & 3);
-    const double lo0 = __shfl_sync(0xffffffffu, hreg[2 * b], srcA0);
-    const double lo1 = __shfl_sync(0xffffffffu, hreg[2 * b], srcA1);
-    const double hi0 = __shfl_sync(0xffffffffu, hreg[2 * b + 1], srcA0);
-    const double hi1 = __shfl_sync(0xffffffffu, hreg[2 * b + 1], srcA1);
-    const double ho0 = g < 4 ? lo0 : hi0, ho1 = g < 4 ? lo1 : hi1;
-    const int k = k0 + g;
-    const double gkk = Gd[k], ginv = Gi[k];
-    const double b0 = fma(gkk, ho0, __dsub_rn(cc0, S0));
-    const double b1 = fma(gkk, ho1, __dsub_rn(cc1, S1));
-    double gblk[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) gblk[i] = Gs[k * LDG + k0 + i];
-    double corr0 = 0.0, corr1 = 0.0, hn0 = ho0, hn1 = ho1;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      double d0 = 0.0, d1 = 0.0;
-      if (g == i) {
-        const double t0 = __dmul_rn(__dsub_rn(b0, corr0), ginv);
-        const double t1 = __dmul_rn(__dsub_rn(b1, corr1), ginv);
-        hn0 = t0 > 0.0 ? t0 : 0.0;
-        hn1 = t1 > 0.0 ? t1 : 0.0;
-        d0 = __dsub_rn(hn0, ho0);
-        d1 = __dsub_rn(hn1, ho1);
-        const double o0 = __dsub_rn(ho0, t0), n0 = __dsub_rn(hn0, t0);
-        const double o1 = __dsub_rn(ho1, t1), n1 = __dsub_rn(hn1, t1);
-        gain = fma(gkk, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-        gain = fma(gkk, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-      }
-      if (i < 7) {
-        const double e0 = __shfl_sync(0xffffffffu, d0, i * 4 + t);
-        const double e1 = __shfl_sync(0xffffffffu, d1, i * 4 + t);
-        if (g > i) {
-          corr0 = fma(gblk[i], e0, corr0);
-          corr1 = fma(gblk[i], e1, corr1);
-        }
-      }
-    }
-    // back to the H layout: lane (g', t') takes rows k0+t' and k0+4+t' of column g'
-    const int srcB_lo = t * 4 + (g >> 1), srcB_hi = (t + 4) * 4 + (g >> 1);
-    const double x0lo = __shfl_sync(0xffffffffu, hn0, srcB_lo);
-    const double x1lo = __shfl_sync(0xffffffffu, hn1, srcB_lo);
-    const double x0hi = __shfl_sync(0xffffffffu, hn0, srcB_hi);
-    const double x1hi = __shfl_sync(0xffffffffu, hn1, srcB_hi);
-    hreg[2 * b] = (g & 1) ? x1lo : x0lo;
-    hreg[2 * b + 1] = (g & 1) ? x1hi : x0hi;
-  }
-  int nf = 0;
-  if (validH) {
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-      const int j = 4 * s + t;
-      if (j < r) {
-        a.H[(long)j * a.ld + colH] = hreg[s];
-        nf |= !isfinite(hreg[s]);
-      }
-    }
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
-// ---- persistent tensor-core sweep (default) ---------------------------------
-//
-// Same blocked Gauss-Seidel as sweep_dmma, restructured after profiling
-// (profiles/r01_sweep_dmma_v1.txt: spills, i-cache misses from the fully
-// unrolled block loop, per-CTA Gram reload, predicated-off FP64 work):
-//   * persistent: one CTA per SM walks the column tiles, the Gram is staged into
-//     shared memory once per launch with cp.async;
-//   * rolled block loop: the current block's rows always sit in slots 0/1 of
-//     the register file image of H (rotated by two slots after each block), the
-//     A-fragment column is indexed by the rotation instead;
-//   * the gain is evaluated after the sequential 8-row pass, by all lanes.
-template <int RMAX, int UB = 1, int NW = kDmmaWarps>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_dmma_p(Args a, int ntiles) {
-  constexpr int LDG = RMAX + 4;
-  constexpr int SL = RMAX / 4;
-  constexpr int NB = RMAX / 8;
-  constexpr int NTH = NW * 32;
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;
-  double* Gd = sm + RMAX * LDG;
-  double* Gi = Gd + RMAX;
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  {
-    // cp.async the r×r Gram into padded rows, each row block's columns rotated
-    // by its own offset:  Gs[k][c] = G[k][(c + 8·(k/8)) mod RMAX]  (padding zero).
-    // With H's register image rotated by 8 slots per 4 blocks, every A-fragment
-    // and in-block coupling address below is a compile-time offset.
-    constexpr int CH = RMAX / 2;  // 16-byte chunks per padded row
-    const bool vec = (r % 2 == 0) && (((uintptr_t)a.G & 15) == 0);
-    for (int e = threadIdx.x; e < RMAX * CH; e += NTH) {
-      const int k = e / CH, c = (e % CH) * 2;
-      const int j = (c + 8 * (k / 8)) & (RMAX - 1);
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(Gs + k * LDG + c);
-      if (vec) {
-        const int valid = (k < r && j < r) ? 16 : 0;
-        const double* srcp = valid ? a.G + (long)k * r + j : a.G;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(srcp), "r"(valid));
-      } else {
-        Gs[k * LDG + c] = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
-        Gs[k * LDG + c + 1] = (k < r && j + 1 < r) ? a.G[(long)k * r + j + 1] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int k = threadIdx.x; k < RMAX; k += NTH) {
-      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-      Gd[k] = d;
-      Gi[k] = __ddiv_rn(1.0, d);
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double gain = 0.0;
-  int nf = 0;
-  bool first = true;
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long c0 = ((long)tile * NW + warp) * 8;
-    const long colH = c0 + g;
-    const bool validH = colH < a.N;
-    double hreg[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-      const int j = 4 * s + t;
-      hreg[s] = (validH && j < r) ? src[(long)j * a.ld + colH] : 0.0;
-    }
-    const long colS = c0 + 2 * t;
-    const bool v0 = colS < a.N, v1 = colS + 1 < a.N;
-    double cn0 = (g < r && v0) ? a.C[(long)g * a.ld + colS] : 0.0;
-    double cn1 = (g < r && v1) ? a.C[(long)g * a.ld + colS + 1] : 0.0;
-    if (first) {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-      __syncthreads();
-      first = false;
-    }
-    const int srcA0 = (2 * t) * 4 + (g & 3), srcA1 = (2 * t + 1) * 4 + (g & 3);
-    const int srcB_lo = t * 4 + (g >> 1), srcB_hi = (t + 4) * 4 + (g >> 1);
-    const double* gbase = Gs + g * LDG + t;
-#pragma unroll 1
-    for (int q = 0; q < NB / UB; ++q) {
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int b = UB * q + u;
-      const int k0 = 8 * b;
-      const int k = k0 + g;
-      const double cc0 = cn0, cc1 = cn1;
-      if (b + 1 < NB) {
-        const int kn = k + 8;
-        cn0 = (kn < r && v0) ? a.C[(long)kn * a.ld + colS] : 0.0;
-        cn1 = (kn < r && v1) ? a.C[(long)kn * a.ld + colS + 1] : 0.0;
-      }
-      // S = G[K, :] · H ; slot s holds original slot (s + 8q) mod SL, i.e. rows
-      // 4((s + 8q) mod SL) + t, stored at rotated column (4s - 8u) mod RMAX + t.
-      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      const double* ga = gbase + k0 * LDG;
-#pragma unroll
-      for (int s = 0; s < SL; ++s) {
-        const int col = (4 * s - 8 * u + RMAX) & (RMAX - 1);
-        dmma884(acc[s & 3][0], acc[s & 3][1], ga[col], hreg[s]);
-      }
-      const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
-      const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
-      const double lo0 = __shfl_sync(0xffffffffu, hreg[2 * u], srcA0);
-      const double lo1 = __shfl_sync(0xffffffffu, hreg[2 * u], srcA1);
-      const double hi0 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], srcA0);
-      const double hi1 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], srcA1);
-      const double ho0 = g < 4 ? lo0 : hi0, ho1 = g < 4 ? lo1 : hi1;
-      const double gkk = Gd[k], ginv = Gi[k];
-      const double b0 = fma(gkk, ho0, __dsub_rn(cc0, S0));
-      const double b1 = fma(gkk, ho1, __dsub_rn(cc1, S1));
-      double corr0 = 0.0, corr1 = 0.0, hn0 = ho0, hn1 = ho1, t0 = 0.0, t1 = 0.0;
-      const double* gk = Gs + k * LDG;  // G[k][k0 + i] sits at rotated column i
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double gki = gk[i];
-        double d0 = 0.0, d1 = 0.0;
-        if (g == i) {
-          t0 = __dmul_rn(__dsub_rn(b0, corr0), ginv);
-          t1 = __dmul_rn(__dsub_rn(b1, corr1), ginv);
-          hn0 = t0 > 0.0 ? t0 : 0.0;
-          hn1 = t1 > 0.0 ? t1 : 0.0;
-          d0 = __dsub_rn(hn0, ho0);
-          d1 = __dsub_rn(hn1, ho1);
-        }
-        if (i < 7) {
-          const double e0 = __shfl_sync(0xffffffffu, d0, i * 4 + t);
-          const double e1 = __shfl_sync(0xffffffffu, d1, i * 4 + t);
-          if (g > i) {
-            corr0 = fma(gki, e0, corr0);
-            corr1 = fma(gki, e1, corr1);
-          }
-        }
-      }
-      {
-        const double o0 = __dsub_rn(ho0, t0), n0 = __dsub_rn(hn0, t0);
-        const double o1 = __dsub_rn(ho1, t1), n1 = __dsub_rn(hn1, t1);
-        gain = fma(gkk, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-        gain = fma(gkk, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-      }
-      const double x0lo = __shfl_sync(0xffffffffu, hn0, srcB_lo);
-      const double x1lo = __shfl_sync(0xffffffffu, hn1, srcB_lo);
-      const double x0hi = __shfl_sync(0xffffffffu, hn0, srcB_hi);
-      const double x1hi = __shfl_sync(0xffffffffu, hn1, srcB_hi);
-      hreg[2 * u] = (g & 1) ? x1lo : x0lo;
-      hreg[2 * u + 1] = (g & 1) ? x1hi : x0hi;
-    }
-    // rotate the register image by 8 slots: the next 4 blocks' rows move to slots 0..7
-    {
-      double tmp[2 * UB];
-#pragma unroll
-      for (int s = 0; s < 2 * UB; ++s) tmp[s] = hreg[s];
-#pragma unroll
-      for (int s = 0; s + 2 * UB < SL; ++s) hreg[s] = hreg[s + 2 * UB];
-#pragma unroll
-      for (int s = 0; s < 2 * UB; ++s) hreg[SL - 2 * UB + s] = tmp[s];
-    }
-    }
-    // after NB/4 groups the rotation is back to the identity (8·NB/4 = SL)
-    if (validH) {
-#pragma unroll
-      for (int s = 0; s < SL; ++s) {
-        const int j = 4 * s + t;
-        if (j < r) {
-          a.H[(long)j * a.ld + colH] = hreg[s];
-          nf |= !isfinite(hreg[s]);
-        }
-      }
-    }
-  }
-  if (first) {
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
-// ---- transposed-tile tensor-core sweep (default) -----------------------------
-//
-// As sweep_dmma_p, but the DMMA computes the block's products column-major,
-//     D[col][row] = sum_j H[j][col] · G[k0+row][j]      (A = H fragment, B = G fragment),
-// so lane (g, t) ends up with rows k0+2t, k0+2t+1 of column g.  In the
-// sequential 8-row pass every active lane then finishes ONE (row, column)
-// element per step and 8 lanes (one per column) are active instead of 4
-// lanes × 2 columns: half the FP64 instructions of the pass.  δ of a row is
-// forwarded inside the lane quad of its column.
-template <int RMAX, int UB, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_dmma_t(Args a, int ntiles) {
-  constexpr int LDG = RMAX + 4;
-  constexpr int SL = RMAX / 4;
-  constexpr int NB = RMAX / 8;
-  constexpr int NTH = NW * 32;
-  static_assert(NB % UB == 0, "row blocks per group");
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;
-  double* Gd = sm + RMAX * LDG;
-  double* Gi = Gd + RMAX;
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  {
-    // Gs[k][c] = G[k][(c + 8·(k/8)) mod RMAX] (see sweep_dmma_p), zero padding
-    constexpr int CH = RMAX / 2;
-    const bool vec = (r % 2 == 0) && (((uintptr_t)a.G & 15) == 0);
-    for (int e = threadIdx.x; e < RMAX * CH; e += NTH) {
-      const int k = e / CH, c = (e % CH) * 2;
-      const int j = (c + 8 * (k / 8)) & (RMAX - 1);
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(Gs + k * LDG + c);
-      if (vec) {
-        const int valid = (k < r && j < r) ? 16 : 0;
-        const double* srcp = valid ? a.G + (long)k * r + j : a.G;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(srcp), "r"(valid));
-      } else {
-        Gs[k * LDG + c] = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
-        Gs[k * LDG + c + 1] = (k < r && j + 1 < r) ? a.G[(long)k * r + j + 1] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int k = threadIdx.x; k < RMAX; k += NTH) {
-      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-      Gd[k] = d;
-      Gi[k] = __ddiv_rn(1.0, d);
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double gain = 0.0;
-  int nf = 0;
-  bool first = true;
-  // gather sources (H layout -> tile layout): rows k0+2t+e live in lane (g, (2t+e)&3)
-  const int sg0 = g * 4 + ((2 * t) & 3), sg1 = g * 4 + ((2 * t + 1) & 3);
-  const bool upper = t >= 2;  // rows k0+4.. (second slot of the block)
-  // scatter sources (tile layout -> H layout): row k0+t lives in lane (g, t/2) elem t&1,
-  // row k0+4+t in lane (g, 2 + t/2) elem t&1
-  const int ss_lo = g * 4 + (t >> 1), ss_hi = g * 4 + 2 + (t >> 1);
-  const bool odd = t & 1;
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long col = ((long)tile * NW + warp) * 8 + g;   // this lane's column (both layouts)
-    const bool valid = col < a.N;
-    double hreg[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-      const int j = 4 * s + t;
-      hreg[s] = (valid && j < r) ? src[(long)j * a.ld + col] : 0.0;
-    }
-    const double* cp = a.C + col;
-    double cn0 = (valid && 2 * t < r) ? cp[(long)(2 * t) * a.ld] : 0.0;
-    double cn1 = (valid && 2 * t + 1 < r) ? cp[(long)(2 * t + 1) * a.ld] : 0.0;
-    if (first) {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-      __syncthreads();
-      first = false;
-    }
-    const double* gbase = Gs + g * LDG + t;   // B fragment: G[k0 + g][rotated col + t]
-#pragma unroll 1
-    for (int q = 0; q < NB / UB; ++q) {
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int b = UB * q + u;
-        const int k0 = 8 * b;
-        const int ka = k0 + 2 * t;          // this lane's two rows: ka, ka+1
-        const double cc0 = cn0, cc1 = cn1;
-        if (b + 1 < NB) {
-          cn0 = (valid && ka + 8 < r) ? cp[(long)(ka + 8) * a.ld] : 0.0;
-          cn1 = (valid && ka + 9 < r) ? cp[(long)(ka + 9) * a.ld] : 0.0;
-        }
-        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-        const double* gb = gbase + k0 * LDG;
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-          const int c = (4 * s - 8 * u + RMAX) & (RMAX - 1);
-          dmma884(acc[s & 3][0], acc[s & 3][1], hreg[s], gb[c]);
-        }
-        const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
-        const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
-        // h_old of rows ka, ka+1 (slot 2u for rows k0..k0+3, 2u+1 for k0+4..k0+7)
-        const double xa0 = __shfl_sync(0xffffffffu, hreg[2 * u], sg0);
-        const double xb0 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg0);
-        const double xa1 = __shfl_sync(0xffffffffu, hreg[2 * u], sg1);
-        const double xb1 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg1);
-        const double x0 = upper ? xb0 : xa0, x1 = upper ? xb1 : xa1;
-        const double* gk0 = Gs + ka * LDG;        // G[ka][k0 + i] at rotated column i
-        const double* gk1 = gk0 + LDG;
-        const double g00 = Gd[ka], g11 = Gd[ka + 1];
-        const double i00 = Gi[ka], i11 = Gi[ka + 1];
-        double b0 = fma(g00, x0, __dsub_rn(cc0, S0));
-        double b1 = fma(g11, x1, __dsub_rn(cc1, S1));
-        double h0 = x0, h1 = x1, t0 = 0.0, t1 = 0.0;
-        // sequential pass: row k0+i is element i&1 of lane t = i/2
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          double d0 = 0.0, d1 = 0.0;
-          if (2 * t == i) {
-            t0 = __dmul_rn(b0, i00);
-            h0 = t0 > 0.0 ? t0 : 0.0;
-            d0 = __dsub_rn(h0, x0);
-            b1 = fma(-gk1[i], d0, b1);            // row ka+1 sees row ka at once
-            t1 = __dmul_rn(b1, i11);
-            h1 = t1 > 0.0 ? t1 : 0.0;
-            d1 = __dsub_rn(h1, x1);
-          }
-          if (i < 6) {
-            const double e0 = __shfl_sync(0xffffffffu, d0, g * 4 + i / 2);
-            const double e1 = __shfl_sync(0xffffffffu, d1, g * 4 + i / 2);
-            if (2 * t > i) {
-              b0 = fma(-gk0[i], e0, b0);
-              b0 = fma(-gk0[i + 1], e1, b0);
-              b1 = fma(-gk1[i], e0, b1);
-              b1 = fma(-gk1[i + 1], e1, b1);
-            }
-          }
-        }
-        {
-          const double o0 = __dsub_rn(x0, t0), n0 = __dsub_rn(h0, t0);
-          const double o1 = __dsub_rn(x1, t1), n1 = __dsub_rn(h1, t1);
-          gain = fma(g00, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-          gain = fma(g11, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-        }
-        // back to the H layout
-        const double y0 = __shfl_sync(0xffffffffu, h0, ss_lo);
-        const double y1 = __shfl_sync(0xffffffffu, h1, ss_lo);
-        const double z0 = __shfl_sync(0xffffffffu, h0, ss_hi);
-        const double z1 = __shfl_sync(0xffffffffu, h1, ss_hi);
-        hreg[2 * u] = odd ? y1 : y0;
-        hreg[2 * u + 1] = odd ? z1 : z0;
-      }
-      if (NB / UB > 1) {
-        double tmp[2 * UB];
-#pragma unroll
-        for (int s = 0; s < 2 * UB; ++s) tmp[s] = hreg[s];
-#pragma unroll
-        for (int s = 0; s + 2 * UB < SL; ++s) hreg[s] = hreg[s + 2 * UB];
-#pragma unroll
-        for (int s = 0; s < 2 * UB; ++s) hreg[SL - 2 * UB + s] = tmp[s];
-      }
-    }
-    if (valid) {
-#pragma unroll
-      for (int s = 0; s < SL; ++s) {
-        const int j = 4 * s + t;
-        if (j < r) {
-          a.H[(long)j * a.ld + col] = hreg[s];
-          nf |= !isfinite(hreg[s]);
-        }
-      }
-    }
-  }
-  if (first) {
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
-// ---- phase-convoy tensor-core sweep (default) --------------------------------
-//
-// Measured on B200 (tools/probe/contend_probe.cu, profiles/r01_notes.md): FP64
-// scalar instructions share the FP64 pipe with DMMA, and a dependent DADD/DMUL
-// waits ~16 cycles per DMMA-issuing warp on its SM sub-partition (8 -> 56
-// cycles with three).  The row-by-row block solve is a chain of such ops, so
-// interleaving it with other warps' DMMAs (all previous variants) stretches it
-// ~5×.  Here all warps of the CTA move in lock-step phases separated by
-// __syncthreads: every warp issues its block products (DMMA phase, pipe
-// saturated), then every warp solves its block (scalar phase, pipe free).
-// The solve chain is also shortened: the diagonal block's lower triangle
-// (diagonal included) is zeroed in the DMMA operand, so
-//     b_k = C_k - S_k - sum_{j<k in block} G_kj h_new_j
-// needs one DMUL + one DFMA per row on the chain, and max(t, 0) is an integer
-// compare (t > 0 exactly: 0 < bits(t) <= bits(+inf)).
-ENMF_DEV double pos_part(double t) {
-  const long long b = __double_as_longlong(t);
-  return (b > 0 && b <= 0x7FF0000000000000LL) ? t : 0.0;
-}
-
-template <int RMAX>
-constexpr int cv_smem_bytes() {
-  return RMAX * (RMAX + 4) * 8 + 2 * RMAX * 8 + (RMAX / 8) * 72 * 8;
-}
-
-// MODE (timing experiments only): 0 = normal, 1 = skeleton without the row
-// chain (wrong results), 2 = no phase barriers.
-template <int RMAX, int UB, int NW, int MODE = 0>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_cv(Args a, int ntiles) {
-  constexpr int LDG = RMAX + 4;
-  constexpr int SL = RMAX / 4;
-  constexpr int NB = RMAX / 8;
-  constexpr int NTH = NW * 32;
-  static_assert(NB % UB == 0, "row blocks per group");
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;                  // skewed G, diagonal blocks: strictly upper part only
-  double* Gd = sm + RMAX * LDG;
-  double* Gi = Gd + RMAX;
-  double* GL = Gi + RMAX;           // [NB][8][9]: strictly lower part of each diagonal block
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
-    const int k = e / RMAX, c = e % RMAX;
-    const int j = (c + 8 * (k / 8)) & (RMAX - 1);
-    const double v = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
-    const bool diagblk = c < 8;      // rotated column c in [0, 8) <=> j in k's own block
-    Gs[k * LDG + c] = (diagblk && c <= (k & 7)) ? 0.0 : v;
-    if (diagblk) GL[(k >> 3) * 72 + (k & 7) * 9 + c] = (c < (k & 7)) ? v : 0.0;
-  }
-  for (int k = threadIdx.x; k < RMAX; k += NTH) {
-    const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-    Gd[k] = d;
-    Gi[k] = __ddiv_rn(1.0, d);
-  }
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double gain = 0.0;
-  int nf = 0;
-  const int sg0 = g * 4 + ((2 * t) & 3), sg1 = g * 4 + ((2 * t + 1) & 3);
-  const bool upper = t >= 2;
-  const int ss_lo = g * 4 + (t >> 1), ss_hi = g * 4 + 2 + (t >> 1);
-  const bool odd = t & 1;
-  long long prof[6] = {0, 0, 0, 0, 0, 0};   // MODE 3: dmma, bar1, scalar, bar2, tile-load, total
-  const long long tstart = (MODE == 3) ? clock64() : 0;
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long col = ((long)tile * NW + warp) * 8 + g;
-    const bool valid = col < a.N;
-    long long tl0 = 0;
-    if (MODE == 3) tl0 = clock64();
-    double hreg[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-      const int j = 4 * s + t;
-      hreg[s] = (valid && j < r) ? src[(long)j * a.ld + col] : 0.0;
-    }
-    const double* cp = a.C + col;
-    double cn0 = (valid && 2 * t < r) ? cp[(long)(2 * t) * a.ld] : 0.0;
-    double cn1 = (valid && 2 * t + 1 < r) ? cp[(long)(2 * t + 1) * a.ld] : 0.0;
-    if (MODE == 3) {
-      if (hreg[SL - 1] == 12345.678 || cn1 == 0.123) gain += 1.0;
-      prof[4] += clock64() - tl0;
-    }
-    const double* gbase = Gs + g * LDG + t;
-#pragma unroll 1
-    for (int q = 0; q < NB / UB; ++q) {
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int b = UB * q + u;
-        const int k0 = 8 * b;
-        const int ka = k0 + 2 * t;
-        const double cc0 = cn0, cc1 = cn1;
-        if (b + 1 < NB) {
-          cn0 = (valid && ka + 8 < r) ? cp[(long)(ka + 8) * a.ld] : 0.0;
-          cn1 = (valid && ka + 9 < r) ? cp[(long)(ka + 9) * a.ld] : 0.0;
-        }
-        long long tk0 = 0;
-        if (MODE == 3) tk0 = clock64();
-        // ---- DMMA phase ----
-        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-        const double* gb = gbase + k0 * LDG;
-#pragma unroll
-        for (int s = 0; s < SL; ++s) {
-          const int c = (4 * s - 8 * u + RMAX) & (RMAX - 1);
-          dmma884(acc[s & 3][0], acc[s & 3][1], hreg[s], gb[c]);
-        }
-        const double S0 = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]), __dadd_rn(acc[2][0], acc[3][0]));
-        const double S1 = __dadd_rn(__dadd_rn(acc[0][1], acc[1][1]), __dadd_rn(acc[2][1], acc[3][1]));
-        if (MODE == 3) {
-          // force completion of the products before reading the clock
-          if (S0 == 12345.678 && S1 == 0.5) gain += 1.0;
-          prof[0] += clock64() - tk0;
-        }
-        const double xa0 = __shfl_sync(0xffffffffu, hreg[2 * u], sg0);
-        const double xb0 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg0);
-        const double xa1 = __shfl_sync(0xffffffffu, hreg[2 * u], sg1);
-        const double xb1 = __shfl_sync(0xffffffffu, hreg[2 * u + 1], sg1);
-        const double x0 = upper ? xb0 : xa0, x1 = upper ? xb1 : xa1;
-        double b0 = __dsub_rn(cc0, S0);
-        double b1 = __dsub_rn(cc1, S1);
-        const double* gl0 = GL + b * 72 + (2 * t) * 9;
-        const double* gl1 = gl0 + 9;
-        const double i00 = Gi[ka], i11 = Gi[ka + 1];
-        const double l10 = gl1[2 * t];    // G[ka+1][ka]
-        long long tk1 = 0;
-        if (MODE == 3) tk1 = clock64();
-        if (MODE != 2) __syncthreads();
-        long long tk2 = 0;
-        if (MODE == 3) {
-          tk2 = clock64();
-          prof[1] += tk2 - tk1;
-        }
-        // ---- scalar phase: rows k0..k0+7 in order, row k0+i in lane t = i/2 ----
-        double t0 = 0.0, t1 = 0.0, h0 = 0.0, h1 = 0.0;
-        if (MODE == 1) {
-          t0 = __dmul_rn(b0, i00); h0 = pos_part(t0);
-          t1 = __dmul_rn(b1, i11); h1 = pos_part(t1);
-        }
-#pragma unroll
-        for (int i = 0; i < (MODE == 1 ? 0 : 8); i += 2) {
-          const double tt0 = __dmul_rn(b0, i00);
-          const double hh0 = pos_part(tt0);
-          const double tt1 = __dmul_rn(fma(-l10, hh0, b1), i11);
-          const double hh1 = pos_part(tt1);
-          if (2 * t == i) {
-            t0 = tt0; h0 = hh0; t1 = tt1; h1 = hh1;
-          }
-          if (i < 6) {
-            const double e0 = __shfl_sync(0xffffffffu, hh0, g * 4 + i / 2);
-            const double e1 = __shfl_sync(0xffffffffu, hh1, g * 4 + i / 2);
-            if (2 * t > i) {
-              b0 = fma(-gl0[i], e0, b0);
-              b1 = fma(-gl1[i], e0, b1);
-              b0 = fma(-gl0[i + 1], e1, b0);
-              b1 = fma(-gl1[i + 1], e1, b1);
-            }
-          }
-        }
-        {
-          const double g00 = Gd[ka], g11 = Gd[ka + 1];
-          const double o0 = __dsub_rn(x0, t0), n0 = __dsub_rn(h0, t0);
-          const double o1 = __dsub_rn(x1, t1), n1 = __dsub_rn(h1, t1);
-          gain = fma(g00, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-          gain = fma(g11, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-        }
-        const double y0 = __shfl_sync(0xffffffffu, h0, ss_lo);
-        const double y1 = __shfl_sync(0xffffffffu, h1, ss_lo);
-        const double z0 = __shfl_sync(0xffffffffu, h0, ss_hi);
-        const double z1 = __shfl_sync(0xffffffffu, h1, ss_hi);
-        hreg[2 * u] = odd ? y1 : y0;
-        hreg[2 * u + 1] = odd ? z1 : z0;
-        long long tk3 = 0;
-        if (MODE == 3) {
-          if (hreg[2 * u] == 12345.678) gain += 1.0;
-          tk3 = clock64();
-          prof[2] += tk3 - tk2;
-        }
-        if (MODE != 2) __syncthreads();
-        if (MODE == 3) prof[3] += clock64() - tk3;
-      }
-      if (NB / UB > 1) {
-        double tmp[2 * UB];
-#pragma unroll
-        for (int s = 0; s < 2 * UB; ++s) tmp[s] = hreg[s];
-#pragma unroll
-        for (int s = 0; s + 2 * UB < SL; ++s) hreg[s] = hreg[s + 2 * UB];
-#pragma unroll
-        for (int s = 0; s < 2 * UB; ++s) hreg[SL - 2 * UB + s] = tmp[s];
-      }
-    }
-    if (valid) {
-#pragma unroll
-      for (int s = 0; s < SL; ++s) {
-        const int j = 4 * s + t;
-        if (j < r) {
-          a.H[(long)j * a.ld + col] = hreg[s];
-          nf |= !isfinite(hreg[s]);
-        }
-      }
-    }
-  }
-  if (MODE == 3 && lane == 0 && a.terms) {
-    prof[5] = clock64() - tstart;
-    double* o = a.terms + ((long)blockIdx.x * NW + warp) * 8;
-    for (int i = 0; i < 6; ++i) o[i] = (double)prof[i];
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
-// ---- look-ahead tensor-core sweep ---------------------------------------------
-//
-// Left-looking blocked Gauss-Seidel (sweep_dmma_t layout: lane (g, t) owns rows
-// k0+2t, k0+2t+1 of column g in the block being solved) with a one-block
-// look-ahead: while block b is solved row by row (latency-bound), the warp
-// already issues the 30 DMMAs of block b+1's products with every row block
-// except b,
-//     P_{b+1} = sum_{j not in block b} G[b+1 rows][j] · h_j,
-// which do not depend on block b's solution; block b+1 then only adds the two
-// DMMAs of G[b+1 rows][block b] · H_new[b].  The solve and the next block's
-// tensor work are independent instruction streams in one basic block, so the
-// scheduler interleaves them and the sequential chain hides behind DMMA issue.
-template <int RMAX, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_la(Args a, int ntiles) {
-  constexpr int LDG = RMAX + 4;
-  constexpr int SL = RMAX / 4;
-  constexpr int NB = RMAX / 8;
-  constexpr int NTH = NW * 32;
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;
-  double* Gd = sm + RMAX * LDG;
-  double* Gi = Gd + RMAX;
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  {
-    // Gs[k][c] = G[k][(c + 8·(k/8)) mod RMAX], zero padding (see sweep_dmma_p)
-    constexpr int CH = RMAX / 2;
-    const bool vec = (r % 2 == 0) && (((uintptr_t)a.G & 15) == 0);
-    for (int e = threadIdx.x; e < RMAX * CH; e += NTH) {
-      const int k = e / CH, c = (e % CH) * 2;
-      const int j = (c + 8 * (k / 8)) & (RMAX - 1);
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(Gs + k * LDG + c);
-      if (vec) {
-        const int valid = (k < r && j < r) ? 16 : 0;
-        const double* srcp = valid ? a.G + (long)k * r + j : a.G;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(srcp), "r"(valid));
-      } else {
-        Gs[k * LDG + c] = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
-        Gs[k * LDG + c + 1] = (k < r && j + 1 < r) ? a.G[(long)k * r + j + 1] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int k = threadIdx.x; k < RMAX; k += NTH) {
-      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-      Gd[k] = d;
-      Gi[k] = __ddiv_rn(1.0, d);
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double gain = 0.0;
-  int nf = 0;
-  bool first = true;
-  const int sg0 = g * 4 + ((2 * t) & 3), sg1 = g * 4 + ((2 * t + 1) & 3);
-  const bool upper = t >= 2;
-  const int ss_lo = g * 4 + (t >> 1), ss_hi = g * 4 + 2 + (t >> 1);
-  const bool odd = t & 1;
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long col = ((long)tile * NW + warp) * 8 + g;
-    const bool valid = col < a.N;
-    double hreg[SL];
-#pragma unroll
-    for (int s = 0; s < SL; ++s) {
-      const int j = 4 * s + t;
-      hreg[s] = (valid && j < r) ? src[(long)j * a.ld + col] : 0.0;
-    }
-    const double* cp = a.C + col;
-    double cn0 = (valid && 2 * t < r) ? cp[(long)(2 * t) * a.ld] : 0.0;
-    double cn1 = (valid && 2 * t + 1 < r) ? cp[(long)(2 * t + 1) * a.ld] : 0.0;
-    if (first) {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-      __syncthreads();
-      first = false;
-    }
-    const double* gbase = Gs + g * LDG + t;
-    // P for block 0: all slots (block 0's rows are old values)
-    double pa[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-    for (int s = 0; s < SL; ++s) dmma884(pa[s & 3][0], pa[s & 3][1], hreg[s], gbase[4 * s]);
-#pragma unroll 1
-    for (int b = 0; b < NB; ++b) {
-      const int k0 = 8 * b;
-      const int ka = k0 + 2 * t;
-      const double cc0 = cn0, cc1 = cn1;
-      if (b + 1 < NB) {
-        cn0 = (valid && ka + 8 < r) ? cp[(long)(ka + 8) * a.ld] : 0.0;
-        cn1 = (valid && ka + 9 < r) ? cp[(long)(ka + 9) * a.ld] : 0.0;
-      }
-      const double* gb = gbase + k0 * LDG;
-      // complete S_b with the previous block's new rows (slots SL-2, SL-1)
-      double S0 = __dadd_rn(__dadd_rn(pa[0][0], pa[1][0]), __dadd_rn(pa[2][0], pa[3][0]));
-      double S1 = __dadd_rn(__dadd_rn(pa[0][1], pa[1][1]), __dadd_rn(pa[2][1], pa[3][1]));
-      if (b > 0) {
-        dmma884(S0, S1, hreg[SL - 2], gb[4 * (SL - 2)]);
-        dmma884(S0, S1, hreg[SL - 1], gb[4 * (SL - 1)]);
-      }
-      // look-ahead: P_{b+1} over all slots except this block's (0, 1), issued in
-      // five chunks interleaved with the solve below (in-order issue per warp)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) pa[i][0] = pa[i][1] = 0.0;
-      const bool ahead = b + 1 < NB;
-      const double* gn = gb + 8 * LDG;
-      constexpr int CHK = (SL - 2 + 4) / 5;   // DMMAs per chunk
-      auto look = [&](int chunk) {
-        if (ahead) {
-#pragma unroll
-          for (int q = 0; q < CHK; ++q) {
-            const int s = 2 + chunk * CHK + q;
-            if (s < SL) dmma884(pa[s & 3][0], pa[s & 3][1], hreg[s], gn[4 * s - 8]);
-          }
-        }
-      };
-      look(0);
-      // solve block b
-      const double xa0 = __shfl_sync(0xffffffffu, hreg[0], sg0);
-      const double xb0 = __shfl_sync(0xffffffffu, hreg[1], sg0);
-      const double xa1 = __shfl_sync(0xffffffffu, hreg[0], sg1);
-      const double xb1 = __shfl_sync(0xffffffffu, hreg[1], sg1);
-      const double x0 = upper ? xb0 : xa0, x1 = upper ? xb1 : xa1;
-      const double* gk0 = Gs + ka * LDG;
-      const double* gk1 = gk0 + LDG;
-      const double g00 = Gd[ka], g11 = Gd[ka + 1];
-      const double i00 = Gi[ka], i11 = Gi[ka + 1];
-      double b0 = fma(g00, x0, __dsub_rn(cc0, S0));
-      double b1 = fma(g11, x1, __dsub_rn(cc1, S1));
-      double h0 = x0, h1 = x1, t0 = 0.0, t1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        // branch-free: every lane computes, only the owner's values are kept
-        const bool own = 2 * t == i;
-        const double tt0 = __dmul_rn(b0, i00);
-        const double hh0 = tt0 > 0.0 ? tt0 : 0.0;
-        const double dd0 = __dsub_rn(hh0, x0);
-        const double bb1 = fma(-gk1[i], dd0, b1);
-        const double tt1 = __dmul_rn(bb1, i11);
-        const double hh1 = tt1 > 0.0 ? tt1 : 0.0;
-        const double dd1 = __dsub_rn(hh1, x1);
-        if (own) {
-          t0 = tt0; h0 = hh0; t1 = tt1; h1 = hh1;
-        }
-        look(1 + i / 2);
-        if (i < 6) {
-          const double e0 = __shfl_sync(0xffffffffu, dd0, g * 4 + i / 2);
-          const double e1 = __shfl_sync(0xffffffffu, dd1, g * 4 + i / 2);
-          if (2 * t > i) {
-            b0 = fma(-gk0[i], e0, b0);
-            b0 = fma(-gk0[i + 1], e1, b0);
-            b1 = fma(-gk1[i], e0, b1);
-            b1 = fma(-gk1[i + 1], e1, b1);
-          }
-        }
-      }
-      {
-        const double o0 = __dsub_rn(x0, t0), n0 = __dsub_rn(h0, t0);
-        const double o1 = __dsub_rn(x1, t1), n1 = __dsub_rn(h1, t1);
-        gain = fma(g00, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-        gain = fma(g11, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-      }
-      const double y0 = __shfl_sync(0xffffffffu, h0, ss_lo);
-      const double y1 = __shfl_sync(0xffffffffu, h1, ss_lo);
-      const double z0 = __shfl_sync(0xffffffffu, h0, ss_hi);
-      const double z1 = __shfl_sync(0xffffffffu, h1, ss_hi);
-      // rotate by two slots; this block's new rows go to SL-2, SL-1
-#pragma unroll
-      for (int s = 0; s + 2 < SL; ++s) hreg[s] = hreg[s + 2];
-      hreg[SL - 2] = odd ? y1 : y0;
-      hreg[SL - 1] = odd ? z1 : z0;
-    }
-    if (valid) {
-#pragma unroll
-      for (int s = 0; s < SL; ++s) {
-        const int j = 4 * s + t;
-        if (j < r) {
-          a.H[(long)j * a.ld + col] = hreg[s];
-          nf |= !isfinite(hreg[s]);
-        }
-      }
-    }
-  }
-  if (first) {
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
-// ---- right-looking tensor-core sweep ------------------------------------------
-//
-// Gauss-Seidel written right-looking.  Per column keep the residual
-//     R_k = C_k - sum_{j processed} G_kj h_new_j - sum_{j not yet processed, j != k} G_kj h_old_j
-// so that row k's update is  h_new_k = max(0, R_k / G_kk)  (nnls.hpp:116-134).
-// For a tile of 8 columns per warp (lane (g, t): column g, rows 8K+2t, 8K+2t+1
-// of every 8-row block K — 32 doubles of R in registers):
-//   1. R = C - U·H_old, U = the strictly upper part of G (block-upper tiles plus
-//      the strictly upper triangle of each diagonal 8×8 block): independent DMMA
-//      chains, one per row block.
-//   2. for each row block b: finish its 8 rows sequentially (lower triangle of
-//      the diagonal block, shuffles inside the column's lane quad), write them,
-//      then R[K'] -= G[K', b]·H_new[b] for every later block K' > b (DMMA).
-// The DMMA work equals the reference's r² per column; unlike the left-looking
-// kernels each block's products are independent of the block solve that
-// follows, so other warps' tensor work overlaps it.  -G is staged in shared
-// memory so every DMMA accumulates (D = A·B + C) straight into R.
-template <int RMAX>
-constexpr int rl_smem_bytes() {
-  return RMAX * (RMAX + 4) * 8 + 2 * RMAX * 8 + (RMAX / 8) * 64 * 8;
-}
-
-template <int RMAX, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sweep_rl(Args a, int ntiles) {
-  constexpr int LDG = RMAX + 4;
-  constexpr int NB = RMAX / 8;
-  constexpr int NTH = NW * 32;
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  double* Gn = sm;                  // -G, full (diagonal blocks: strictly upper part only, rest 0)
-  double* Gd = sm + RMAX * LDG;     // G_kk (1 on padding rows)
-  double* Gi = Gd + RMAX;           // 1 / G_kk
-  double* GL = Gi + RMAX;           // [NB][8][8] +G strictly lower part of each diagonal block
-  __shared__ double red[NTH + 33];
-
-  const int r = a.r;
-  for (int e = threadIdx.x; e < RMAX * RMAX; e += NTH) {
-    const int k = e / RMAX, j = e % RMAX;
-    const double v = (k < r && j < r) ? a.G[(long)k * r + j] : 0.0;
-    const bool same = (k >> 3) == (j >> 3);
-    Gn[k * LDG + j] = (!same || j > k) ? -v : 0.0;
-    if (same) GL[(k >> 3) * 64 + (k & 7) * 8 + (j & 7)] = (j < k) ? v : 0.0;
-  }
-  for (int k = threadIdx.x; k < RMAX; k += NTH) {
-    const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-    Gd[k] = d;
-    Gi[k] = __ddiv_rn(1.0, d);
-  }
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  const int ss_lo = g * 4 + (t >> 1), ss_hi = g * 4 + 2 + (t >> 1);
-  const bool odd = t & 1;
-  double gain = 0.0;
-  int nf = 0;
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long col = ((long)tile * NW + warp) * 8 + g;
-    const bool valid = col < a.N;
-    const double* hs = src + col;
-    double* ho = a.H + col;
-    const double* cs = a.C + col;
-    auto ld = [&](const double* p, int row) -> double {
-      return (valid && row < r) ? p[(long)row * a.ld] : 0.0;
-    };
-    // ---- phase 1: R = C - U·H_old --------------------------------------------
-    double R[NB][2];
-#pragma unroll
-    for (int K = 0; K < NB; ++K) {
-      R[K][0] = ld(cs, 8 * K + 2 * t);
-      R[K][1] = ld(cs, 8 * K + 2 * t + 1);
-    }
-#pragma unroll
-    for (int jb = 0; jb < NB; ++jb) {
-      const double a0 = ld(hs, 8 * jb + t), a1 = ld(hs, 8 * jb + 4 + t);
-      const double* gcol = Gn + g * LDG + 8 * jb + t;
-#pragma unroll
-      for (int K = 0; K <= jb; ++K) {   // K == jb: strictly upper triangle of the diagonal block
-        dmma884(R[K][0], R[K][1], a0, gcol[8 * K * LDG]);
-        dmma884(R[K][0], R[K][1], a1, gcol[8 * K * LDG + 4]);
-      }
-    }
-    // ---- phase 2: block solves + right-looking updates -------------------------
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int ka = 8 * b + 2 * t;
-      const double x0 = ld(hs, ka), x1 = ld(hs, ka + 1);
-      const double* gl0 = GL + b * 64 + (2 * t) * 8;   // row ka of the diagonal block (lower part)
-      const double* gl1 = gl0 + 8;                     // row ka+1
-      const double i0 = Gi[ka], i1 = Gi[ka + 1];
-      double b0 = R[b][0], b1 = R[b][1];
-      double h0 = 0.0, h1 = 0.0, t0 = 0.0, t1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        if (2 * t == i) {
-          t0 = __dmul_rn(b0, i0);
-          h0 = t0 > 0.0 ? t0 : 0.0;
-          b1 = fma(-gl1[i], h0, b1);
-          t1 = __dmul_rn(b1, i1);
-          h1 = t1 > 0.0 ? t1 : 0.0;
-        }
-        if (i < 6) {
-          const double e0 = __shfl_sync(0xffffffffu, h0, g * 4 + i / 2);
-          const double e1 = __shfl_sync(0xffffffffu, h1, g * 4 + i / 2);
-          if (2 * t > i) {
-            b0 = fma(-gl0[i], e0, b0);
-            b0 = fma(-gl0[i + 1], e1, b0);
-            b1 = fma(-gl1[i], e0, b1);
-            b1 = fma(-gl1[i + 1], e1, b1);
-          }
-        }
-      }
-      {
-        const double g0 = Gd[ka], g1 = Gd[ka + 1];
-        const double o0 = __dsub_rn(x0, t0), n0 = __dsub_rn(h0, t0);
-        const double o1 = __dsub_rn(x1, t1), n1 = __dsub_rn(h1, t1);
-        gain = fma(g0, __dsub_rn(__dmul_rn(o0, o0), __dmul_rn(n0, n0)), gain);
-        gain = fma(g1, __dsub_rn(__dmul_rn(o1, o1), __dmul_rn(n1, n1)), gain);
-      }
-      if (valid) {
-        if (ka < r) ho[(long)ka * a.ld] = h0;
-        if (ka + 1 < r) ho[(long)(ka + 1) * a.ld] = h1;
-        nf |= !isfinite(h0) | !isfinite(h1);
-      }
-      if (b + 1 < NB) {
-        // A fragments of H_new[b]: rows 8b+t and 8b+4+t of column g
-        const double y0 = __shfl_sync(0xffffffffu, h0, ss_lo);
-        const double y1 = __shfl_sync(0xffffffffu, h1, ss_lo);
-        const double z0 = __shfl_sync(0xffffffffu, h0, ss_hi);
-        const double z1 = __shfl_sync(0xffffffffu, h1, ss_hi);
-        const double a0 = odd ? y1 : y0, a1 = odd ? z1 : z0;
-        const double* gcol = Gn + g * LDG + 8 * b + t;
-#pragma unroll
-        for (int K = b + 1; K < NB; ++K) {
-          dmma884(R[K][0], R[K][1], a0, gcol[8 * K * LDG]);
-          dmma884(R[K][0], R[K][1], a1, gcol[8 * K * LDG + 4]);
-        }
-      }
-    }
-  }
-  const double bg = block_reduce_sum_any(gain, red);
-  nf = __syncthreads_or(nf);
-  last_block_reduce_n<NTH>(a, bg, nf, red);
-}
-
 // ---- paired-warp tensor-core sweep (default) ----------------------------------
 //
 // Every SM sub-partition runs one PAIR of warps over its own 32 columns:
