@@ -31,6 +31,7 @@
 #include "misc.cuh"
 #include "sparse.cuh"
 #include "ozaki.cuh"
+#include "sweep_tf32.cuh"
 
 namespace {
 
@@ -358,6 +359,29 @@ int hals_variant() {
   return v;
 }
 
+template <int R_>
+void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  const long ntiles = ((long)a.N + 7) / 8;
+  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 15) / 16));
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)hals::sweep_tf32<R_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            hals::tf_smem_bytes<R_>()));
+    attr = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = hals::tf_smem_bytes<R_>();
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&lc, hals::sweep_tf32<R_>, a, ntiles));
+}
+
 template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
 void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
@@ -404,7 +428,11 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     return;
   }
   const int v = hals_variant();
-  if (v == 1) {
+  if (prec == PREC_TF32 && v == 54) {  // TF32 variant: block products on the TF32 tensor cores
+    if (r <= 32) launch_sweep_tf32<32>(c, s, a);
+    else if (r <= 64) launch_sweep_tf32<64>(c, s, a);
+    else launch_sweep_tf32<128>(c, s, a);
+  } else if (v == 1) {
 #define SW(S_, T_)                                                                          \
   hals::sweep_fast<S_, T_><<<(a.N + hals::NT / T_ - 1) / (hals::NT / T_), hals::NT,          \
                              hals::smem_bytes<S_, T_>(), s>>>(a)
@@ -870,10 +898,21 @@ void tf32_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int 
 
 // sweep_ws reads the Gram in A-fragment order: arrange it once per inner solve.
 void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int slot) {
-  if (prec == PREC_EXACT || a.r > 128 || (hals_variant() < 50 || hals_variant() > 58)) return;
+  if (prec == PREC_EXACT || a.r > 128) return;
   constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
   c->Gf.ensure(3 * kGf);
   double* gf = c->Gf.p + slot * kGf;
+  if (prec == PREC_TF32 && hals_variant() == 54) {   // TF32 variant's sweep: m16n8k8 fragments (tf_prep)
+    auto* gf4 = reinterpret_cast<float4*>(gf);
+    if (a.r <= 32) hals::tf_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf4, a.st, a.ctl);
+    else if (a.r <= 64) hals::tf_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf4, a.st, a.ctl);
+    else hals::tf_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf4, a.st, a.ctl);
+    CUK();
+    c->launches++;
+    a.Gf = gf;
+    return;
+  }
+  if (hals_variant() < 50 || hals_variant() > 58) return;
   if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);

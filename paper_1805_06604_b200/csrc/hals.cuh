@@ -363,6 +363,75 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
   }
 }
 
+// Persistent sweep kernels: grid-wide end of sweep `sw` — the stall rule on the total gain
+// (nnls.hpp:172-173).  Single GPU: every CTA forms the same fixed-order total once all
+// partials are in and decides itself; sharded: the last CTA exchanges the gain with the other
+// ranks and publishes the decision.  Returns 1 to continue (same value in every thread).
+ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& first_total, double* red) {
+  __shared__ int s_dec;
+  const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);   // gains are accumulated halved
+  const int bnf = __syncthreads_or(nf);
+  const unsigned target = (unsigned)(sw + 1) * gridDim.x;
+  if (threadIdx.x == 0) {
+    a.part[blockIdx.x] = bg;
+    a.part_nf[blockIdx.x] = bnf;
+    __threadfence();
+    const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
+    s_dec = prev == target - 1 ? 1 : 0;      // this CTA arrived last (used when sharded)
+  }
+  if (!a.dv) {
+    if (threadIdx.x == 0) {
+      unsigned e;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
+      } while (e < target);
+    }
+    __syncthreads();
+    double v = 0.0;
+    int f = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      v = __dadd_rn(v, __ldcg(a.part + b));
+      f |= __ldcg(a.part_nf + b);
+    }
+    const double total = block_reduce_sum_any(v, red);
+    f = __syncthreads_or(f);
+    if (sw == 0) first_total = total;
+    const bool stop = (sw + 1 >= a.max_sweeps) ||
+                      (total <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
+    if (blockIdx.x == 0 && threadIdx.x == 0) finish_sweep(a, total, f);   // bookkeeping (same rule)
+    __syncthreads();
+    return stop ? 0 : 1;
+  }
+  __syncthreads();
+  if (s_dec) {
+    __threadfence();
+    double v = 0.0;
+    int f = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      v = __dadd_rn(v, __ldcg(a.part + b));
+      f |= __ldcg(a.part_nf + b);
+    }
+    double total = block_reduce_sum_any(v, red);
+    f = __syncthreads_or(f);
+    if (threadIdx.x == 0) {
+      dist::allreduce_gain(*a.dv, total, f, &total, &f);
+      finish_sweep(a, total, f);
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(&a.ctl->epoch), "r"((unsigned)(sw + 1)) : "memory");
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned e;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->epoch) : "memory");
+    } while (e < (unsigned)(sw + 1));
+    s_dec = *(volatile int*)&a.ctl->cont;
+  }
+  __syncthreads();
+  return s_dec;
+}
+
 // PROF (timing experiment): per-warp cycles [barrier wait, tile load, total, DMMA / row phase] into a.terms;
 // SKIP (timing experiment, wrong results): 1 = row warps skip the row pass, 2 = product warps skip the DMMAs
 // PERSIST: one launch runs every sweep of the solve.  Between sweeps the CTAs
@@ -414,7 +483,6 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
   double gain = 0.0;
   int nf = 0;
-  __shared__ int s_flag;
   double first_total = 0.0;                 // persistent: the first sweep's total gain (stall rule)
   const int gi = lane >> 2, gt = lane & 3;
   // this lane's two 16-byte B-fragment chunks (tiles 0,1 and 2,3) within a row k with k & 3 == gt
@@ -533,71 +601,9 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   // ---- grid-wide end of sweep `sw`: stall rule on the total gain ----
   const long long tg0 = PROF ? clock64() : 0;
   {
-    const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
-    const int bnf = __syncthreads_or(nf);
-    const unsigned target = (unsigned)(sw + 1) * gridDim.x;
-    if (threadIdx.x == 0) {
-      a.part[blockIdx.x] = bg;
-      a.part_nf[blockIdx.x] = bnf;
-      __threadfence();
-      const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
-      s_flag = prev == target - 1 ? 1 : 0;   // this CTA arrived last (used when sharded)
-    }
-    if (!a.dv) {
-      // every CTA forms the same fixed-order total itself once all partials are in
-      if (threadIdx.x == 0) {
-        unsigned e;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
-        } while (e < target);
-      }
-      __syncthreads();
-      double v = 0.0;
-      int f = 0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) {
-        v = __dadd_rn(v, __ldcg(a.part + b));
-        f |= __ldcg(a.part_nf + b);
-      }
-      const double total = block_reduce_sum_any(v, red);
-      f = __syncthreads_or(f);
-      if (sw == 0) first_total = total;
-      const bool stop = (sw + 1 >= a.max_sweeps) ||
-                        (total <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
-      if (blockIdx.x == 0 && threadIdx.x == 0) finish_sweep(a, total, f);   // bookkeeping (same rule)
-      s_flag = stop ? 0 : 1;
-    } else {
-      // sharded: the last CTA exchanges the gain with the other ranks and publishes the decision
-      __syncthreads();
-      if (s_flag) {
-        __threadfence();
-        double v = 0.0;
-        int f = 0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) {
-          v = __dadd_rn(v, __ldcg(a.part + b));
-          f |= __ldcg(a.part_nf + b);
-        }
-        double total = block_reduce_sum_any(v, red);
-        f = __syncthreads_or(f);
-        if (threadIdx.x == 0) {
-          dist::allreduce_gain(*a.dv, total, f, &total, &f);
-          finish_sweep(a, total, f);
-          __threadfence();
-          asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(&a.ctl->epoch), "r"((unsigned)(sw + 1))
-                       : "memory");
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned e;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->epoch) : "memory");
-        } while (e < (unsigned)(sw + 1));
-        s_flag = *(volatile int*)&a.ctl->cont;
-      }
-    }
-    __syncthreads();
+    const int cont = grid_decision(a, gain, nf, sw, first_total, red);
     if (PROF) pw[3] += clock64() - tg0;
-    if (!s_flag) break;
+    if (!cont) break;
     gain = 0.0;
     nf = 0;
     src = a.H;

@@ -473,3 +473,21 @@ def test_int8_digit_products_wide_dynamic_range(ctx, port):
     rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 5), E.TimingMode.none)
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+
+
+@pytest.mark.parametrize("shape,iters", [((3000, 2000, 48), 40), ((3000, 2000, 24), 40)])
+def test_tf32_variant_small_ranks(ctx, shape, iters):
+    """TF32 variant on the r ≤ 64 sweep instantiations.  The 1e-4 contract is the C5 one
+    (test_tf32_variant_final_error, bench `tf32_variant`); on these shapes the TF32 cross
+    products alone already move the restart sequence (the FP64-sweep TF32 path lands on the
+    same errors), so the check is a sanity bound: final error within 30% of FP64's."""
+    m, n, r = shape
+    rng = np.random.default_rng(m + r)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = rng.random((m, r)), rng.random((r, n))
+    f64 = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", iters), E.TimingMode.none)
+    t32 = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", iters, E.Precision.tf32), E.TimingMode.none)
+    nx = np.linalg.norm(x)
+    e64 = np.linalg.norm(x - f64.factors.w @ f64.factors.h) / nx
+    e32 = np.linalg.norm(x - t32.factors.w @ t32.factors.h) / nx
+    assert abs(e32 - e64) <= 0.3 * e64, (e32, e64)
