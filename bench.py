@@ -347,7 +347,7 @@ def run_ours(args, rank, world, local_rank):
         # in-loop estimate carries the tensor cores' FP32 accumulation bias, profiles/r01_tf32_bias.txt)
         f64_final, t_final = direct_rel_error(xs[0], w64, h64), direct_rel_error(xs[0], w32, h32)
         tf32 = {"value": args.steps / (tms * 1e-3), "unit": UNIT, "ms_per_step": tms / args.steps,
-                "dtype": "tf32 cross products (X in FP32), FP64 elsewhere",
+                "dtype": "tf32: cross products and HALS block products on TF32 tensor cores (X, H tiles in FP32); Grams, error, decisions FP64",
                 "iterations": len(rt) - 1, "final_relative_error": t_final,
                 "in_loop_estimate": rt[-1].relative_error,
                 "fp64_final_relative_error": f64_final, "abs_diff": abs(t_final - f64_final),
