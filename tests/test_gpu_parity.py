@@ -491,3 +491,16 @@ def test_tf32_variant_small_ranks(ctx, shape, iters):
     e64 = np.linalg.norm(x - f64.factors.w @ f64.factors.h) / nx
     e32 = np.linalg.norm(x - t32.factors.w @ t32.factors.h) / nx
     assert abs(e32 - e64) <= 0.3 * e64, (e32, e64)
+
+
+def test_eanls_large_with_int8_digit_products(ctx, port):
+    """E-ANLS (block principal pivoting, nnls.hpp:259-406) at 4096×4096 r=32, where the cross
+    products take the INT8-digit path: 3 iterations vs the oracle."""
+    m = n = 4096
+    r = 32
+    rng = np.random.default_rng(51)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, 52)
+    ref = port.run_dense(x, w0, h0, preset("e-anls-hp1", max_outer_iterations=3))
+    rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 3), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=True)
