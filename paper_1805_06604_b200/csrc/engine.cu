@@ -101,6 +101,7 @@ struct enmf_gpu_ctx {
   } xd_xt, xd_x, xd_cols, xd_rows;          // one GPU: X scaled per row (T·Xᵀ) / per column (W_yᵀX)
   DBuf<int8_t> adig;
   DBuf<int> aexp;
+  DBuf<unsigned long long> amax;
   DBuf<int> ocbuf;
   DBuf<double> opart;
   void* lt = nullptr;                     // LtCache (cuBLASLt handle, workspace, per-shape plans)
@@ -823,15 +824,18 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   c->ocbuf.ensure(std::max((size_t)acc, ((size_t)(ozaki::SMAX * (ozaki::SMAX + 1) / 2) * r + 256) *
                                             std::max(c->m, c->n)));
   if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
-  ozaki::row_exp<<<r, 256, 0, s>>>(A, K, lda, c->aexp.p, st);
-  ozaki::split<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
-      A, r, K, lda, c->aexp.p, 1, c->adig.p, st);
+  c->amax.ensure((size_t)r);
+  CU(cudaMemsetAsync(c->amax.p, 0, (size_t)r * sizeof(unsigned long long), s));
+  const unsigned kb = (unsigned)std::max<long>(1, std::min<long>((K + 2047) / 2048, 64));
+  ozaki::row_absmax<<<dim3(kb, r), 256, 0, s>>>(A, K, lda, c->amax.p, st);
+  ozaki::split_rows<<<dim3(kb, r), 256, 0, s>>>(A, r, K, lda, c->amax.p, c->aexp.p, c->adig.p, st);
   CUK();
   c->launches += 2;
   for (int q = 0; q < S; ++q)
     lt_gemm(c, s, c->adig.p, xd.d.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
-  ozaki::combine<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 32), 256, 0, s>>>(
-      c->ocbuf.p, off, S, r, N, c->aexp.p, xd.e.p, out, ldo, st);
+  const dim3 cg((unsigned)std::max<long>(1, std::min<long>((N + 255) / 256, 64)), (unsigned)r);
+  if (S == 7) ozaki::combine<7><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
+  else ozaki::combine<8><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
   CUK();
   c->launches += 1 + S;
   return true;

@@ -81,6 +81,51 @@ __global__ void row_exp(const double* __restrict__ a, long K, long lda, int* e, 
   }
 }
 
+// Per-product factor path (R ≤ a few hundred rows, K long): row maxima with many blocks per
+// row (bit patterns of non-negative doubles order like the values: atomicMax on them), then
+// the digits in a 2-D grid (row = blockIdx.y, no divisions) that also derives the exponent.
+__global__ void row_absmax(const double* __restrict__ a, long K, long lda, unsigned long long* mx,
+                           const DevState* st) {
+  if (st && !dev_active(st)) return;
+  __shared__ double sh[32];
+  const double* row = a + (long)blockIdx.y * lda;
+  double m = 0.0;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(row[k]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    atomicMax(mx + blockIdx.y, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// digits of row blockIdx.y (SMAX planes, plane stride R·K) from its maximum; block (0, i)
+// also publishes the row's exponent for the recombination
+__global__ void split_rows(const double* __restrict__ a, long R, long K, long lda,
+                           const unsigned long long* mx, int* e_out, int8_t* __restrict__ out,
+                           const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const long i = blockIdx.y;
+  const int e = exp_above(__longlong_as_double((long long)mx[i]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) e_out[i] = e;
+  const double scale = __longlong_as_double((long long)(1023 - e) << 52);   // 2^-e, exact (|e| small)
+  const double* row = a + i * lda;
+  int8_t* o = out + i * K;
+  const long dstride = R * K;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
+    double r = row[k] * scale;                      // exact, |r| < 1
+#pragma unroll
+    for (int p = 0; p < SMAX; ++p) {
+      r *= 128.0;
+      const double d = trunc(r);
+      r -= d;
+      o[p * dstride + k] = (int8_t)(int)d;
+    }
+  }
+}
+
 // e[k] for max_i |a[i][k]| of an R × K row-major matrix (thread per column, coalesced rows)
 __global__ void col_exp(const double* __restrict__ a, long R, long K, long lda, int* e) {
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
@@ -158,25 +203,26 @@ __global__ void split(const double* __restrict__ a, long R, long K, long lda, co
 struct Offsets { long q[SMAX]; };   // start of digit GEMM q's output (its rows p·R + i, p < S - q)
 
 // eb: the X digits' exponents, per output column j (X scaled per row for T·Xᵀ, per column for W_yᵀX)
-__global__ void combine(const int* __restrict__ C, Offsets off, int S, long R, long N, const int* ea,
-                        const int* eb, double* __restrict__ out, long ldo, const DevState* st) {
+template <int S>
+__global__ void combine(const int* __restrict__ C, Offsets off, long R, long N, const int* ea, const int* eb,
+                        double* __restrict__ out, long ldo, const DevState* st) {
   if (st && !dev_active(st)) return;
-  const long total = R * N;
-  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
-    const long i = idx / N, j = idx - i * N;
-    const int base = ea[i] + eb[j];
+  const long i = blockIdx.y;
+  const int ei = ea[i];
+  for (long j = (long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long)gridDim.x * blockDim.x) {
+    int v[S][S];                                     // v[q][p] = digit product (p, q), p + q < S
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+      for (int p = 0; p < S - q; ++p) v[q][p] = __ldcs(C + off.q[q] + ((long)p * R + i) * N + j);
+    const int base = ei + eb[j];
     double acc = 0.0;
 #pragma unroll
-    for (int w = SMAX - 1; w >= 0; --w) {         // w = p + q, weight 2^{-7(w+2)}
-      if (w >= S) continue;
-      double part = 0.0;                         // sum of the exact int32 terms of this weight
+    for (int w = S - 1; w >= 0; --w) {             // smallest weight 2^{-7(w+2)} first
+      long long part = 0;                            // exact: at most S terms below 2^31 each
 #pragma unroll
-      for (int q = 0; q < SMAX; ++q) {
-        const int p = w - q;
-        if (p < 0 || q >= S) continue;
-        part += (double)C[off.q[q] + (p * R + i) * N + j];   // |part| < 2^34: exact in FP64
-      }
-      acc += ldexp(part, base - 7 * (w + 2));
+      for (int q = 0; q <= w; ++q) part += v[q][w - q];
+      acc += ldexp((double)part, base - 7 * (w + 2));
     }
     out[i * ldo + j] = acc;
   }
