@@ -17,6 +17,7 @@
 #include <cublasLt.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -771,25 +772,30 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
   // along it stands in for both operands: 7 levels up to 2.5, 8 up to 16, beyond that the
   // product stays on the FP64 DMMA GEMM (levels = 0)
-  c->opart.ensure(1);
+  constexpr int kChunks = 64;
+  c->opart.ensure(1 + (by_row ? 0 : 2 * (size_t)kChunks * cols));
   CU(cudaMemsetAsync(c->opart.p, 0, sizeof(double), s));
   auto* rb = reinterpret_cast<unsigned long long*>(c->opart.p);
-  if (by_row) ozaki::row_range<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, rb);
-  else ozaki::col_range<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(x, rows, cols,
-                                                                                                     cols, rb);
+  if (by_row) {
+    ozaki::row_stats<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, xd.e.p, rb);
+  } else {
+    double* pm = c->opart.p + 1;
+    double* ps = pm + (size_t)kChunks * cols;
+    ozaki::col_stats_part<<<dim3((unsigned)((cols + 255) / 256), kChunks), 256, 0, s>>>(x, rows, cols, cols, kChunks,
+                                                                                         pm, ps);
+    ozaki::col_stats_final<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(
+        pm, ps, rows, cols, kChunks, xd.e.p, rb);
+  }
   CUK();
   double ratio = 0.0;
   CU(cudaMemcpyAsync(&ratio, c->opart.p, sizeof ratio, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   xd.levels = ratio <= 2.5 ? 7 : ratio <= 16.0 ? 8 : 0;
-  c->launches++;
-  if (by_row) ozaki::row_exp<<<(unsigned)rows, 256, 0, s>>>(x, cols, cols, xd.e.p, nullptr);
-  else ozaki::col_exp<<<(unsigned)std::min<long>((cols + 255) / 256, (long)c->sms * 8), 256, 0, s>>>(x, rows, cols,
-                                                                                                   cols, xd.e.p);
-  ozaki::split<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(
-      x, rows, cols, cols, xd.e.p, by_row ? 1 : 2, xd.d.p, nullptr);
+  c->launches += by_row ? 1 : 2;
+  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols + 255) / 256, 8)), (unsigned)rows), 256, 0,
+                    s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p);
   CUK();
-  c->launches += 2;
+  c->launches++;
   xd.by_row = by_row;
   xd.src = x;
   xd.rows = rows;
@@ -1180,6 +1186,23 @@ void close_session(enmf_gpu_ctx* c) {
   c->sess = nullptr;
 }
 
+// ENMF_TRACE_BEGIN=1: host wall time of begin()'s phases on stderr (synchronizes the stream)
+struct BeginTrace {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit BeginTrace(cudaStream_t s_) : on(std::getenv("ENMF_TRACE_BEGIN") != nullptr), s(s_) {
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto u = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[begin] %-24s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(u - t).count());
+    t = u;
+  }
+};
+
 void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, bool dev_factors,
                 const enmf_gpu_config* cfg) {
   if (!c) throw Fail{ENMF_INVALID_ARGUMENT, "null context"};
@@ -1210,8 +1233,10 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   const size_t wsz = ml * r, hsz = r * nl;
   cudaStream_t s = c->stream;
   (void)cudaGetLastError();  // drop a stale (non-sticky) error from an earlier failed call
+  BeginTrace tr(s);
   set_attrs_once();
   ensure_buffers(c, ml, nl, r);
+  tr.mark("buffers");
   if (cfg->precision == PREC_EXACT || r > 128) c->terms.ensure(std::max(wsz, hsz));
   const size_t K = cfg->max_outer_iterations;
   c->recs.ensure(K + 1);
@@ -1250,6 +1275,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   CU(cudaMemsetAsync(c->bpp_exch.p, 0, 2 * sizeof(unsigned long long), s));
   CU(cudaMemsetAsync(c->bpp_rounds.p, 0, 2 * sizeof(int), s));
   CU(cudaMemsetAsync(c->bpp_nf.p, 0, 2 * sizeof(int), s));
+  tr.mark("factors");
 
   // run state (engine.hpp:471-481)
   DevState hs;
@@ -1310,6 +1336,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   dist_allreduce(c, s, L, c->dd.p + 2, 2, st);
   misc::set_norm<<<1, 1, 0, s>>>(st, c->dd.p + 2);
   CUK();
+  tr.mark("norm");
   gram_launch(c, s, pl.prec, c->H.p, nl, (int)r, (int)nl, c->GW.p, st);
   dist_allreduce(c, s, L, c->GW.p, (int)(r * r), st);
   dist_gather(c, s, L, c->H.p, (int)r, 1, pl, st);       // H0 replica for X·H0ᵀ
@@ -1325,7 +1352,9 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
       ozaki_prepare_x(c, s, c->xd_rows, D->xr, (long)D->mp, (long)n, true);
     } else {
       ozaki_prepare_x(c, s, c->xd_x, c->x, (long)m, (long)n, false);
+      tr.mark("digits x (cols)");
       ozaki_prepare_x(c, s, c->xd_xt, c->x, (long)m, (long)n, true);
+      tr.mark("digits x (rows)");
     }
     if (!ozaki_cross(c, s, D ? L.tfull : c->H.p, (long)n, (int)r, true, c->P.p, (long)ml, st,
                      D ? c->xd_rows : c->xd_xt))
@@ -1343,6 +1372,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   misc::decide<<<1, misc::NT, 0, s>>>(st, c->dd.p, c->GWn.p, c->GW.p, (int)r, pl.prec == PREC_EXACT, c->recs.p, 1);
   CUK();
   c->launches += 2;
+  tr.mark("e0");
 
   // one outer iteration = one graph; one conditional WHILE node per HALS side
   if (K > 0) {
@@ -1370,6 +1400,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
     c->launches = before;
     CU(cudaGraphInstantiate(&se->exec, se->graph, 0));
   }
+  tr.mark("graph");
 }
 
 Session* need_session(enmf_gpu_ctx* c) {

@@ -81,6 +81,81 @@ __global__ void row_exp(const double* __restrict__ a, long K, long lda, int* e, 
   }
 }
 
+// X statistics once per load, in one pass each:
+//  * row_stats: one block per row → e[i] (the row's exponent) and the max over rows of
+//    max_k|x| / mean_k|x| (atomicMax on the positive ratio's bit pattern);
+//  * col_stats_part: a 2-D grid of (column, row chunk) → per-chunk column max / sum;
+//    col_stats_final: fixed-order chunk combine → e[k] and the ratio (deterministic).
+__global__ void row_stats(const double* __restrict__ a, long K, long lda, int* e, unsigned long long* ratio_bits) {
+  __shared__ double smax[32], ssum[32];
+  const double* row = a + (long)blockIdx.x * lda;
+  double m = 0.0, t = 0.0;
+  for (long k = threadIdx.x; k < K; k += blockDim.x) {
+    const double v = fabs(row[k]);
+    m = fmax(m, v);
+    t += v;
+  }
+  for (int o = 16; o; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  if ((threadIdx.x & 31) == 0) { smax[threadIdx.x >> 5] = m; ssum[threadIdx.x >> 5] = t; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = 0.0, tt = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { mm = fmax(mm, smax[w]); tt += ssum[w]; }
+    e[blockIdx.x] = exp_above(mm);
+    if (tt > 0.0) atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(mm * (double)K / tt));
+  }
+}
+__global__ void col_stats_part(const double* __restrict__ a, long R, long K, long lda, int chunks,
+                               double* __restrict__ pmax, double* __restrict__ psum) {
+  const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const long r0 = R * blockIdx.y / chunks, r1 = R * (blockIdx.y + 1) / chunks;
+  double m = 0.0, t = 0.0;
+  for (long i = r0; i < r1; ++i) {
+    const double v = fabs(a[i * lda + k]);
+    m = fmax(m, v);
+    t += v;
+  }
+  pmax[(long)blockIdx.y * K + k] = m;
+  psum[(long)blockIdx.y * K + k] = t;
+}
+__global__ void col_stats_final(const double* __restrict__ pmax, const double* __restrict__ psum, long R, long K,
+                                int chunks, int* e, unsigned long long* ratio_bits) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
+    double m = 0.0, t = 0.0;
+    for (int c = 0; c < chunks; ++c) {
+      m = fmax(m, pmax[(long)c * K + k]);
+      t += psum[(long)c * K + k];
+    }
+    e[k] = exp_above(m);
+    if (t > 0.0) atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(m * (double)R / t));
+  }
+}
+
+// digits of X once per load: row blockIdx.y, exponents per row (by_row) or per column
+__global__ void split_x(const double* __restrict__ a, long R, long K, long lda, const int* __restrict__ e, int by_row,
+                        int8_t* __restrict__ out) {
+  const long i = blockIdx.y;
+  const double* row = a + i * lda;
+  int8_t* o = out + i * K;
+  const long dstride = R * K;
+  const int er = by_row ? e[i] : 0;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
+    const int ex = by_row ? er : e[k];
+    double r = row[k] * __longlong_as_double((long long)(1023 - ex) << 52);   // exact, |r| < 1
+#pragma unroll
+    for (int p = 0; p < SMAX; ++p) {
+      r *= 128.0;
+      const double d = trunc(r);
+      r -= d;
+      o[p * dstride + k] = (int8_t)(int)d;
+    }
+  }
+}
+
 // Per-product factor path (R ≤ a few hundred rows, K long): row maxima with many blocks per
 // row (bit patterns of non-negative doubles order like the values: atomicMax on them), then
 // the digits in a 2-D grid (row = blockIdx.y, no divisions) that also derives the exponent.
