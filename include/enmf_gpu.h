@@ -43,7 +43,10 @@ enum {
   ENMF_NO_CONVERGENCE = 3,     /* enmf::NoConvergence             nnls.hpp:65-68, engine.hpp:290-292 */
   ENMF_DEGENERATE_COLUMN = 4,  /* enmf::DegenerateColumn          nnls.hpp:54-63 */
   ENMF_CUDA_ERROR = 5,         /* device / driver failure (no reference analogue) */
-  ENMF_CACHE_STALE = 6         /* enmf::CacheStale                engine.hpp:41-44 */
+  ENMF_CACHE_STALE = 6,        /* enmf::CacheStale                engine.hpp:41-44 */
+  ENMF_PARSE_ERROR = 7,        /* enmf::ParseError (+ line)       data.hpp:34-43 */
+  ENMF_UNSUPPORTED_FORMAT = 8, /* enmf::UnsupportedFormat         data.hpp:45-48 */
+  ENMF_IO_ERROR = 9            /* enmf::IoError                   data.hpp:50-53 */
 };
 
 /* enmf::InnerSolver (engine.hpp:56) */
@@ -116,6 +119,8 @@ enmf_gpu_beta_schedule enmf_gpu_update_beta(enmf_gpu_beta_schedule s, int error_
 int enmf_gpu_create(enmf_gpu_ctx** out, int device);
 void enmf_gpu_destroy(enmf_gpu_ctx* ctx);
 const char* enmf_gpu_last_error(void);
+/* Line of the last ENMF_PARSE_ERROR (enmf::ParseError::line(), data.hpp:39); 0 = none. */
+size_t enmf_gpu_last_error_line(void);
 /* Number of device kernels this context has launched since creation. */
 uint64_t enmf_gpu_kernel_launches(const enmf_gpu_ctx* ctx);
 
@@ -214,6 +219,43 @@ int enmf_gpu_hals_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cro
  * *rounds = max exchange rounds over the columns. */
 int enmf_gpu_active_set_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cross,
                               const double* h0, size_t r, size_t n, double* h, int32_t* rounds);
+
+
+/* ------------------------------------------------------------------------------------
+ * Data formats and generators (host side, csrc/io.cpp): the reference's enmf/data.hpp.
+ * Readers return a library-owned matrix; read its arrays, then enmf_io_matrix_free().
+ * Sparse results are CSR exactly as SparseMatrix::from_triplets builds them
+ * (matrix.hpp:168-195: rows ascending, columns ascending within a row). */
+typedef struct enmf_io_matrix enmf_io_matrix;
+
+/* read_matrix_market (data.hpp:159-240): coordinate real|integer general, 1-based. */
+int enmf_io_read_matrix_market(const char* path, enmf_io_matrix** out);
+/* read_dense_csv (data.hpp:262-295): headerless, comma separated, CRLF accepted. */
+int enmf_io_read_dense_csv(const char* path, enmf_io_matrix** out);
+void enmf_io_matrix_shape(const enmf_io_matrix* a, size_t* rows, size_t* cols, size_t* nnz, int* is_sparse);
+const uint64_t* enmf_io_matrix_offsets(const enmf_io_matrix* a);      /* rows+1, sparse only */
+const uint64_t* enmf_io_matrix_col_indices(const enmf_io_matrix* a);  /* nnz, sparse only */
+const double* enmf_io_matrix_values(const enmf_io_matrix* a);         /* nnz, or rows*cols row-major */
+void enmf_io_matrix_free(enmf_io_matrix* a);
+
+/* write_matrix_market (data.hpp:242-257) / write_dense_csv (data.hpp:297-309) /
+ * write_run_csv (data.hpp:316-326; E = relative_error - e_min). */
+int enmf_io_write_matrix_market(const char* path, const uint64_t* offsets, const uint64_t* col_idx,
+                                const double* vals, size_t rows, size_t cols);
+int enmf_io_write_dense_csv(const char* path, const double* x, size_t rows, size_t cols);
+int enmf_io_write_run_csv(const char* path, const enmf_gpu_iter* iters, size_t n, double e_min);
+/* format_double (data.hpp:101-105): shortest round-trip form; returns its length and
+ * writes at most cap-1 characters plus a terminator. */
+size_t enmf_io_format_double(double v, char* buf, size_t cap);
+
+/* Generators (data.hpp:58-97, rng.hpp:30-57): one std::mt19937_64 stream each,
+ * uniform [0,1) = (g() >> 11) * 2^-53, row-major fill. */
+uint64_t enmf_mix_seed(uint64_t base, uint64_t a, uint64_t b);
+int enmf_uniform_matrix(size_t rows, size_t cols, uint64_t seed, double* out);
+int enmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* w, double* h);
+int enmf_lowrank_factors(size_t m, size_t n, size_t r, uint64_t seed, double* w, double* h);
+int enmf_gen_lowrank(size_t m, size_t n, size_t r, uint64_t seed, double* x);   /* X = W·H */
+int enmf_gen_fullrank(size_t m, size_t n, uint64_t seed, double* x);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,9 @@ ENMF_NO_CONVERGENCE = 3
 ENMF_DEGENERATE_COLUMN = 4
 ENMF_CUDA_ERROR = 5
 ENMF_CACHE_STALE = 6
+ENMF_PARSE_ERROR = 7
+ENMF_UNSUPPORTED_FORMAT = 8
+ENMF_IO_ERROR = 9
 
 ENMF_INNER_EXACT, ENMF_INNER_HALS = 0, 1
 ENMF_TIMING_WALL, ENMF_TIMING_NONE = 0, 1
@@ -63,8 +66,21 @@ EXPORTS = [
     "enmf_gpu_active_set_solve", "enmf_gpu_begin", "enmf_gpu_step", "enmf_gpu_step_profiled",
     "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream",
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
-    "enmf_gpu_dist_finalize", "enmf_gpu_load_csr",
+    "enmf_gpu_dist_finalize", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
+    # data formats and generators (csrc/io.cpp)
+    "enmf_io_read_matrix_market", "enmf_io_read_dense_csv", "enmf_io_matrix_shape",
+    "enmf_io_matrix_offsets", "enmf_io_matrix_col_indices", "enmf_io_matrix_values",
+    "enmf_io_matrix_free", "enmf_io_write_matrix_market", "enmf_io_write_dense_csv",
+    "enmf_io_write_run_csv", "enmf_io_format_double", "enmf_mix_seed", "enmf_uniform_matrix",
+    "enmf_random_init", "enmf_lowrank_factors", "enmf_gen_lowrank", "enmf_gen_fullrank",
 ]
+
+#: entry points that do not return an ENMF_* status
+_NON_STATUS = ("enmf_gpu_config_default", "enmf_gpu_destroy", "enmf_gpu_last_error",
+               "enmf_gpu_kernel_launches", "enmf_gpu_update_beta", "enmf_gpu_stream",
+               "enmf_gpu_dist_shard", "enmf_gpu_last_error_line", "enmf_io_matrix_shape",
+               "enmf_io_matrix_offsets", "enmf_io_matrix_col_indices", "enmf_io_matrix_values",
+               "enmf_io_matrix_free", "enmf_io_format_double", "enmf_mix_seed")
 
 _lib = None
 
@@ -120,11 +136,35 @@ def load() -> C.CDLL:
     L.enmf_gpu_dist_init.argtypes = [vp, C.c_void_p]
     L.enmf_gpu_load_dense_sharded.argtypes = [vp, dp, dp, C.c_int]
     L.enmf_gpu_dist_finalize.argtypes = [vp]
+    L.enmf_gpu_last_error_line.restype = sz
+    u64p = C.POINTER(C.c_uint64)
+    L.enmf_io_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.enmf_io_read_dense_csv.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.enmf_io_matrix_shape.argtypes = [vp, szp, szp, szp, ip]
+    L.enmf_io_matrix_shape.restype = None
+    L.enmf_io_matrix_offsets.argtypes = [vp]
+    L.enmf_io_matrix_offsets.restype = u64p
+    L.enmf_io_matrix_col_indices.argtypes = [vp]
+    L.enmf_io_matrix_col_indices.restype = u64p
+    L.enmf_io_matrix_values.argtypes = [vp]
+    L.enmf_io_matrix_values.restype = C.POINTER(C.c_double)
+    L.enmf_io_matrix_free.argtypes = [vp]
+    L.enmf_io_matrix_free.restype = None
+    L.enmf_io_write_matrix_market.argtypes = [C.c_char_p, dp, dp, dp, sz, sz]
+    L.enmf_io_write_dense_csv.argtypes = [C.c_char_p, dp, sz, sz]
+    L.enmf_io_write_run_csv.argtypes = [C.c_char_p, C.POINTER(CIter), sz, C.c_double]
+    L.enmf_io_format_double.argtypes = [C.c_double, C.c_char_p, sz]
+    L.enmf_io_format_double.restype = sz
+    L.enmf_mix_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+    L.enmf_mix_seed.restype = C.c_uint64
+    L.enmf_uniform_matrix.argtypes = [sz, sz, C.c_uint64, dp]
+    L.enmf_random_init.argtypes = [sz, sz, sz, C.c_uint64, dp, dp]
+    L.enmf_lowrank_factors.argtypes = [sz, sz, sz, C.c_uint64, dp, dp]
+    L.enmf_gen_lowrank.argtypes = [sz, sz, sz, C.c_uint64, dp]
+    L.enmf_gen_fullrank.argtypes = [sz, sz, C.c_uint64, dp]
     for name in EXPORTS:
         fn = getattr(L, name)
-        if name not in ("enmf_gpu_config_default", "enmf_gpu_destroy", "enmf_gpu_last_error",
-                        "enmf_gpu_kernel_launches", "enmf_gpu_update_beta", "enmf_gpu_stream",
-                        "enmf_gpu_dist_shard"):
+        if name not in _NON_STATUS:
             fn.restype = C.c_int
     _lib = L
     return L

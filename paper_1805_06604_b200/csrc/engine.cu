@@ -1581,6 +1581,10 @@ void* enmf_gpu_stream(enmf_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; 
 
 }  // extern "C"
 
+namespace enmf_host {
+void set_last_error(const std::string& msg) { g_last_error = msg; }   // io.cpp's errors
+}
+
 #include "dist_api.inc"
 #include "cabi.inc"
 #include "kernels_api.inc"

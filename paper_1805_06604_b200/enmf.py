@@ -54,6 +54,22 @@ class DeviceError(RuntimeError):
     """CUDA failure (no reference analogue)."""
 
 
+class ParseError(RuntimeError):
+    """enmf::ParseError (data.hpp:34-43); `line` is 0 when the error has no line."""
+
+    def __init__(self, what: str, line: int = 0):
+        super().__init__(what)
+        self.line = line
+
+
+class UnsupportedFormat(RuntimeError):
+    """enmf::UnsupportedFormat (data.hpp:45-48)"""
+
+
+class IoError(RuntimeError):
+    """enmf::IoError (data.hpp:50-53)"""
+
+
 _ERRORS = {
     L.ENMF_INVALID_ARGUMENT: InvalidArgument,
     L.ENMF_NON_FINITE: NonFiniteIterate,
@@ -61,12 +77,17 @@ _ERRORS = {
     L.ENMF_DEGENERATE_COLUMN: DegenerateColumn,
     L.ENMF_CUDA_ERROR: DeviceError,
     L.ENMF_CACHE_STALE: CacheStale,
+    L.ENMF_UNSUPPORTED_FORMAT: UnsupportedFormat,
+    L.ENMF_IO_ERROR: IoError,
 }
 
 
 def _check(rc: int) -> None:
     if rc != L.ENMF_OK:
-        msg = L.load().enmf_gpu_last_error().decode()
+        lib = L.load()
+        msg = lib.enmf_gpu_last_error().decode()
+        if rc == L.ENMF_PARSE_ERROR:
+            raise ParseError(msg, int(lib.enmf_gpu_last_error_line()))
         raise _ERRORS.get(rc, RuntimeError)(msg)
 
 

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "enmf_gpu.h")).read()
-    return sorted(set(re.findall(r"\b(enmf_gpu_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(enmf_(?:gpu|io|mix|uniform|random|lowrank|gen)_?\w*)\s*\(", src)))
 
 
 def test_library_exports_header():
