@@ -46,7 +46,8 @@ enum {
   ENMF_CACHE_STALE = 6,        /* enmf::CacheStale                engine.hpp:41-44 */
   ENMF_PARSE_ERROR = 7,        /* enmf::ParseError (+ line)       data.hpp:34-43 */
   ENMF_UNSUPPORTED_FORMAT = 8, /* enmf::UnsupportedFormat         data.hpp:45-48 */
-  ENMF_IO_ERROR = 9            /* enmf::IoError                   data.hpp:50-53 */
+  ENMF_IO_ERROR = 9,           /* enmf::IoError                   data.hpp:50-53 */
+  ENMF_ZERO_DIRECTION = 10     /* enmf::ZeroDirection             engine.hpp:46-49 */
 };
 
 /* enmf::InnerSolver (engine.hpp:56) */
@@ -220,6 +221,16 @@ int enmf_gpu_hals_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cro
 int enmf_gpu_active_set_solve(enmf_gpu_ctx* ctx, const double* gram, const double* cross,
                               const double* h0, size_t r, size_t n, double* h, int32_t* rounds);
 
+
+/* optimal_beta_linesearch (engine.hpp:522-540), the diagnostic the reference's tests use:
+ *   beta* = <X − W_n·H_y, (W_n − W)·H_y> / ||(W_n − W)·H_y||²
+ * with W_n, W m×r and H_y r×n row-major host arrays; X dense (m×n) or CSR.  Returns
+ * ENMF_ZERO_DIRECTION when ||(W_n − W)·H_y||² ≤ 1e-30·||X||² (ZeroDirection). */
+int enmf_gpu_optimal_beta_linesearch(enmf_gpu_ctx* ctx, const double* x, size_t m, size_t n, const double* w_n,
+                                     const double* w, const double* h_y, size_t r, double* beta);
+int enmf_gpu_optimal_beta_linesearch_csr(enmf_gpu_ctx* ctx, const uint64_t* offsets, const uint64_t* col_idx,
+                                         const double* vals, size_t m, size_t n, size_t nnz, const double* w_n,
+                                         const double* w, const double* h_y, size_t r, double* beta);
 
 /* ------------------------------------------------------------------------------------
  * Data formats and generators (host side, csrc/io.cpp): the reference's enmf/data.hpp.

@@ -60,6 +60,7 @@ int guard(F&& f) {
   } catch (const enmf::NoConvergence& e) { g_err = e.what(); return ENMF_NO_CONVERGENCE;
   } catch (const enmf::DegenerateColumn& e) { g_err = e.what(); return ENMF_DEGENERATE_COLUMN;
   } catch (const enmf::CacheStale& e) { g_err = e.what(); return ENMF_CACHE_STALE;
+  } catch (const enmf::ZeroDirection& e) { g_err = e.what(); return ENMF_ZERO_DIRECTION;
   } catch (const std::invalid_argument& e) { g_err = e.what(); return ENMF_INVALID_ARGUMENT;
   } catch (const std::exception& e) { g_err = e.what(); return ENMF_INVALID_ARGUMENT; }
 }
@@ -212,4 +213,17 @@ int ref_config_preset(const char* name, enmf_gpu_config* c) {
   return ENMF_INVALID_ARGUMENT;
 }
 
+int ref_optimal_beta_linesearch(const double* x, size_t m, size_t n, const double* wn, const double* w,
+                                const double* h, size_t r, double* beta) {
+  return guard([&] { *beta = enmf::optimal_beta_linesearch(dm(x, m, n), dm(wn, m, r), dm(w, m, r), dm(h, r, n)); });
+}
+int ref_optimal_beta_linesearch_csr(const uint64_t* off, const uint64_t* cidx, const double* vals, size_t m, size_t n,
+                                    const double* wn, const double* w, const double* h, size_t r, double* beta) {
+  return guard([&] {
+    const size_t nnz = off[m];
+    enmf::SparseMatrix x(m, n, std::vector<std::size_t>(off, off + m + 1), std::vector<std::size_t>(cidx, cidx + nnz),
+                         std::vector<double>(vals, vals + nnz));
+    *beta = enmf::optimal_beta_linesearch(x, dm(wn, m, r), dm(w, m, r), dm(h, r, n));
+  });
+}
 }  // extern "C"

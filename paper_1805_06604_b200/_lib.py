@@ -22,6 +22,7 @@ ENMF_CACHE_STALE = 6
 ENMF_PARSE_ERROR = 7
 ENMF_UNSUPPORTED_FORMAT = 8
 ENMF_IO_ERROR = 9
+ENMF_ZERO_DIRECTION = 10
 
 ENMF_INNER_EXACT, ENMF_INNER_HALS = 0, 1
 ENMF_TIMING_WALL, ENMF_TIMING_NONE = 0, 1
@@ -67,6 +68,7 @@ EXPORTS = [
     "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream",
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
     "enmf_gpu_dist_finalize", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
+    "enmf_gpu_optimal_beta_linesearch", "enmf_gpu_optimal_beta_linesearch_csr",
     # data formats and generators (csrc/io.cpp)
     "enmf_io_read_matrix_market", "enmf_io_read_dense_csv", "enmf_io_matrix_shape",
     "enmf_io_matrix_offsets", "enmf_io_matrix_col_indices", "enmf_io_matrix_values",
@@ -137,6 +139,9 @@ def load() -> C.CDLL:
     L.enmf_gpu_load_dense_sharded.argtypes = [vp, dp, dp, C.c_int]
     L.enmf_gpu_dist_finalize.argtypes = [vp]
     L.enmf_gpu_last_error_line.restype = sz
+    L.enmf_gpu_optimal_beta_linesearch.argtypes = [vp, dp, sz, sz, dp, dp, dp, sz, C.POINTER(C.c_double)]
+    L.enmf_gpu_optimal_beta_linesearch_csr.argtypes = [vp, dp, dp, dp, sz, sz, sz, dp, dp, dp, sz,
+                                                       C.POINTER(C.c_double)]
     u64p = C.POINTER(C.c_uint64)
     L.enmf_io_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(vp)]
     L.enmf_io_read_dense_csv.argtypes = [C.c_char_p, C.POINTER(vp)]

@@ -128,6 +128,7 @@ struct enmf_gpu_ctx {
   // standalone kernel API
   int kernel_precision = ENMF_PRECISION_FP64;
   DBuf<double> ka, kb, kc, kd, ke;
+  DBuf<double> ls_part, ls_val;   // optimal_beta_linesearch scratch (never captured in a graph)
   DBuf<HalsCtl> kctl;
 };
 

@@ -173,6 +173,83 @@ __global__ void __launch_bounds__(NT) dd_final(const double* part_hi, const doub
   }
 }
 
+// optimal_beta_linesearch (engine.hpp:522-540) terms.  Element (i,j) of DH = (W_n − W)·H_y
+// and WH = W_n·H_y is formed exactly as the reference's multiply forms it (linalg.hpp:174-189:
+// diff rounded first, products added in ascending p from 0.0, no contraction), then
+// accumulated in double-double: q=0 Σ DH², q=1 Σ WH·DH, q=2 Σ X·DH (dense X only).
+// Element e = i·n + j with j fastest, so H_y rows are read coalesced.  part: 6 per block.
+__global__ void __launch_bounds__(NT) linesearch_terms(const double* __restrict__ x, const double* __restrict__ wn,
+                                                       const double* __restrict__ w, const double* __restrict__ h,
+                                                       long m, long n, int r, double* __restrict__ part) {
+  __shared__ double sh[NT], sl[NT];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (long e = blockIdx.x * (long)NT + threadIdx.x; e < m * n; e += (long)gridDim.x * NT) {
+    const long i = e / n, j = e - i * n;
+    const double* a = wn + i * r;
+    const double* b = w + i * r;
+    double dh = 0.0, wh = 0.0;
+    for (int p = 0; p < r; ++p) {
+      const double hp = h[(long)p * n + j];
+      dh = __dadd_rn(dh, __dmul_rn(__dsub_rn(a[p], b[p]), hp));
+      wh = __dadd_rn(wh, __dmul_rn(a[p], hp));
+    }
+    dd_add_prod(acc[0], acc[1], dh, dh);
+    dd_add_prod(acc[2], acc[3], wh, dh);
+    if (x) dd_add_prod(acc[4], acc[5], x[e], dh);
+  }
+  for (int q = 0; q < 3; ++q) {
+    double hi = acc[2 * q], lo = acc[2 * q + 1];
+    block_reduce_dd<NT>(hi, lo, sh, sl);
+    if (threadIdx.x == 0) {
+      part[6 * blockIdx.x + 2 * q] = hi;
+      part[6 * blockIdx.x + 2 * q + 1] = lo;
+    }
+    __syncthreads();
+  }
+}
+
+// Σ X·DH over the stored entries of a CSR X (frob_inner(SparseMatrix, DenseMatrix),
+// linalg.hpp:192-205), one thread per row; part[2·block .. +1] = (hi, lo).
+__global__ void __launch_bounds__(NT) linesearch_xdh_csr(const unsigned long long* __restrict__ off,
+                                                         const unsigned long long* __restrict__ idx,
+                                                         const double* __restrict__ val, const double* __restrict__ wn,
+                                                         const double* __restrict__ w, const double* __restrict__ h,
+                                                         long m, long n, int r, double* __restrict__ part) {
+  __shared__ double sh[NT], sl[NT];
+  double hi = 0.0, lo = 0.0;
+  for (long i = blockIdx.x * (long)NT + threadIdx.x; i < m; i += (long)gridDim.x * NT) {
+    const double* a = wn + i * r;
+    const double* b = w + i * r;
+    for (unsigned long long q = off[i]; q < off[i + 1]; ++q) {
+      const long j = (long)idx[q];
+      double dh = 0.0;
+      for (int p = 0; p < r; ++p) dh = __dadd_rn(dh, __dmul_rn(__dsub_rn(a[p], b[p]), h[(long)p * n + j]));
+      dd_add_prod(hi, lo, val[q], dh);
+    }
+  }
+  block_reduce_dd<NT>(hi, lo, sh, sl);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = hi;
+    part[2 * blockIdx.x + 1] = lo;
+  }
+}
+
+// Fixed-order combination of `streams` interleaved (hi, lo) partial streams:
+// part[(b·streams + q)·2 + {0,1}] → out[2q], out[2q+1].  One block.
+__global__ void __launch_bounds__(NT) dd_final_multi(const double* part, int nparts, int streams, double* out) {
+  __shared__ double sh[NT], sl[NT];
+  for (int q = 0; q < streams; ++q) {
+    double hi = 0.0, lo = 0.0;
+    for (int b = threadIdx.x; b < nparts; b += NT) dd_add(hi, lo, part[(b * streams + q) * 2], part[(b * streams + q) * 2 + 1]);
+    block_reduce_dd<NT>(hi, lo, sh, sl);
+    if (threadIdx.x == 0) {
+      out[2 * q] = hi;
+      out[2 * q + 1] = lo;
+    }
+    __syncthreads();
+  }
+}
+
 // Reference-order Neumaier sum of x[i]^2 or a[i]*b[i] (frob_norm_sq, frob_inner), one thread.
 // For the fast_error cross term: a = W_nᵀ (r×m), b = P (r×m) visited in W_n's
 // row-major order (i outer, k inner), term = -2*w*x.

@@ -54,6 +54,10 @@ class DeviceError(RuntimeError):
     """CUDA failure (no reference analogue)."""
 
 
+class ZeroDirection(RuntimeError):
+    """enmf::ZeroDirection (engine.hpp:46-49)"""
+
+
 class ParseError(RuntimeError):
     """enmf::ParseError (data.hpp:34-43); `line` is 0 when the error has no line."""
 
@@ -79,6 +83,7 @@ _ERRORS = {
     L.ENMF_CACHE_STALE: CacheStale,
     L.ENMF_UNSUPPORTED_FORMAT: UnsupportedFormat,
     L.ENMF_IO_ERROR: IoError,
+    L.ENMF_ZERO_DIRECTION: ZeroDirection,
 }
 
 
@@ -433,6 +438,31 @@ class Context:
                                              float(stall_fraction), _p(h), C.byref(sw)))
         return h, sw.value
 
+    def optimal_beta_linesearch(self, x, w_n, w, h_y) -> float:
+        """enmf::optimal_beta_linesearch (engine.hpp:522-540); x dense or a data.SparseMatrix."""
+        w_n, w, h_y = _f64(w_n, "w_n"), _f64(w, "w"), _f64(h_y, "h_y")
+        m, r = w_n.shape
+        n = h_y.shape[1]
+        if w.shape != (m, r) or h_y.shape[0] != r:
+            raise InvalidArgument("optimal_beta_linesearch: shape mismatch")
+        beta = C.c_double(0)
+        if hasattr(x, "offsets"):
+            if (x.rows, x.cols) != (m, n):
+                raise InvalidArgument("optimal_beta_linesearch: shape mismatch")
+            off = np.ascontiguousarray(x.offsets, dtype=np.uint64)
+            idx = np.ascontiguousarray(x.col_indices, dtype=np.uint64)
+            val = _f64(x.values, "vals")
+            _check(self._lib.enmf_gpu_optimal_beta_linesearch_csr(self._h, off.ctypes.data, idx.ctypes.data,
+                                                                  val.ctypes.data, m, n, val.size, _p(w_n), _p(w),
+                                                                  _p(h_y), r, C.byref(beta)))
+        else:
+            x = _f64(x, "x")
+            if x.shape != (m, n):
+                raise InvalidArgument("optimal_beta_linesearch: shape mismatch")
+            _check(self._lib.enmf_gpu_optimal_beta_linesearch(self._h, _p(x), m, n, _p(w_n), _p(w), _p(h_y), r,
+                                                              C.byref(beta)))
+        return beta.value
+
     def active_set_solve(self, gram, cross, h0):
         gram, cross, h0 = _f64(gram, "gram"), _f64(cross, "cross"), _f64(h0, "h0")
         r, n = h0.shape
@@ -524,6 +554,10 @@ def fast_error(norm_x_sq, w, xht, hht):
 
 def hals_solve(gram_, cross, h0, max_sweeps, stall_fraction=0.01):
     return default_context().hals_solve(gram_, cross, h0, max_sweeps, stall_fraction)
+
+
+def optimal_beta_linesearch(x, w_n, w, h_y):
+    return default_context().optimal_beta_linesearch(x, w_n, w, h_y)
 
 
 def active_set_solve(gram_, cross, h0):

@@ -179,6 +179,46 @@ def stock_nlohmann_layout(text: str) -> str:
     return re.sub(r"^( *)(\"[^\"]*\": )\[(-?\d+(?:,-?\d+)*)\]", expand, text, flags=re.M)
 
 
+def linesearch_cases():
+    """Inputs for optimal_beta_linesearch (engine.hpp:522-540), after test_engine.cpp:493-539:
+    random small cases, a zero-residual case, a larger one, a CSR X and a zero direction."""
+    rng = np.random.default_rng(127)
+    cases = []
+    for k in range(10):
+        m, n, r = 10, 9, 3
+        cases.append(("small%d" % k, rng.random((m, n)), rng.random((m, r)), rng.random((m, r)), rng.random((r, n))))
+    wn, w, h = rng.random((9, 3)), rng.random((9, 3)), rng.random((3, 8))
+    cases.append(("zero_residual", wn @ h, wn, w, h))
+    cases.append(("large", rng.random((300, 257)), rng.random((300, 17)), rng.random((300, 17)),
+                  rng.random((17, 257))))
+    xs = rng.random((200, 150))
+    xs[rng.random(xs.shape) > 0.05] = 0.0
+    cases.append(("csr", xs, rng.random((200, 6)), rng.random((200, 6)), rng.random((6, 150))))
+    wn = rng.random((8, 2))
+    cases.append(("zero_direction", rng.random((8, 7)), wn, wn.copy(), rng.random((2, 7))))
+    return cases
+
+
+def linesearch_golden():
+    R = C.CDLL(REF_SO)
+    sz, dp = C.c_size_t, C.c_void_p
+    R.ref_optimal_beta_linesearch.argtypes = [dp, sz, sz, dp, dp, dp, sz, C.POINTER(C.c_double)]
+    R.ref_optimal_beta_linesearch_csr.argtypes = [dp, dp, dp, sz, sz, dp, dp, dp, sz, C.POINTER(C.c_double)]
+    out = {}
+    for name, x, wn, w, h in linesearch_cases():
+        b = C.c_double(0)
+        m, n, r = x.shape[0], x.shape[1], wn.shape[1]
+        args = [wn.ctypes.data, w.ctypes.data, h.ctypes.data, r, C.byref(b)]
+        if name == "csr":
+            off, idx, val = csr_of(x)
+            rc = R.ref_optimal_beta_linesearch_csr(off.ctypes.data, idx.ctypes.data, val.ctypes.data, m, n, *args)
+        else:
+            rc = R.ref_optimal_beta_linesearch(x.ctypes.data, m, n, *args)
+        out[name] = (rc, b.value)
+    np.savez_compressed(os.path.join(OUT, "linesearch.npz"), names=np.array(list(out)),
+                        rc=np.array([v[0] for v in out.values()]), beta=np.array([v[1] for v in out.values()]))
+
+
 def main():
     L = lib()
     R = C.CDLL(REF_SO)
@@ -245,6 +285,8 @@ def main():
         shutil.rmtree(tmp)
     with open(os.path.join(OUT, "io.json"), "w") as f:
         json.dump(g, f, indent=0, sort_keys=True)
+
+    linesearch_golden()
 
     sdir = os.path.join(OUT, "suite")
     shutil.rmtree(sdir, ignore_errors=True)

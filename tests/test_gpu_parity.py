@@ -10,6 +10,8 @@ Bars (BASELINE.json north_star), FP64:
 The bitwise-faithful mode (Precision.fp64_exact) must reproduce the reference
 bit for bit.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -504,3 +506,32 @@ def test_eanls_large_with_int8_digit_products(ctx, port):
     ref = port.run_dense(x, w0, h0, preset("e-anls-hp1", max_outer_iterations=3))
     rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 3), E.TimingMode.none)
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=True)
+
+
+@pytest.mark.gpu
+def test_optimal_beta_linesearch_matches_reference():
+    """engine.hpp:522-540 on the device (dense and CSR X) against the reference's own values
+    (tests/golden/linesearch.npz): the DH / WH elements are formed in the reference's
+    multiply order, the three sums in double-double, so β* agrees to ~1e-15 relative;
+    the zero-residual case to 1e-12 absolute (test_engine.cpp:531-539) and a vanishing
+    direction raises ZeroDirection (test_engine.cpp:522-529)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_golden_io import linesearch_cases
+    from paper_1805_06604_b200.data import SparseMatrix
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "linesearch.npz"))
+    want = {str(k): (int(rc), float(b)) for k, rc, b in zip(g["names"], g["rc"], g["beta"])}
+    ctx = E.Context()
+    for name, x, wn, w, h in linesearch_cases():
+        rc, beta = want[name]
+        xa = SparseMatrix.from_dense(x) if name == "csr" else x
+        if rc == 10:
+            with pytest.raises(E.ZeroDirection):
+                ctx.optimal_beta_linesearch(xa, wn, w, h)
+            continue
+        got = ctx.optimal_beta_linesearch(xa, wn, w, h)
+        if name == "zero_residual":
+            assert abs(got) <= 1e-12 and abs(got - beta) <= 1e-12
+        else:
+            assert abs(got - beta) <= 1e-13 * abs(beta), (name, got, beta)
+    ctx.close()
