@@ -198,6 +198,9 @@ void set_attrs_once() {
   big((const void*)hals::sweep_ws<32, false, 0, true>, hals::ws_smem_bytes<32>());
   big((const void*)hals::sweep_ws<64, false, 0, true>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128, false, 0, true>, hals::ws_smem_bytes<128>());
+  big((const void*)hals::sweep_t2<32>, hals::t2_smem_bytes<32>());
+  big((const void*)hals::sweep_t2<64>, hals::t2_smem_bytes<64>());
+  big((const void*)hals::sweep_t2<128>, hals::t2_smem_bytes<128>());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -357,7 +360,8 @@ int hals_variant() {
     const char* e = std::getenv("ENMF_HALS_KERNEL");
     const std::string s = e ? e : "";
     v = s == "fma" ? 1 : s == "ws" ? 50 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53
-      : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58 : 54;
+      : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58
+      : s == "t2" ? 60 : s == "t2skip1" ? 61 : s == "t2skip2" ? 62 : s == "t2skip3" ? 63 : s == "t2prof" ? 64 : 54;
   }
   return v;
 }
@@ -415,10 +419,39 @@ void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   hals::sweep_ws<R_, PROF, SKIP><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 
+// Two-team persistent sweep (row passes on a DMMA-free sub-partition): one cooperative
+// launch per inner solve, one CTA per SM.
+template <int R_, int SKIP = 0, bool PROF = false>
+void launch_sweep_t2(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  const long ntiles = ((long)a.N + 7) / 8;
+  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 23) / 24));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = hals::t2_smem_bytes<R_>();
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (SKIP || PROF) {
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute((const void*)hals::sweep_t2<R_, SKIP, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              hals::t2_smem_bytes<R_>()));
+      attr = true;
+    }
+  }
+  CU(cudaLaunchKernelEx(&lc, hals::sweep_t2<R_, SKIP, PROF>, a, ntiles));
+}
+
 bool hals_use_fma() { return hals_variant() == 1; }
 
 // The persistent sweep kernel runs a whole inner solve in one launch.
-bool hals_persistent(int prec, int r) { return prec != PREC_EXACT && r <= 128 && hals_variant() == 54; }
+bool hals_persistent(int prec, int r) {
+  return prec != PREC_EXACT && r <= 128 && (hals_variant() == 54 || (hals_variant() >= 60 && hals_variant() <= 64));
+}
 
 void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   const int r = a.r;
@@ -444,6 +477,18 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     else if (r <= 64) SW(32, 2);
     else SW(32, 4);
 #undef SW
+  } else if (v == 60) {                 // two-team persistent sweep
+    if (r <= 32) launch_sweep_t2<32>(c, s, a);
+    else if (r <= 64) launch_sweep_t2<64>(c, s, a);
+    else launch_sweep_t2<128>(c, s, a);
+  } else if (v == 61) {                 // timing experiments: t2 without row passes / DMMAs / both
+    launch_sweep_t2<128, 1>(c, s, a);
+  } else if (v == 62) {
+    launch_sweep_t2<128, 2>(c, s, a);
+  } else if (v == 63) {
+    launch_sweep_t2<128, 3>(c, s, a);
+  } else if (v == 64) {
+    launch_sweep_t2<128, 0, true>(c, s, a);
   } else if (v == 50) {                 // one launch per sweep
     if (r <= 32) launch_sweep_ws<32>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64>(c, s, a);
@@ -923,7 +968,16 @@ void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int sl
     a.Gf = gf;
     return;
   }
-  if (hals_variant() < 50 || hals_variant() > 58) return;
+  if (hals_variant() < 50 || hals_variant() > 64) return;
+  if (hals_variant() >= 60) {                        // sweep_t2: fragments without the tail split
+    if (a.r <= 32) hals::ws_prep<32, false><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+    else if (a.r <= 64) hals::ws_prep<64, false><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+    else hals::ws_prep<128, false><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+    CUK();
+    c->launches++;
+    a.Gf = gf;
+    return;
+  }
   if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
