@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libenmf_gpu.so")
+LIB_PATH = os.environ.get("ENMF_GPU_LIB") or os.path.join(HERE, "libenmf_gpu.so")   # override: A/B timing of builds
 
 ENMF_OK = 0
 ENMF_INVALID_ARGUMENT = 1

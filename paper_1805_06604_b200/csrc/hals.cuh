@@ -474,7 +474,8 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
       int l = 1;
       while (l * (l + 1) / 2 <= j) ++l;
       const int i = j - l * (l - 1) / 2, k = 8 * b + l, c = 8 * b + i;
-      v = (k < r && c < r) ? a.G[(long)k * r + c] : 0.0;
+      // scaled by the row's inverse diagonal: the row pass carries t = b / G_kk directly
+      v = (k < r && c < r) ? __dmul_rn(a.G[(long)k * r + c], __ddiv_rn(1.0, a.G[(long)k * r + k])) : 0.0;
     } else if (j < 44) {
       const int k = 8 * b + ((j - 28) & 7);
       const double d = k < r ? a.G[(long)k * r + k] : 1.0;
@@ -575,21 +576,22 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
         double x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          bb[i] = __dsub_rn(bb[i], Ss[i * WS_SLD + lane]);
+          // t = (C - S)/G_kk for all 8 rows up front; the chain then needs no multiply:
+          // h_i = max(t_i, 0), t_l -= (G_li/G_ll) h_i
+          bb[i] = __dmul_rn(__dsub_rn(bb[i], Ss[i * WS_SLD + lane]), gc[36 + i]);
           x[i] = hrow[i * 32 + hoff[i & 3]];
         }
         double hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int i = 0; i < ((SKIP & 1) ? 0 : 8); ++i) {
-          const double t = __dmul_rn(bb[i], gc[36 + i]);
-          const double h = pos_part_ws(t);
+          const double h = pos_part_ws(bb[i]);
           hv[i] = h;
 #pragma unroll
           for (int l = i + 1; l < 8; ++l) bb[l] = fma(-gc[l * (l - 1) / 2 + i], h, bb[l]);
           hrow[i * 32 + hoff[i & 3]] = h;
-          // G_kk((x-t)² - (h-t)²) = (x-h)(G_kk(x+h) - 2b_k), accumulated halved
+          // G_kk((x-t)² - (h-t)²) = (x-h)·(G_kk/2)·(x+h-2t)·2, accumulated halved
           const double u = __dsub_rn(x[i], h), v = __dadd_rn(x[i], h);
-          gain = fma(u, fma(gc[28 + i], v, -bb[i]), gain);
+          gain = fma(__dmul_rn(u, gc[28 + i]), fma(-2.0, bb[i], v), gain);
         }
         if (b + 1 < NB) nb_arrive(idH);
         if (PROF) pw[2] += clock64() - c1;
