@@ -318,6 +318,10 @@ def run_ours(args, rank, world, local_rank):
     sweeps_w = [r.inner_w_count for r in timed]
     # dominant kernel: FP64 DMMA GEMM, timed per phase with CUDA events on the engine stream
     phases = [ctx.step_profiled() for _ in range(prof_steps)]
+    try:
+        levels = tuple(ctx.digit_levels)   # INT8-digit levels S per product (0 = FP64 DMMA GEMM)
+    except Exception:
+        levels = (0, 0)
     recs = ctx.sync()
     w64 = torch.empty(wi_s.shape, dtype=torch.float64, device=dev)
     h64 = torch.empty(hi_s.shape, dtype=torch.float64, device=dev)
@@ -364,6 +368,7 @@ def run_ours(args, rank, world, local_rank):
     sweep_flops = 2.0 * R * R * (nh * ph["sweeps_h"] + mw * ph["sweeps_w"])
     achieved = sweep_flops / (sweep_ms * 1e-3) / 1e12
     cross_ms = statistics.mean([(p["cross_wx"] + p["cross_xht"]) / 2 for p in phases])
+    digit_gemms = statistics.mean([lv * (lv + 1) / 2 for lv in levels])
     cross_flops = 2.0 * R * M * N / world
     iter_ms = ms / args.steps
     flops_alg = 4.0 * M * N * R + 2.0 * (M + N) * R * R
@@ -439,10 +444,14 @@ def run_ours(args, rank, world, local_rank):
                              "frac": achieved / FP64_PEAK_TFLOPS, "traffic": args.traffic,
                              "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
                              "cross_products": {
-                                 "kernel": "FP64-accurate W_yᵀX / X·Tᵀ: 7-digit INT8 splitting, 7 int8 digit "
-                                           "GEMMs (cuBLASLt) + FP64 recombination (ozaki.cuh)",
+                                 "kernel": "FP64-accurate W_yᵀX / X·Tᵀ: X and the factor cut into S 8-bit "
+                                           "digit planes, S int8 digit GEMMs (cuBLASLt) over S(S+1)/2 digit "
+                                           "pairs, exact rank-one offset corrections, truncation-bias "
+                                           "estimate, FP64 recombination (ozaki.cuh)",
+                                 "digit_levels": list(levels), "digit_products": digit_gemms,
                                  "ms": cross_ms, "fp64_equiv_tflops": cross_flops / (cross_ms * 1e-3) / 1e12,
-                                 "int8_tops": 28 * cross_flops / (cross_ms * 1e-3) / 1e12,
+                                 "int8_tops": (digit_gemms * cross_flops / (cross_ms * 1e-3) / 1e12
+                                               if digit_gemms else None),
                                  "int8_peak_tops": INT8_PEAK_TOPS, "int8_peak_source": INT8_PEAK_SRC},
                              "iteration": {"flops_alg": flops_alg, "t_roof_ms": t_roof_ms,
                                            "frac": t_roof_ms / iter_ms,

@@ -175,6 +175,10 @@ int enmf_gpu_sync(enmf_gpu_ctx* ctx, enmf_gpu_iter* iters, size_t iters_cap, siz
 int enmf_gpu_end(enmf_gpu_ctx* ctx, double* w_out, double* h_out, double* norm_x);
 /* The context's CUDA stream (cudaStream_t) — for event timing by the caller. */
 void* enmf_gpu_stream(enmf_gpu_ctx* ctx);
+/* Digit levels S of the INT8-digit cross products for the loaded X (S(S+1)/2 int8 digit
+ * GEMMs per product; 0 = that product runs on the FP64 DMMA GEMM or X is not loaded):
+ * levels[0] for W_yᵀX, levels[1] for X·Tᵀ.  Reporting only (bench roofline). */
+int enmf_gpu_digit_levels(const enmf_gpu_ctx* ctx, int32_t* levels);
 
 /* ---- multi-GPU: one problem sharded over `world` GPUs ----------
  * One process per GPU.  Rank p owns rows [row0, row0+mp) of W and X (row block,

@@ -65,7 +65,7 @@ EXPORTS = [
     "enmf_gpu_solve", "enmf_gpu_set_precision", "enmf_gpu_gram", "enmf_gpu_cross_wx",
     "enmf_gpu_cross_xht", "enmf_gpu_frob_norm_sq", "enmf_gpu_fast_error", "enmf_gpu_hals_solve",
     "enmf_gpu_active_set_solve", "enmf_gpu_begin", "enmf_gpu_step", "enmf_gpu_step_profiled",
-    "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream",
+    "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream", "enmf_gpu_digit_levels",
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
     "enmf_gpu_dist_finalize", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
     "enmf_gpu_optimal_beta_linesearch", "enmf_gpu_optimal_beta_linesearch_csr",

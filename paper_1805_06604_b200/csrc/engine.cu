@@ -95,13 +95,14 @@ struct enmf_gpu_ctx {
   struct XDig {                            // digits of one X operand (full X, or a rank's block)
     DBuf<int8_t> d;
     DBuf<int> e;
+    DBuf<int> sums;                        // digit sums along the contracted index, SMAX × N
     const double* src = nullptr;
     long rows = 0, cols = 0;
     bool ready = false, by_row = false;
-    int levels = 7;                        // digit levels used (ozaki::combine's S)
+    int levels = 6;                        // digit levels used (ozaki::combine's S)
   } xd_xt, xd_x, xd_cols, xd_rows;          // one GPU: X scaled per row (T·Xᵀ) / per column (W_yᵀX)
   DBuf<int8_t> adig;
-  DBuf<int> aexp;
+  DBuf<int> aexp, asum;
   DBuf<unsigned long long> amax;
   DBuf<int> ocbuf;
   DBuf<double> opart;
@@ -816,7 +817,7 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   xd.e.ensure((size_t)(by_row ? rows : cols));
   // digit levels: the neglected terms of level S scale with K·max|a|·max|b| / |sum a·b|; the
   // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
-  // along it stands in for both operands: 7 levels up to 2.5, 8 up to 16, beyond that the
+  // along it stands in for both operands: 6 levels up to 2.5, 7 up to 16, beyond that the
   // product stays on the FP64 DMMA GEMM (levels = 0)
   constexpr int kChunks = 64;
   c->opart.ensure(1 + (by_row ? 0 : 2 * (size_t)kChunks * cols));
@@ -836,12 +837,21 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   double ratio = 0.0;
   CU(cudaMemcpyAsync(&ratio, c->opart.p, sizeof ratio, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  xd.levels = ratio <= 2.5 ? 7 : ratio <= 16.0 ? 8 : 0;
+  xd.levels = ratio <= 2.5 ? 6 : ratio <= 16.0 ? 7 : 0;
   c->launches += by_row ? 1 : 2;
+  const long nsum = by_row ? rows : cols;
+  xd.sums.ensure((size_t)ozaki::SMAX * nsum);
+  CU(cudaMemsetAsync(xd.sums.p, 0, (size_t)ozaki::SMAX * nsum * sizeof(int), s));
   ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols + 255) / 256, 8)), (unsigned)rows), 256, 0,
-                    s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p);
+                    s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p, xd.sums.p);
   CUK();
   c->launches++;
+  if (!by_row) {                           // column sums of the digit planes (W_yᵀX contracts X's rows)
+    ozaki::digit_colsums<<<dim3((unsigned)((cols + 255) / 256), kChunks), 256, 0, s>>>(xd.d.p, rows, cols, kChunks,
+                                                                                       xd.sums.p);
+    CUK();
+    c->launches++;
+  }
   xd.by_row = by_row;
   xd.src = x;
   xd.rows = rows;
@@ -860,6 +870,7 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   if (S == 0) return false;
   c->adig.ensure((size_t)ozaki::SMAX * r * K);
   c->aexp.ensure((size_t)r);
+  c->asum.ensure((size_t)ozaki::SMAX * r);
   // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
   // are slow below 256 rows with an N-contiguous B, so short stacks are padded with further
   // (unused) digits there
@@ -878,16 +889,19 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
   c->amax.ensure((size_t)r);
   CU(cudaMemsetAsync(c->amax.p, 0, (size_t)r * sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(c->asum.p, 0, (size_t)ozaki::SMAX * r * sizeof(int), s));
   const unsigned kb = (unsigned)std::max<long>(1, std::min<long>((K + 2047) / 2048, 64));
   ozaki::row_absmax<<<dim3(kb, r), 256, 0, s>>>(A, K, lda, c->amax.p, st);
-  ozaki::split_rows<<<dim3(kb, r), 256, 0, s>>>(A, r, K, lda, c->amax.p, c->aexp.p, c->adig.p, st);
+  ozaki::split_rows<<<dim3(kb, r), 256, 0, s>>>(A, r, K, lda, c->amax.p, c->aexp.p, c->adig.p, c->asum.p, st);
   CUK();
   c->launches += 2;
   for (int q = 0; q < S; ++q)
     lt_gemm(c, s, c->adig.p, xd.d.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
   const dim3 cg((unsigned)std::max<long>(1, std::min<long>((N + 255) / 256, 64)), (unsigned)r);
-  if (S == 7) ozaki::combine<7><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
-  else ozaki::combine<8><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, c->aexp.p, xd.e.p, out, ldo, st);
+  if (S == 6)
+    ozaki::combine<6><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
+  else
+    ozaki::combine<7><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
   CUK();
   c->launches += 1 + S;
   return true;
@@ -1633,6 +1647,18 @@ int enmf_gpu_end(enmf_gpu_ctx* c, double* w_out, double* h_out, double* norm_x) 
 }
 
 void* enmf_gpu_stream(enmf_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int enmf_gpu_digit_levels(const enmf_gpu_ctx* c, int32_t* levels) {
+  return guard([&] {
+    if (!c || !levels) throw Fail{ENMF_INVALID_ARGUMENT, "digit_levels: bad arguments"};
+    const bool d = c->dist != nullptr;
+    const auto& wx = d ? c->xd_cols : c->xd_x;
+    const auto& xt = d ? c->xd_rows : c->xd_xt;
+    levels[0] = wx.ready ? wx.levels : 0;
+    levels[1] = xt.ready ? xt.levels : 0;
+    return ENMF_OK;
+  });
+}
 
 }  // extern "C"
 

@@ -389,6 +389,14 @@ class Context:
         """cudaStream_t of this context (for torch.cuda.ExternalStream)."""
         return int(self._lib.enmf_gpu_stream(self._h) or 0)
 
+    @property
+    def digit_levels(self) -> tuple:
+        """(W_yᵀX, X·Tᵀ) digit levels S of the INT8-digit cross products for the loaded X
+        (S(S+1)/2 int8 GEMMs per product; 0 = FP64 DMMA GEMM or no X loaded)."""
+        lv = (C.c_int32 * 2)()
+        _check(self._lib.enmf_gpu_digit_levels(self._h, lv))
+        return (lv[0], lv[1])
+
     # -- kernels --------------------------------------------------------------
     def gram(self, a) -> np.ndarray:
         a = _f64(a, "a")

@@ -12,6 +12,6 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_ws -s 2 -c 1 -o gpurun_out/prof_sweep $CMD > gpurun_out/ncu_sweep.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cutlass|gemm|Kernel" -s 20 -c 3 -o gpurun_out/prof_i8 $CMD > gpurun_out/ncu_i8.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"i256x256x32gemm_s8" -s 6 -c 6 -o gpurun_out/prof_i8 $CMD > gpurun_out/ncu_i8.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_i8.log
 fi
