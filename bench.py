@@ -45,6 +45,9 @@ METRIC = "E-A-HALS outer iters/sec + % roofline, 32768² r=128, 1/2/4/8 B200"
 UNIT = "outer_iters/s"
 FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.txt)
 FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry)"
+# DRAM bytes per HALS sweep inside sweep_ws: ncu --set full of one 24-sweep launch,
+# dram__bytes_read.sum + dram__bytes_write.sum = 72.60 + 9.72 MB (profiles/r01_sweep_ncu.txt)
+SWEEP_DRAM_BYTES = (72.602368e6 + 9.718272e6) / 24
 INT8_PEAK_TOPS = 3216.0      # best cuBLASLt int8 GEMM measured on this pool's B200 (profiles/r01_int8_probe.txt)
 INT8_PEAK_SRC = "measured cuBLASLt int8 GEMM, M=1024 K=N=32768 (profiles/r01_int8_probe.txt); nominal dense 4500"
 
@@ -441,7 +444,10 @@ def run_ours(args, rank, world, local_rank):
                              "kernel": "hals::sweep_ws (persistent FP64 DMMA HALS sweeps, one launch per "
                                        "inner solve; 2·r²·N flop per sweep)",
                              "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": args.traffic,
+                             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": (args.traffic if args.traffic is not None else SWEEP_DRAM_BYTES * (ph["sweeps_h"] + ph["sweeps_w"]) / 2),
+                             "traffic_note": "DRAM bytes per launch (one inner solve), from the ncu --set full capture's "
+                                             "bytes per sweep (profiles/r01_sweep_ncu.txt); H and C stay L2-resident, "
+                                             "so it is far below the 2·r·N·8 B per sweep the iterate and C occupy",
                              "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
                              "cross_products": {
                                  "kernel": "FP64-accurate W_yᵀX / X·Tᵀ: X and the factor cut into S 8-bit "
