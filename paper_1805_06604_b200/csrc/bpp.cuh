@@ -41,8 +41,9 @@ struct Args {
 
 template <int RM, int WPB>
 constexpr int smem_bytes() {
-  // G (RM×RM) + per warp: L (RM×RM), cff row cache not needed, x/d/res (3×RM), fidx (RM ints)
-  return RM * RM * 8 + WPB * (RM * RM * 8 + 3 * RM * 8 + RM * 4);
+  // G (RM×(RM+1), odd row stride) + per warp: L (RM×(RM+1): the odd row stride keeps the
+  // lane-per-row loads of the factorization off one bank), x/d/res (3×RM), fidx (RM ints)
+  return RM * (RM + 1) * 8 + WPB * (RM * (RM + 1) * 8 + 3 * RM * 8 + RM * 4);
 }
 
 ENMF_DEV unsigned long long warp_or64(unsigned long long v) {
@@ -58,17 +59,19 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
   const int r = a.r;
   double* Gs = sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* L = sm + RM * RM + warp * (RM * RM + 3 * RM);
-  double* xf = L + RM * RM;
+  constexpr int LDL = RM + 1;             // row stride of L (bank spread for lane-per-row access)
+  double* L = sm + RM * LDL + warp * (RM * LDL + 3 * RM);
+  double* xf = L + RM * LDL;
   double* df = xf + RM;
   double* rs = df + RM;
-  int* fidx = reinterpret_cast<int*>(sm + RM * RM + WPB * (RM * RM + 3 * RM)) + warp * RM;
+  int* fidx = reinterpret_cast<int*>(sm + RM * LDL + WPB * (RM * LDL + 3 * RM)) + warp * RM;
 
-  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[e] = a.G[e];
+  const int gld = r | 1;                   // odd row stride of the Gram copy (bank spread)
+  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
   __syncthreads();
 
   double maxd = 0.0;
-  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * r + i]) ? Gs[i * r + i] : maxd;
+  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * gld + i]) ? Gs[i * gld + i] : maxd;
   const double pivot_floor = __dmul_rn(1e-12, maxd);
   const double feas_tol = __dmul_rn(1e-12, __dadd_rn(1.0, *a.cmax));
   const unsigned long long limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
@@ -98,12 +101,12 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
           double ljj = 0.0;
           int ok = 1;
           if (lane == 0) {
-            double d = Gs[fidx[j] * r + fidx[j]];
-            for (int p = 0; p < j; ++p) d = __dsub_rn(d, __dmul_rn(L[j * RM + p], L[j * RM + p]));
+            double d = Gs[fidx[j] * gld + fidx[j]];
+            for (int p = 0; p < j; ++p) d = __dsub_rn(d, __dmul_rn(L[j * LDL + p], L[j * LDL + p]));
             ok = (d > pivot_floor) ? 1 : 0;
             if (ok) {
               ljj = __dsqrt_rn(d);
-              L[j * RM + j] = ljj;
+              L[j * LDL + j] = ljj;
             }
           }
           ok = __shfl_sync(0xffffffffu, ok, 0);
@@ -111,9 +114,9 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
           ljj = __shfl_sync(0xffffffffu, ljj, 0);
           __syncwarp();
           for (int i = j + 1 + lane; i < f; i += 32) {
-            double s = Gs[fidx[i] * r + fidx[j]];
-            for (int p = 0; p < j; ++p) s = __dsub_rn(s, __dmul_rn(L[i * RM + p], L[j * RM + p]));
-            L[i * RM + j] = __ddiv_rn(s, ljj);
+            double s = Gs[fidx[i] * gld + fidx[j]];
+            for (int p = 0; p < j; ++p) s = __dsub_rn(s, __dmul_rn(L[i * LDL + p], L[j * LDL + p]));
+            L[i * LDL + j] = __ddiv_rn(s, ljj);
           }
           __syncwarp();
         }
@@ -136,13 +139,13 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
         if (lane == 0) {
           for (int i = 0; i < f; ++i) {
             double s = b[i];
-            for (int p = 0; p < i; ++p) s = __dsub_rn(s, __dmul_rn(L[i * RM + p], b[p]));
-            b[i] = __ddiv_rn(s, L[i * RM + i]);
+            for (int p = 0; p < i; ++p) s = __dsub_rn(s, __dmul_rn(L[i * LDL + p], b[p]));
+            b[i] = __ddiv_rn(s, L[i * LDL + i]);
           }
           for (int ii = f - 1; ii >= 0; --ii) {
             double s = b[ii];
-            for (int p = ii + 1; p < f; ++p) s = __dsub_rn(s, __dmul_rn(L[p * RM + ii], b[p]));
-            b[ii] = __ddiv_rn(s, L[ii * RM + ii]);
+            for (int p = ii + 1; p < f; ++p) s = __dsub_rn(s, __dmul_rn(L[p * LDL + ii], b[p]));
+            b[ii] = __ddiv_rn(s, L[ii * LDL + ii]);
           }
         }
         __syncwarp();
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
         chol_solve(xf);
         for (int q = lane; q < f; q += 32) {
           double s = df[q];
-          for (int b2 = 0; b2 < f; ++b2) s = __dsub_rn(s, __dmul_rn(Gs[fidx[q] * r + fidx[b2]], xf[b2]));
+          for (int b2 = 0; b2 < f; ++b2) s = __dsub_rn(s, __dmul_rn(Gs[fidx[q] * gld + fidx[b2]], xf[b2]));
           rs[q] = s;
         }
         __syncwarp();
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
       for (int i = lane; i < r; i += 32) {
         if (((P | B) >> i) & 1ULL) continue;
         double y = -a.C[(long)i * a.ld + col];
-        for (int q = 0; q < f; ++q) y = __dadd_rn(y, __dmul_rn(Gs[i * r + fidx[q]], xf[q]));
+        for (int q = 0; q < f; ++q) y = __dadd_rn(y, __dmul_rn(Gs[i * gld + fidx[q]], xf[q]));
         if (y < -feas_tol) I |= 1ULL << i;
       }
       I = warp_or64(I);
@@ -194,6 +197,175 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
       const double v = xf[q] > 0.0 ? xf[q] : 0.0;
       a.H[(long)fidx[q] * a.ld + col] = v;
       nf |= !isfinite(v);
+    }
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) {
+      if (exch) atomicAdd(a.exchanges, exch);
+      atomicMax(a.rounds, solves);
+      if (nf) atomicOr(a.nonfinite, 1);
+    }
+    __syncwarp();
+  }
+}
+
+
+// ---- lane-parallel solver (FP64 product mode, r <= 32) -------------------------------
+//
+// Same block-principal-pivoting control flow as `solve` (passive-set exchanges, pivot
+// drop/ban, one refinement step, full / backup(3) / largest-index rules, nnls.hpp:259-406),
+// but the arithmetic is spread over the warp instead of following the reference's sequential
+// order: lane q owns row q of the passive set; the Cholesky factor of G[F,F] is formed
+// right-looking (per pivot: one broadcast, a lane-parallel scale and a lane-parallel trailing
+// update), the triangular solves are lane-parallel column sweeps with the pivot reciprocals
+// precomputed, FMA throughout.  The dependent chain per round shrinks from O(f²) serial
+// FP64 ops on lane 0 to O(f); the result is the same NNLS solution up to rounding (the
+// bitwise-faithful `solve` stays the kernel of `fp64_exact` and of the kernel-level API).
+template <int WPB>
+constexpr int fast_smem_bytes() {
+  // G (32×33) + per warp: L (32×33), x (32), 1/diag (32), fidx (32 ints)
+  return 32 * 33 * 8 + WPB * (32 * 33 * 8 + 2 * 32 * 8 + 32 * 4);
+}
+
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
+  if (a.st && !dev_active(a.st)) return;
+  constexpr int LDL = 33;
+  extern __shared__ __align__(16) double sm[];
+  const int r = a.r;
+  double* Gs = sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* L = sm + 32 * LDL + warp * (32 * LDL + 64);
+  double* xs = L + 32 * LDL;
+  double* invd = xs + 32;
+  int* fidx = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + warp * 32;
+
+  const int gld = r | 1;
+  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
+  __syncthreads();
+
+  double maxd = 0.0;
+  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * gld + i]) ? Gs[i * gld + i] : maxd;
+  const double pivot_floor = __dmul_rn(1e-12, maxd);
+  const double feas_tol = __dmul_rn(1e-12, __dadd_rn(1.0, *a.cmax));
+  const unsigned long long limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
+
+  // lane-parallel triangular solves with the factor in L: b (lane q's entry) -> A⁻¹ b
+  auto chol_solve = [&](double b, int f) -> double {
+    for (int i = 0; i < f; ++i) {                 // forward: L y = b
+      const double yi = __shfl_sync(0xffffffffu, b, i) * invd[i];
+      if (lane == i) b = yi;
+      else if (lane > i && lane < f) b = fma(-L[lane * LDL + i], yi, b);
+    }
+    for (int i = f - 1; i >= 0; --i) {            // backward: Lᵀ x = y
+      const double xi = __shfl_sync(0xffffffffu, b, i) * invd[i];
+      if (lane == i) b = xi;
+      else if (lane < i) b = fma(-L[i * LDL + lane], xi, b);
+    }
+    return b;
+  };
+
+  for (int col = blockIdx.x * WPB + warp; col < a.N; col += gridDim.x * WPB) {
+    unsigned long long P = 0, B = 0;
+    if (lane < r && a.H0[(long)lane * a.ld + col] > 0.0) P = 1ULL << lane;
+    P = warp_or64(P);
+    int best_inf = 0x7fffffff, backup = 3, solves = 0;
+    unsigned long long exch = 0;
+    int f = 0, fq = 0;
+    double x = 0.0;                               // lane q: x_F[q]
+    for (;;) {
+      ++solves;
+      // passive index list (ascending) from the mask
+      const unsigned pm = (unsigned)P;
+      if (lane < r && ((pm >> lane) & 1u)) fidx[__popc(pm & ((1u << lane) - 1u))] = lane;
+      f = __popc(pm);
+      __syncwarp();
+      // factor G[F,F] right-looking, dropping and banning variables whose pivot collapses
+      for (;;) {
+        if (f == 0) break;
+        fq = lane < f ? fidx[lane] : 0;
+        if (lane < f)
+          for (int k = 0; k <= lane; ++k) L[lane * LDL + k] = Gs[fq * gld + fidx[k]];
+        __syncwarp();
+        int bad = f;
+        for (int j = 0; j < f; ++j) {
+          const double d = L[j * LDL + j];
+          if (!(d > pivot_floor)) { bad = j; break; }
+          const double ljj = sqrt(d), inv = 1.0 / ljj;
+          double lqj = 0.0;
+          if (lane > j && lane < f) {
+            lqj = L[lane * LDL + j] * inv;
+            L[lane * LDL + j] = lqj;
+          }
+          if (lane == j) {
+            L[j * LDL + j] = ljj;
+            invd[j] = inv;
+          }
+          __syncwarp();
+          if (lane > j && lane < f)
+            for (int k = j + 1; k <= lane; ++k) L[lane * LDL + k] = fma(-lqj, L[k * LDL + j], L[lane * LDL + k]);
+          __syncwarp();
+        }
+        if (bad == f) break;
+        if (lane == 0) {
+          const int var = fidx[bad];
+          P &= ~(1ULL << var);
+          B |= 1ULL << var;
+          for (int q = bad; q + 1 < f; ++q) fidx[q] = fidx[q + 1];
+        }
+        P = __shfl_sync(0xffffffffu, P, 0);
+        B = __shfl_sync(0xffffffffu, B, 0);
+        --f;
+        __syncwarp();
+      }
+      fq = lane < f ? fidx[lane] : 0;
+      // x_F = chol_solve(C[F,col]) + one refinement step
+      x = 0.0;
+      if (f > 0) {
+        const double df = lane < f ? a.C[(long)fq * a.ld + col] : 0.0;
+        x = chol_solve(df, f);
+        xs[lane] = x;
+        __syncwarp();
+        double rs = df;
+        if (lane < f)
+          for (int b2 = 0; b2 < f; ++b2) rs = fma(-Gs[fq * gld + fidx[b2]], xs[b2], rs);
+        rs = chol_solve(rs, f);
+        x += rs;
+        __syncwarp();
+        xs[lane] = x;
+        __syncwarp();
+      }
+      // infeasible set
+      unsigned long long I = 0;
+      if (lane < f && x < -feas_tol) I = 1ULL << fq;
+      if (lane < r && !(((P | B) >> lane) & 1ULL)) {
+        double y = -a.C[(long)lane * a.ld + col];
+        for (int q = 0; q < f; ++q) y = fma(Gs[lane * gld + fidx[q]], xs[q], y);
+        if (y < -feas_tol) I |= 1ULL << lane;
+      }
+      I = warp_or64(I);
+      if (I == 0) break;
+      if (++exch > limit) break;
+      const int count = __popcll(I);
+      if (count < best_inf) {
+        best_inf = count;
+        backup = 3;
+        P ^= I;
+      } else if (backup > 0) {
+        --backup;
+        P ^= I;
+      } else {
+        P ^= 1ULL << (63 - __clzll(I));
+      }
+      __syncwarp();
+    }
+    // write the column: max(x, 0) on F, zero elsewhere
+    int nf = 0;
+    if (lane < r) a.H[(long)lane * a.ld + col] = 0.0;
+    __syncwarp();
+    if (lane < f) {
+      const double v = x > 0.0 ? x : 0.0;
+      a.H[(long)fq * a.ld + col] = v;
+      nf = !isfinite(v);
     }
     nf = __any_sync(0xffffffffu, nf);
     if (lane == 0) {

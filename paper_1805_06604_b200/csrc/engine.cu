@@ -207,6 +207,7 @@ void set_attrs_once() {
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
   big((const void*)hals::sweep_fast<32, 4>, hals::smem_bytes<32, 4>());
   big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
+  big((const void*)bpp::solve_fast<8>, bpp::fast_smem_bytes<8>());
   big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
   done = true;
 }
@@ -518,12 +519,21 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
 }
 
 // dv/dscratch/Ntotal: multi-GPU (global max|C|, exchange count and NaN flag across ranks).
+// fast: the lane-parallel solver (FP64 product mode, r <= 32); otherwise the bitwise-faithful one
+// (fp64_exact, r > 32, and the kernel-level enmf_gpu_active_set_solve).  ENMF_BPP=exact forces the
+// latter everywhere.
 void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a, const dist::View* dv = nullptr,
-                double* dscratch = nullptr, long Ntotal = 0) {
+                double* dscratch = nullptr, long Ntotal = 0, bool fast = false) {
   const int r = a.r;
+  static const bool force_exact = [] {
+    const char* e = std::getenv("ENMF_BPP");
+    return e && std::string(e) == "exact";
+  }();
   bpp::absmax<<<1, 256, 0, s>>>(a.C, a.ld, r, a.N, const_cast<double*>(a.cmax), a.st, dv);
   CUK();
-  if (r <= 32) {
+  if (fast && !force_exact && r <= 32) {
+    bpp::solve_fast<8><<<(a.N + 7) / 8, 256, bpp::fast_smem_bytes<8>(), s>>>(a);
+  } else if (r <= 32) {
     bpp::solve<32, 8><<<(a.N + 7) / 8, 256, bpp::smem_bytes<32, 8>(), s>>>(a);
   } else {
     bpp::solve<64, 4><<<(a.N + 3) / 4, 128, bpp::smem_bytes<64, 4>(), s>>>(a);
@@ -1057,8 +1067,9 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     a.G = G; a.C = Cm; a.H0 = Hin; a.H = Hout; a.ld = rows_n; a.r = pl.r; a.N = rows_n;
     a.cmax = c->cmax.p + side; a.st = st; a.side = side;
     a.exchanges = c->bpp_exch.p + side; a.rounds = c->bpp_rounds.p + side; a.nonfinite = c->bpp_nf.p + side;
-    if (D) bpp_launch(c, s, a, D->dview, D->scratch, rows_total);
-    else bpp_launch(c, s, a);
+    const bool fast = pl.prec != PREC_EXACT;
+    if (D) bpp_launch(c, s, a, D->dview, D->scratch, rows_total, fast);
+    else bpp_launch(c, s, a, nullptr, nullptr, 0, fast);
   }
 }
 
