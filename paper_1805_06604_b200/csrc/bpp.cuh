@@ -222,8 +222,9 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
 // bitwise-faithful `solve` stays the kernel of `fp64_exact` and of the kernel-level API).
 template <int WPB>
 constexpr int fast_smem_bytes() {
-  // G (32×33) + per warp: L (32×33), x (32), 1/diag (32), fidx (32 ints)
-  return 32 * 33 * 8 + WPB * (32 * 33 * 8 + 2 * 32 * 8 + 32 * 4);
+  // G (32×33) + per warp: L (32×33), x (32), 1/diag (32), fidx (32 ints); + the lower-triangle
+  // index table (528 packed (u, v) pairs) shared by the block
+  return 32 * 33 * 8 + WPB * (32 * 33 * 8 + 2 * 32 * 8 + 32 * 4) + 528 * 4;
 }
 
 template <int WPB>
@@ -238,9 +239,12 @@ __global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
   double* xs = L + 32 * LDL;
   double* invd = xs + 32;
   int* fidx = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + warp * 32;
+  int* tri = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + WPB * 32;
 
   const int gld = r | 1;
   for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
+  for (int u = warp; u < 32; u += WPB)           // tri[u(u+1)/2 + v] = (u, v), v <= u
+    for (int v = lane; v <= u; v += 32) tri[u * (u + 1) / 2 + v] = (u << 8) | v;
   __syncthreads();
 
   double maxd = 0.0;
@@ -301,8 +305,14 @@ __global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
             invd[j] = inv;
           }
           __syncwarp();
-          if (lane > j && lane < f)
-            for (int k = j + 1; k <= lane; ++k) L[lane * LDL + k] = fma(-lqj, L[k * LDL + j], L[lane * LDL + k]);
+          // trailing update L[i][k] -= L[i][j]·L[k][j] (j < k <= i < f), the triangle's entries
+          // dealt round-robin over the lanes (balanced, instead of one row per lane)
+          const int nt = f - j - 1;
+          for (int e = lane; e < nt * (nt + 1) / 2; e += 32) {
+            const int uv = tri[e], i = j + 1 + (uv >> 8), k = j + 1 + (uv & 255);
+            L[i * LDL + k] = fma(-L[i * LDL + j], L[k * LDL + j], L[i * LDL + k]);
+          }
+          (void)lqj;
           __syncwarp();
         }
         if (bad == f) break;
