@@ -408,6 +408,24 @@ def test_int8_digit_cross_products_parity(ctx, port):
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
     assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+    assert ctx.digit_levels == (6, 6)          # both products on 6 levels of 8-bit digits
+
+
+def test_int8_digit_products_seven_levels(ctx, port):
+    """X with rows and columns scaled over one decade: max/mean along both contracted indices
+    between 2.5 and 16, so both products take 7 digit levels (28 digit GEMMs); vs the oracle."""
+    m = n = 4096
+    r = 32
+    rng = np.random.default_rng(61)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    x *= 10.0 ** rng.uniform(-0.5, 0.5, (m, 1))
+    x *= 10.0 ** rng.uniform(-0.5, 0.5, (1, n))
+    w0, h0 = port.random_init(m, n, r, 62)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=5))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 5), E.TimingMode.none)
+    assert ctx.digit_levels == (7, 7), ctx.digit_levels
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
 
 
 def test_tf32_variant_final_error(ctx):
