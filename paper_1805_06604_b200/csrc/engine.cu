@@ -852,13 +852,13 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   const long nsum = by_row ? rows : cols;
   xd.sums.ensure((size_t)ozaki::SMAX * nsum);
   CU(cudaMemsetAsync(xd.sums.p, 0, (size_t)ozaki::SMAX * nsum * sizeof(int), s));
-  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols + 255) / 256, 8)), (unsigned)rows), 256, 0,
-                    s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p, xd.sums.p);
+  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols / 8 + 255) / 256, 8)), (unsigned)rows), 256,
+                    0, s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p, xd.sums.p);
   CUK();
   c->launches++;
   if (!by_row) {                           // column sums of the digit planes (W_yᵀX contracts X's rows)
-    ozaki::digit_colsums<<<dim3((unsigned)((cols + 255) / 256), kChunks), 256, 0, s>>>(xd.d.p, rows, cols, kChunks,
-                                                                                       xd.sums.p);
+    ozaki::digit_colsums<<<dim3((unsigned)((cols / 4 + 255) / 256), kChunks), 256, 0, s>>>(xd.d.p, rows, cols,
+                                                                                           kChunks, xd.sums.p);
     CUK();
     c->launches++;
   }

@@ -74,52 +74,6 @@ ENMF_DEV int exp_above(double mx) {
   return e;
 }
 
-__global__ void absmax_partial(const double* __restrict__ x, long cnt, double* part) {
-  __shared__ double sh[32];
-  double m = 0.0;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long)gridDim.x * blockDim.x)
-    m = fmax(m, fabs(x[i]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    m = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) part[blockIdx.x] = m;
-  }
-}
-
-__global__ void absmax_final(const double* part, int nb, int* e_out) {
-  double m = 0.0;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmax(m, part[i]);
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ double sh[32];
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
-    m = fmax(m, sh[0]);
-    *e_out = exp_above(m);
-  }
-}
-
-// one block per row of an R × K row-major matrix: e[i] for max_k |a[i][k]|
-__global__ void row_exp(const double* __restrict__ a, long K, long lda, int* e, const DevState* st) {
-  if (st && !dev_active(st)) return;
-  __shared__ double sh[32];
-  const double* row = a + (long)blockIdx.x * lda;
-  double m = 0.0;
-  for (long k = threadIdx.x; k < K; k += blockDim.x) m = fmax(m, fabs(row[k]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
-    m = fmax(m, sh[0]);
-    e[blockIdx.x] = exp_above(m);
-  }
-}
-
 // X statistics once per load, in one pass each:
 //  * row_stats: one block per row → e[i] (the row's exponent) and the max over rows of
 //    max_k|x| / mean_k|x| (atomicMax on the positive ratio's bit pattern);
@@ -175,7 +129,9 @@ __global__ void col_stats_final(const double* __restrict__ pmax, const double* _
 }
 
 // digits of X once per load: row blockIdx.y, exponents per row (by_row) or per column;
-// by_row also adds the row's digit sums into sums[p·R + i] (zeroed by the caller)
+// by_row also adds the row's digit sums into sums[p·R + i] (zeroed by the caller).  Eight
+// consecutive elements per thread (K % 8 == 0, as the INT8 path requires 16-aligned shapes):
+// four 16-byte loads, one 8-byte store per digit plane.
 __global__ void split_x(const double* __restrict__ a, long R, long K, long lda, const int* __restrict__ e, int by_row,
                         int8_t* __restrict__ out, int* __restrict__ sums) {
   const long i = blockIdx.y;
@@ -184,28 +140,53 @@ __global__ void split_x(const double* __restrict__ a, long R, long K, long lda, 
   const long dstride = R * K;
   const int er = by_row ? e[i] : 0;
   int acc[SMAX] = {};
-  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
-    const int ex = (by_row ? er : e[k]) + 1;
-    int dig[SMAX];
-    cut8(row[k] * __longlong_as_double((long long)(1023 - ex) << 52), o + k, dstride, dig);   // |z| < 1/2
+  for (long k = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 8; k < K; k += (long)gridDim.x * blockDim.x * 8) {
+    double v[8];
 #pragma unroll
-    for (int p = 0; p < SMAX; ++p) acc[p] += dig[p];
+    for (int h = 0; h < 4; ++h) {
+      const double2 t = *reinterpret_cast<const double2*>(row + k + 2 * h);
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+    unsigned long long packed[SMAX] = {};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ex = (by_row ? er : e[k + u]) + 1;
+      int8_t dd[SMAX];
+      int dig[SMAX];
+      cut8(v[u] * __longlong_as_double((long long)(1023 - ex) << 52), dd, 1, dig);   // |z| < 1/2
+#pragma unroll
+      for (int p = 0; p < SMAX; ++p) {
+        acc[p] += dig[p];
+        packed[p] |= (unsigned long long)(unsigned char)dd[p] << (8 * u);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < SMAX; ++p) *reinterpret_cast<unsigned long long*>(o + p * dstride + k) = packed[p];
   }
   if (by_row) add_digit_sums(acc, sums + i, R);
 }
 
 // column sums of the SMAX digit planes of an R × K int8 matrix: sums[p·K + k] (zeroed by the
-// caller); grid (column blocks, row chunks)
+// caller); grid (column blocks of 4 columns per thread, row chunks); K % 4 == 0
 __global__ void digit_colsums(const int8_t* __restrict__ d, long R, long K, int chunks, int* __restrict__ sums) {
-  const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long k = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (k >= K) return;
   const long r0 = R * blockIdx.y / chunks, r1 = R * (blockIdx.y + 1) / chunks;
-  int acc[SMAX] = {};
+  int acc[SMAX][4] = {};
   for (long i = r0; i < r1; ++i)
 #pragma unroll
-    for (int p = 0; p < SMAX; ++p) acc[p] += d[(long)p * R * K + i * K + k];
+    for (int p = 0; p < SMAX; ++p) {
+      const char4 c = *reinterpret_cast<const char4*>(d + (long)p * R * K + i * K + k);
+      acc[p][0] += c.x;
+      acc[p][1] += c.y;
+      acc[p][2] += c.z;
+      acc[p][3] += c.w;
+    }
 #pragma unroll
-  for (int p = 0; p < SMAX; ++p) atomicAdd(sums + (long)p * K + k, acc[p]);
+  for (int p = 0; p < SMAX; ++p)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) atomicAdd(sums + (long)p * K + k + u, acc[p][u]);
 }
 
 // Per-product factor path (R ≤ a few hundred rows, K long): row maxima with many blocks per
@@ -250,58 +231,6 @@ __global__ void split_rows(const double* __restrict__ a, long R, long K, long ld
     for (int p = 0; p < SMAX; ++p) acc[p] += dig[p];
   }
   add_digit_sums(acc, sums + i, R);
-}
-
-// e[k] for max_i |a[i][k]| of an R × K row-major matrix (thread per column, coalesced rows)
-__global__ void col_exp(const double* __restrict__ a, long R, long K, long lda, int* e) {
-  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
-    double m = 0.0;
-    for (long i = 0; i < R; ++i) m = fmax(m, fabs(a[i * lda + k]));
-    e[k] = exp_above(m);
-  }
-}
-
-// Dynamic range of an R × K row-major matrix along K: ratio[0] = max over rows of
-// max_k |a| / mean_k |a| (rows with a zero sum are skipped).  One block per row.
-__global__ void row_range(const double* __restrict__ a, long K, long lda, unsigned long long* ratio_bits) {
-  __shared__ double smax[32], ssum[32];
-  const double* row = a + (long)blockIdx.x * lda;
-  double m = 0.0, t = 0.0;
-  for (long k = threadIdx.x; k < K; k += blockDim.x) {
-    const double v = fabs(row[k]);
-    m = fmax(m, v);
-    t += v;
-  }
-  for (int o = 16; o; o >>= 1) {
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    t += __shfl_xor_sync(0xffffffffu, t, o);
-  }
-  if ((threadIdx.x & 31) == 0) { smax[threadIdx.x >> 5] = m; ssum[threadIdx.x >> 5] = t; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tt = 0.0;
-    m = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      m = fmax(m, smax[w]);
-      tt += ssum[w];
-    }
-    if (tt > 0.0) {
-      const double ratio = m * (double)K / tt;      // positive: the bit pattern orders like the value
-      atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(ratio));
-    }
-  }
-}
-// Same along the rows: thread per column.
-__global__ void col_range(const double* __restrict__ a, long R, long K, long lda, unsigned long long* ratio_bits) {
-  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (long)gridDim.x * blockDim.x) {
-    double m = 0.0, t = 0.0;
-    for (long i = 0; i < R; ++i) {
-      const double v = fabs(a[i * lda + k]);
-      m = fmax(m, v);
-      t += v;
-    }
-    if (t > 0.0) atomicMax(ratio_bits, (unsigned long long)__double_as_longlong(m * (double)R / t));
-  }
 }
 
 // out[i][j] = sum_{q} sum_{p < S-q} 2^{ea_i + eb_j + 2 - 8(p+q+2)} · (D^A_p·D^B_q)_ij with
