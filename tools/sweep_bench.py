@@ -6,7 +6,7 @@ import numpy as np
 import paper_1805_06604_b200 as E
 
 LONG = int(os.environ.get("SWEEP_LONG", "40"))
-r, n = 128, int(os.environ.get("SWEEP_N", "32768"))
+r, n = int(os.environ.get("SWEEP_R", "128")), int(os.environ.get("SWEEP_N", "32768"))
 rng = np.random.default_rng(0)
 w = rng.random((4096, r))
 G = w.T @ w
