@@ -368,6 +368,19 @@ int hals_variant() {
   return v;
 }
 
+// Tiles (8 columns) per CTA the sweep grid aims for (capped at one CTA per SM).  2 measured
+// best from N = 200 to 8192 columns (tools/sweep_grid.sh, profiles/r01_sweep_grid.txt): a
+// rank's 4096 columns when C5 is sharded over 8 GPUs sweep in 17.4 µs on 148 CTAs vs 30.0 µs
+// on 32 (the previous 16 tiles per CTA); C5 itself fills every SM either way.
+// ENMF_SWEEP_TPC overrides (timing experiments).
+long sweep_tiles_per_cta() {
+  static long v = [] {
+    const char* e = std::getenv("ENMF_SWEEP_TPC");
+    return e ? std::max(1L, std::atol(e)) : 2L;
+  }();
+  return v;
+}
+
 template <int R_>
 void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
@@ -389,19 +402,6 @@ void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   lc.attrs = at;
   lc.numAttrs = 1;
   CU(cudaLaunchKernelEx(&lc, hals::sweep_tf32<R_>, a, ntiles));
-}
-
-// Tiles (8 columns) per CTA the sweep grid aims for (capped at one CTA per SM).  2 measured
-// best from N = 200 to 8192 columns (tools/sweep_grid.sh, profiles/r01_sweep_grid.txt): a
-// rank's 4096 columns when C5 is sharded over 8 GPUs sweep in 17.4 µs on 148 CTAs vs 30.0 µs
-// on 32 (the previous 16 tiles per CTA); C5 itself fills every SM either way.
-// ENMF_SWEEP_TPC overrides (timing experiments).
-long sweep_tiles_per_cta() {
-  static long v = [] {
-    const char* e = std::getenv("ENMF_SWEEP_TPC");
-    return e ? std::max(1L, std::atol(e)) : 2L;
-  }();
-  return v;
 }
 
 template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
