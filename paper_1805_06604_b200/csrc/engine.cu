@@ -701,6 +701,7 @@ void sparse_gather(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const long long*
   const long warps = std::max<long>(1, lines);
   const unsigned grid = (unsigned)std::min<long>((warps + 7) / 8, (long)c->sms * 16);
   if (exact) sparse::gather_lines<true><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
+  else if (r <= 32) sparse::gather_lines_par<<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
   else sparse::gather_lines<false><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
   CUK();
   c->launches++;

@@ -45,4 +45,59 @@ __global__ void __launch_bounds__(256) gather_lines(const long long* ptr, const 
   }
 }
 
+// FP64 product mode, r <= 32: the stored entries of a line are dealt round-robin over the lanes
+// (lane l takes entries l, l+32, …, each contributing its whole gathered row to r accumulators),
+// then one reduce-scatter leaves the total for k = l in lane l.  The dependent chain per line
+// drops from its length to length/32, which is what matters for the term rows of a Zipf corpus
+// (the most frequent terms occur in most documents: one warp walking a 10^4-entry row was the
+// whole X·Tᵀ time at C4).  Fixed order per line: deterministic.
+__global__ void __launch_bounds__(256) gather_lines_par(const long long* ptr, const int* idx, const double* v,
+                                                        const double* G, int lines, int r, double* out, long ldo,
+                                                        const DevState* st) {
+  if (st && !dev_active(st)) return;
+  const int lane = threadIdx.x & 31;
+  const long wid = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long i = wid; i < lines; i += nw) {
+    const long p0 = ptr[i], p1 = ptr[i + 1];
+    double acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    if ((r & 1) == 0) {
+      // even r: the gathered row (8r bytes, 16-byte aligned) in 16-byte loads
+      for (long p = p0 + lane; p < p1; p += 32) {
+        const double x = __ldg(v + p);
+        const double2* g = reinterpret_cast<const double2*>(G + (long)__ldg(idx + p) * r);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (2 * k < r) {
+            const double2 t = __ldg(g + k);
+            acc[2 * k] = fma(t.x, x, acc[2 * k]);
+            acc[2 * k + 1] = fma(t.y, x, acc[2 * k + 1]);
+          }
+      }
+    } else {
+      for (long p = p0 + lane; p < p1; p += 32) {
+        const double x = __ldg(v + p);
+        const double* g = G + (long)__ldg(idx + p) * r;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < r) acc[k] = fma(__ldg(g + k), x, acc[k]);
+      }
+    }
+    // reduce-scatter over the lanes: afterwards acc[0] of lane l is the line's total for k = l
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+      const bool upper = (lane & w) != 0;
+#pragma unroll
+      for (int j = 0; j < w; ++j) {
+        const double send = upper ? acc[j] : acc[j + w];
+        const double keep = upper ? acc[j + w] : acc[j];
+        acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+      }
+    }
+    if (lane < r) out[(long)lane * ldo + i] = acc[0];
+  }
+}
+
 }  // namespace sparse
