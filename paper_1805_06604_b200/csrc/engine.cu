@@ -89,6 +89,13 @@ struct enmf_gpu_ctx {
   bool sparse = false;
   size_t nnz = 0;
   DBuf<long long> csr_ptr, csc_ptr;
+  // fixed-size chunks of the CSR rows / CSC columns for the FP64-mode gathers (sparse.cuh)
+  struct Chunks {
+    DBuf<int> line, slot, mline, mfirst, mcount;
+    DBuf<long long> beg, end;
+    int n = 0, nmulti = 0, nslots = 0;
+  } ch_csr, ch_csc;
+  DBuf<double> chunk_part;
   DBuf<int> csr_idx, csc_idx;
   DBuf<double> csr_val, csc_val, rowmaj;
   // FP64 cross products on INT8 tensor cores (ozaki.cuh): X digits (cut once per load)
@@ -697,7 +704,24 @@ void mark(enmf_gpu_ctx* c, cudaStream_t s, Prof* p, int phase) {
 // CSR products (sparse.cuh): the r-major factor is transposed into the row-major
 // scratch, then gathered once per stored entry in the reference's order.
 void sparse_gather(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const long long* ptr, const int* idx,
-                   const double* val, long lines, const double* Frm, int r, double* out, const DevState* st) {
+                   const double* val, long lines, const double* Frm, int r, double* out, const DevState* st,
+                   const enmf_gpu_ctx::Chunks* ch = nullptr) {
+  if (!exact && r <= 32 && ch && ch->n > 0) {
+    c->chunk_part.ensure((size_t)std::max(1, ch->nslots) * 32);
+    const unsigned grid = (unsigned)std::min<long>(((long)ch->n + 7) / 8, (long)c->sms * 16);
+    sparse::gather_chunks<<<grid, 256, 0, s>>>(ch->line.p, ch->beg.p, ch->end.p, ch->slot.p, ch->n, idx, val, Frm, r,
+                                               out, lines, c->chunk_part.p, st);
+    CUK();
+    c->launches++;
+    if (ch->nmulti > 0) {
+      sparse::combine_chunks<<<(unsigned)std::max(1L, std::min<long>(((long)ch->nmulti * r + 255) / 256, 1024)), 256, 0,
+                               s>>>(ch->mline.p, ch->mfirst.p, ch->mcount.p, ch->nmulti, c->chunk_part.p, r, out, lines,
+                                    st);
+      CUK();
+      c->launches++;
+    }
+    return;
+  }
   const long warps = std::max<long>(1, lines);
   const unsigned grid = (unsigned)std::min<long>((warps + 7) / 8, (long)c->sms * 16);
   if (exact) sparse::gather_lines<true><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
@@ -705,6 +729,44 @@ void sparse_gather(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const long long*
   else sparse::gather_lines<false><<<grid, 256, 0, s>>>(ptr, idx, val, Frm, (int)lines, r, out, lines, st);
   CUK();
   c->launches++;
+}
+
+// Chunk table of a compressed line structure (CSR rows or CSC columns): lines longer than
+// `chunk` entries are split (host, once per load).
+void build_chunks(enmf_gpu_ctx::Chunks& ch, const std::vector<long long>& ptr, long chunk) {
+  std::vector<int> line, slot, mline, mfirst, mcount;
+  std::vector<long long> beg, end;
+  int nslots = 0;
+  const long lines = (long)ptr.size() - 1;
+  for (long i = 0; i < lines; ++i) {
+    const long long b = ptr[i], e = ptr[i + 1];
+    const long long len = e - b;
+    const long long nc = std::max<long long>(1, (len + chunk - 1) / chunk);
+    if (nc > 1) {
+      mline.push_back((int)i);
+      mfirst.push_back(nslots);
+      mcount.push_back((int)nc);
+    }
+    for (long long q = 0; q < nc; ++q) {
+      line.push_back((int)i);
+      beg.push_back(b + q * chunk);
+      end.push_back(std::min(e, b + (q + 1) * chunk));
+      slot.push_back(nc > 1 ? nslots++ : -1);
+    }
+  }
+  ch.n = (int)line.size();
+  ch.nmulti = (int)mline.size();
+  ch.nslots = nslots;
+  auto up_i = [](DBuf<int>& d, const std::vector<int>& h) {
+    d.ensure(std::max<size_t>(1, h.size()));
+    if (!h.empty()) CU(cudaMemcpy(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+  };
+  auto up_l = [](DBuf<long long>& d, const std::vector<long long>& h) {
+    d.ensure(std::max<size_t>(1, h.size()));
+    if (!h.empty()) CU(cudaMemcpy(d.p, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  };
+  up_i(ch.line, line); up_i(ch.slot, slot); up_i(ch.mline, mline); up_i(ch.mfirst, mfirst); up_i(ch.mcount, mcount);
+  up_l(ch.beg, beg); up_l(ch.end, end);
 }
 
 void transpose_launch(enmf_gpu_ctx* c, cudaStream_t s, const double* in, double* out, long rows, long cols) {
@@ -719,7 +781,7 @@ void sparse_xht(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* Tm, i
                 const DevState* st) {
   c->rowmaj.ensure(std::max(c->m, c->n) * (size_t)r);
   transpose_launch(c, s, Tm, c->rowmaj.p, r, (long)c->n);
-  sparse_gather(c, s, exact, c->csr_ptr.p, c->csr_idx.p, c->csr_val.p, (long)c->m, c->rowmaj.p, r, out, st);
+  sparse_gather(c, s, exact, c->csr_ptr.p, c->csr_idx.p, c->csr_val.p, (long)c->m, c->rowmaj.p, r, out, st, &c->ch_csr);
 }
 
 // W_yᵀX (r×n) for CSR X (through the CSC copy), W_yᵀ r×m  (linalg.hpp:86-104)
@@ -727,7 +789,7 @@ void sparse_wx(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* WyT, i
                const DevState* st) {
   c->rowmaj.ensure(std::max(c->m, c->n) * (size_t)r);
   transpose_launch(c, s, WyT, c->rowmaj.p, r, (long)c->m);
-  sparse_gather(c, s, exact, c->csc_ptr.p, c->csc_idx.p, c->csc_val.p, (long)c->n, c->rowmaj.p, r, out, st);
+  sparse_gather(c, s, exact, c->csc_ptr.p, c->csc_idx.p, c->csc_val.p, (long)c->n, c->rowmaj.p, r, out, st, &c->ch_csc);
 }
 
 // ---- FP64 cross products on INT8 tensor cores (ozaki.cuh) ----------------------
