@@ -377,6 +377,19 @@ def test_c4_shaped_csr_parity(ctx, port):
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
 
 
+@pytest.mark.parametrize("r", [7, 21, 40])
+def test_csr_gather_paths_parity(ctx, port, r):
+    """CSR gathers in FP64 mode across their paths: 512-entry chunks with split term rows and
+    16-byte row loads (even r <= 32), scalar loads (odd r), the lane-per-k kernel (r > 32);
+    3000×1500 documents vs the oracle."""
+    m, n = 3000, 1500
+    off, cidx, vals = port.gen_docs(m, n, 13)
+    w0, h0 = port.random_init(m, n, r, 14)
+    ref = port.run_csr(off, cidx, vals, m, n, w0, h0, preset("e-ahals-hp3", max_outer_iterations=6))
+    rec = ctx.run_csr(off, cidx, vals, m, n, w0, h0, _cfg("e-ahals-hp3", 6), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+
+
 def test_csr_validation_errors(ctx):
     """SparseMatrix::validate (matrix.hpp:226-251): same failures, InvalidArgument."""
     w0 = np.ones((3, 2))
