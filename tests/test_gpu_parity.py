@@ -377,6 +377,19 @@ def test_c4_shaped_csr_parity(ctx, port):
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
 
 
+@pytest.mark.parametrize("r", [5, 31, 40])
+def test_eanls_bpp_paths_parity(ctx, port, r):
+    """E-ANLS through the engine on both BPP kernels: the lane-parallel solver (r <= 32, FP64
+    product mode) and the reference-order one (r > 32); 600×500 vs the oracle."""
+    m, n = 600, 500
+    rng = np.random.default_rng(r)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.05 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, r + 1)
+    ref = port.run_dense(x, w0, h0, preset("e-anls-hp1", max_outer_iterations=8))
+    rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 8), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=True)
+
+
 @pytest.mark.parametrize("r", [7, 21, 40])
 def test_csr_gather_paths_parity(ctx, port, r):
     """CSR gathers in FP64 mode across their paths: 512-entry chunks with split term rows and
