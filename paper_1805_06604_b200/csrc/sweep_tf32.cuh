@@ -204,10 +204,11 @@ __global__ void __launch_bounds__(256, 1) sweep_tf32(Args a, long ntiles) {
       if (producer) {
         tf_producer_round<RMAX>(a, col0, nt, Hs, Ss, gf, g, t, idS, idH);
       } else {
+        // predicated stores with a running row pointer (no branches, no per-row 64-bit multiplies)
         const long col = col0 + lane;
         const bool valid = lane < nt * 8 && col < a.N;
-        const int rv = valid ? r : 0;
-        double* hp = a.H + col;
+        const long ld = a.ld, ld8 = 8 * ld;
+        double* hp = a.H + (valid ? col : 0);     // row 8b of this lane's column
         int hmax = 0;
 #pragma unroll 1
         for (int b = 0; b < NB; ++b) {
@@ -239,12 +240,10 @@ __global__ void __launch_bounds__(256, 1) sweep_tf32(Args a, long ntiles) {
           if (b + 1 < NB) nb_arrive(idH);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            if (8 * b + k < rv) {
-              hp[(long)(8 * b + k) * a.ld] = (double)hv[k];
-              const int hb = __float_as_int(hv[k]);
-              hmax = hb > hmax ? hb : hmax;
-            }
+            if (valid && 8 * b + k < r) hp[k * ld] = (double)hv[k];
+            hmax = max(hmax, __float_as_int(hv[k]));
           }
+          hp += ld8;
         }
         nf |= hmax >= 0x7F800000;
         gain_d += (double)gain;
