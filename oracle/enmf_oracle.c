@@ -23,6 +23,15 @@
 #include <time.h>
 
 static _Thread_local char g_err[512];
+/* Multi-threaded bit-exact replica kernels (replica.c); used when orc_set_threads(n > 1). */
+extern int g_orc_threads;
+void rep_cross_wx(const double* w, const double* x, size_t m, size_t n, size_t r, double* out);
+void rep_cross_xht(const double* x, const double* h, size_t m, size_t n, size_t r, double* out);
+void rep_gram(const double* a, size_t rows, size_t r, double* g);
+void rep_gram_rows(const double* t, size_t r, size_t n, double* g);
+int rep_hals_solve(const double* gram, const double* cross, const double* h0, size_t r, size_t n,
+                   uint64_t max_sweeps, double stall_fraction, double* h, int32_t* sweeps);
+
 static void set_err(const char* msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
 const char* orc_last_error(void) { return g_err; }
 
@@ -205,7 +214,8 @@ double orc_fast_error(double norm_x_sq, const double* w, const double* xht, cons
   cs_add(&acc, norm_x_sq);
   for (size_t i = 0; i < m * r; ++i) cs_add(&acc, -2.0 * w[i] * xht[i]);
   double* wtw = (double*)malloc(sizeof(double) * r * r);
-  orc_gram(w, m, r, wtw);
+  if (g_orc_threads > 1) rep_gram(w, m, r, wtw);
+  else orc_gram(w, m, r, wtw);
   for (size_t i = 0; i < r * r; ++i) cs_add(&acc, wtw[i] * hht[i]);
   free(wtw);
   const double v = cs_value(&acc);
@@ -472,11 +482,13 @@ typedef struct {
 } xmat;
 
 static void x_cross_wx(const xmat* X, const double* w, size_t r, double* out) {
-  if (X->sparse) orc_cross_wx_csr(w, X->off, X->cidx, X->vals, X->m, X->n, r, out);
+  if (!X->sparse && g_orc_threads > 1) rep_cross_wx(w, X->x, X->m, X->n, r, out);
+  else if (X->sparse) orc_cross_wx_csr(w, X->off, X->cidx, X->vals, X->m, X->n, r, out);
   else orc_cross_wx(w, X->x, X->m, X->n, r, out);
 }
 static void x_cross_xht(const xmat* X, const double* h, size_t r, double* out) {
-  if (X->sparse) orc_cross_xht_csr(X->off, X->cidx, X->vals, h, X->m, X->n, r, out);
+  if (!X->sparse && g_orc_threads > 1) rep_cross_xht(X->x, h, X->m, X->n, r, out);
+  else if (X->sparse) orc_cross_xht_csr(X->off, X->cidx, X->vals, h, X->m, X->n, r, out);
   else orc_cross_xht(X->x, h, X->m, X->n, r, out);
 }
 
@@ -506,14 +518,20 @@ static int gram_with_reinit(double* a, size_t rows, size_t r, size_t rs, size_t 
                             uint64_t reinit_seed, uint64_t salt, int* modified, double* g) {
   size_t* bad = (size_t*)malloc(sizeof(size_t) * (r ? r : 1));
   for (uint64_t attempt = 0;; ++attempt) {
-    memset(g, 0, sizeof(double) * r * r);
-    for (size_t i = 0; i < rows; ++i)
-      for (size_t k = 0; k < r; ++k) {
-        const double aik = a[k * cs + i * rs];
-        for (size_t j = k; j < r; ++j) g[k * r + j] += aik * a[j * cs + i * rs];
-      }
-    for (size_t k = 0; k < r; ++k)
-      for (size_t j = k + 1; j < r; ++j) g[j * r + k] = g[k * r + j];
+    if (g_orc_threads > 1 && cs == 1 && rs == r) {
+      rep_gram(a, rows, r, g);
+    } else if (g_orc_threads > 1 && rs == 1 && cs == rows) {
+      rep_gram_rows(a, r, rows, g);
+    } else {
+      memset(g, 0, sizeof(double) * r * r);
+      for (size_t i = 0; i < rows; ++i)
+        for (size_t k = 0; k < r; ++k) {
+          const double aik = a[k * cs + i * rs];
+          for (size_t j = k; j < r; ++j) g[k * r + j] += aik * a[j * cs + i * rs];
+        }
+      for (size_t k = 0; k < r; ++k)
+        for (size_t j = k + 1; j < r; ++j) g[j * r + k] = g[k * r + j];
+    }
     const double floor_ = 1e-16 * max_diagonal(g, r);
     size_t nb = 0;
     for (size_t k = 0; k < r; ++k) if (!(g[k * r + k] > floor_)) bad[nb++] = k;
@@ -529,6 +547,17 @@ static int gram_with_reinit(double* a, size_t rows, size_t r, size_t rs, size_t 
       for (size_t i = 0; i < rows; ++i) a[bad[q] * cs + i * rs] = orc_uniform_unit(&gen);
     if (modified) *modified = 1;
   }
+}
+
+/* hals_solve through the replica when threaded; the replica reports the degenerate row
+ * without the message, so the port's solver reruns to produce it (same result). */
+static int hals(const double* gram, const double* cross, const double* h0, size_t r, size_t n,
+                uint64_t max_sweeps, double stall_fraction, double* h, int32_t* sweeps) {
+  if (g_orc_threads > 1 && r <= 4096) {
+    int rc = rep_hals_solve(gram, cross, h0, r, n, max_sweeps, stall_fraction, h, sweeps);
+    if (rc != ENMF_DEGENERATE_COLUMN) return rc;
+  }
+  return orc_hals_solve(gram, cross, h0, r, n, max_sweeps, stall_fraction, h, sweeps);
 }
 
 typedef struct {
@@ -569,8 +598,8 @@ static int step(const xmat* X, double norm_x_sq, ext_state* st, const enmf_gpu_c
   } else {
     uint64_t ms = cfg->inner_max_sweeps ? cfg->inner_max_sweeps
                   : orc_derive_max_sweeps(setup_flops, (double)n * (double)r * (double)r, cfg->inner_sweep_ratio);
-    rc = orc_hals_solve(gram_h, cross_h, st->h_y, r, n, ms, cfg->inner_stall_fraction, st->h_n,
-                        &rec->inner_h_count);
+    rc = hals(gram_h, cross_h, st->h_y, r, n, ms, cfg->inner_stall_fraction, st->h_n,
+              &rec->inner_h_count);
   }
   if (rc) return rc;
   if (!all_finite(st->h_n, r * n)) { set_err("H update produced a non-finite value"); return ENMF_NON_FINITE; }
@@ -596,8 +625,8 @@ static int step(const xmat* X, double norm_x_sq, ext_state* st, const enmf_gpu_c
   } else {
     uint64_t ms = cfg->inner_max_sweeps ? cfg->inner_max_sweeps
                   : orc_derive_max_sweeps(setup_flops, (double)m * (double)r * (double)r, cfg->inner_sweep_ratio);
-    rc = orc_hals_solve(gram_t, pw_cross, wy_t, r, m, ms, cfg->inner_stall_fraction, wn_t,
-                        &rec->inner_w_count);
+    rc = hals(gram_t, pw_cross, wy_t, r, m, ms, cfg->inner_stall_fraction, wn_t,
+              &rec->inner_w_count);
   }
   if (rc) return rc;
   transpose(wn_t, r, m, st->w_n);
@@ -614,7 +643,8 @@ static int step(const xmat* X, double norm_x_sq, ext_state* st, const enmf_gpu_c
   /* error (:402-416) */
   double err;
   if (cfg->hp == 1 && cfg->literal_hp1_order && cfg->extrapolation_enabled) {
-    orc_gram_rows(st->h_y, r, n, lit_g);
+    if (g_orc_threads > 1) rep_gram_rows(st->h_y, r, n, lit_g);
+    else orc_gram_rows(st->h_y, r, n, lit_g);
     x_cross_xht(X, st->h_y, r, lit_x);
     err = orc_fast_error(norm_x_sq, st->w_n, lit_x, lit_g, m, r);
   } else {
@@ -676,7 +706,8 @@ static int run_impl(const xmat* X, const double* w0, const double* h0, size_t r,
   {
     double* g0 = ws;
     double* x0 = ws + r * r;
-    orc_gram_rows(h0, r, n, g0);
+    if (g_orc_threads > 1) rep_gram_rows(h0, r, n, g0);
+    else orc_gram_rows(h0, r, n, g0);
     x_cross_xht(X, h0, r, x0);
     const double e0 = orc_fast_error(norm_x_sq, w0, x0, g0, m, r);
     st.err_prev = e0;
@@ -726,7 +757,8 @@ int orc_time_steps(const double* x, size_t m, size_t n, const double* w0, const 
   st.schedule.beta = cfg->beta0; st.schedule.beta_bar = 1.0; st.schedule.beta_prev = cfg->beta0;
   st.schedule.gamma = cfg->gamma; st.schedule.gamma_bar = cfg->gamma_bar; st.schedule.eta = cfg->eta;
   st.restarted = 0;
-  orc_gram_rows(h0, r, n, ws);
+  if (g_orc_threads > 1) rep_gram_rows(h0, r, n, ws);
+  else orc_gram_rows(h0, r, n, ws);
   x_cross_xht(&X, h0, r, ws + r * r);
   st.err_prev = orc_fast_error(nx2, w0, ws + r * r, ws, m, r);
   struct timespec t0, t1;

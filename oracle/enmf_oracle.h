@@ -87,6 +87,15 @@ int orc_gen_docs(size_t m, size_t n, double zipf_s, uint64_t seed, uint64_t** of
                  double** vals, size_t* nnz);
 void orc_free(void* p);
 
+/* ---- replica.c: bit-exact multi-threaded execution of the dense path ----
+ * n > 1 routes cross_wx, cross_xht, gram and hals_solve of orc_run_dense /
+ * orc_time_steps through OpenMP kernels that keep every element's reference
+ * summation order (bitwise identical results); 1 = the plain port. */
+void orc_set_threads(int n);
+int orc_get_threads(void);
+/* C5 data (X = W0·H0 + 0.01·|N(0,1)|) on T×T tiles with per-tile streams (replica.c). */
+int orc_gen_tiled(size_t m, size_t n, size_t r, uint64_t seed, size_t T, double* x);
+
 const char* orc_last_error(void);
 
 #ifdef __cplusplus

@@ -161,6 +161,9 @@ class Oracle:
             L.orc_derive_max_sweeps.argtypes = [C.c_double, C.c_double, C.c_double]
             L.orc_derive_max_sweeps.restype = C.c_uint64
             L.orc_config_validate.argtypes = [C.POINTER(Config)]
+            L.orc_set_threads.argtypes = [C.c_int]
+            L.orc_get_threads.restype = C.c_int
+            L.orc_gen_tiled.argtypes = [_sz, _sz, _sz, C.c_uint64, _sz, _dp]
         else:
             L.ref_gram.argtypes = [_dp, _sz, _sz, _dp]
             L.ref_cross_wx.argtypes = [_dp, _dp, _sz, _sz, _sz, _dp]
@@ -286,6 +289,27 @@ class Oracle:
         x = np.zeros((m, n))
         self._check(self.lib.orc_gen_config(which, m, n, r, seed, x))
         return x
+
+    def gen_tiled(self, m, n, r, seed, tile=4096, threads=None):
+        """C5 data on tiles with per-tile streams (replica.c orc_gen_tiled); any thread count
+        gives the same bits."""
+        x = np.empty((m, n))
+        old = self.threads
+        self.threads = threads or os.cpu_count() or 1
+        try:
+            self._check(self.lib.orc_gen_tiled(m, n, r, seed, tile, x))
+        finally:
+            self.threads = old
+        return x
+
+    @property
+    def threads(self) -> int:
+        """Replica threads for run_dense / time_steps (1 = the plain single-threaded port)."""
+        return self.lib.orc_get_threads()
+
+    @threads.setter
+    def threads(self, n: int) -> None:
+        self.lib.orc_set_threads(int(n))
 
     def gen_docs(self, m, n, seed, zipf_s=1.1):
         po, pc, pv = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)(), C.POINTER(C.c_double)()

@@ -120,7 +120,7 @@ struct enmf_gpu_ctx {
   // factors and products
   DBuf<double> WT, WyT, WnT, H, Hy, Hn, CH, P, Plit, GH, GW, GWn, Glit, scratch, Gf;
   DBuf<double> partials, gain_part, terms, ddpart, dd;
-  DBuf<int> part_nf, flags;
+  DBuf<int> part_nf, flags, kpart_nf;
   DBuf<unsigned> counters;
   DBuf<unsigned long long> bpp_exch;
   DBuf<int> bpp_rounds, bpp_nf;
@@ -203,12 +203,9 @@ void set_attrs_once() {
   big((const void*)hals::sweep_ws<32>, hals::ws_smem_bytes<32>());
   big((const void*)hals::sweep_ws<64>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128>, hals::ws_smem_bytes<128>());
-  big((const void*)hals::sweep_ws<32, false, 0, true>, hals::ws_smem_bytes<32>());
-  big((const void*)hals::sweep_ws<64, false, 0, true>, hals::ws_smem_bytes<64>());
-  big((const void*)hals::sweep_ws<128, false, 0, true>, hals::ws_smem_bytes<128>());
-  big((const void*)hals::sweep_t2<32>, hals::t2_smem_bytes<32>());
-  big((const void*)hals::sweep_t2<64>, hals::t2_smem_bytes<64>());
-  big((const void*)hals::sweep_t2<128>, hals::t2_smem_bytes<128>());
+  big((const void*)hals::sweep_ws<32, true>, hals::ws_smem_bytes<32>());
+  big((const void*)hals::sweep_ws<64, true>, hals::ws_smem_bytes<64>());
+  big((const void*)hals::sweep_ws<128, true>, hals::ws_smem_bytes<128>());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -362,15 +359,13 @@ void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, lon
 // ---- inner solvers ------------------------------------------------------------
 int hals_variant() {
   // ENMF_HALS_KERNEL: "" / "wsp" persistent paired-warp kernel (default), "ws" one launch per
-  // sweep, "fma" CUDA-core kernel, "ws[p]prof*" timing experiments.  Retired variants and their
-  // measurements: profiles/r01_sweep_variants.md.
+  // sweep, "fma" CUDA-core kernel.  Retired variants, the timing-experiment builds and their
+  // measurements: profiles/r01_sweep_variants.md (the experiment builds are not in the product).
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("ENMF_HALS_KERNEL");
     const std::string s = e ? e : "";
-    v = s == "fma" ? 1 : s == "ws" ? 50 : s == "wsprof" ? 51 : s == "wsprof1" ? 52 : s == "wsprof2" ? 53
-      : s == "wspprof" ? 55 : s == "wspprof1" ? 56 : s == "wspprof2" ? 57 : s == "wspprof3" ? 58
-      : s == "t2" ? 60 : s == "t2skip1" ? 61 : s == "t2skip2" ? 62 : s == "t2skip3" ? 63 : s == "t2prof" ? 64 : 54;
+    v = s == "fma" ? 1 : s == "ws" ? 50 : 54;
   }
   return v;
 }
@@ -411,19 +406,11 @@ void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   CU(cudaLaunchKernelEx(&lc, hals::sweep_tf32<R_>, a, ntiles));
 }
 
-template <int R_, bool PROF = false, int SKIP = 0, bool PERSIST = false>
+template <int R_, bool PERSIST = false>
 void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
   const long tpc = sweep_tiles_per_cta();
   const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + tpc - 1) / tpc));
-  if (PROF) {
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute((const void*)hals::sweep_ws<R_, true, SKIP, PERSIST>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, hals::ws_smem_bytes<R_>()));
-      attr = true;
-    }
-  }
   if (PERSIST) {
     // every CTA must be resident for the grid-wide decision between sweeps
     cudaLaunchConfig_t lc = {};
@@ -436,44 +423,17 @@ void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&lc, hals::sweep_ws<R_, PROF, SKIP, true>, a, ntiles));
+    CU(cudaLaunchKernelEx(&lc, hals::sweep_ws<R_, true>, a, ntiles));
     return;
   }
-  hals::sweep_ws<R_, PROF, SKIP><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
-}
-
-// Two-team persistent sweep (row passes on a DMMA-free sub-partition): one cooperative
-// launch per inner solve, one CTA per SM.
-template <int R_, int SKIP = 0, bool PROF = false>
-void launch_sweep_t2(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
-  const long ntiles = ((long)a.N + 7) / 8;
-  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 23) / 24));
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(256);
-  lc.dynamicSmemBytes = hals::t2_smem_bytes<R_>();
-  lc.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  if (SKIP || PROF) {
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute((const void*)hals::sweep_t2<R_, SKIP, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              hals::t2_smem_bytes<R_>()));
-      attr = true;
-    }
-  }
-  CU(cudaLaunchKernelEx(&lc, hals::sweep_t2<R_, SKIP, PROF>, a, ntiles));
+  hals::sweep_ws<R_><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 
 bool hals_use_fma() { return hals_variant() == 1; }
 
 // The persistent sweep kernel runs a whole inner solve in one launch.
 bool hals_persistent(int prec, int r) {
-  return prec != PREC_EXACT && r <= 128 && (hals_variant() == 54 || (hals_variant() >= 60 && hals_variant() <= 64));
+  return prec != PREC_EXACT && r <= 128 && hals_variant() == 54;
 }
 
 void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
@@ -500,40 +460,14 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     else if (r <= 64) SW(32, 2);
     else SW(32, 4);
 #undef SW
-  } else if (v == 60) {                 // two-team persistent sweep
-    if (r <= 32) launch_sweep_t2<32>(c, s, a);
-    else if (r <= 64) launch_sweep_t2<64>(c, s, a);
-    else launch_sweep_t2<128>(c, s, a);
-  } else if (v == 61) {                 // timing experiments: t2 without row passes / DMMAs / both
-    launch_sweep_t2<128, 1>(c, s, a);
-  } else if (v == 62) {
-    launch_sweep_t2<128, 2>(c, s, a);
-  } else if (v == 63) {
-    launch_sweep_t2<128, 3>(c, s, a);
-  } else if (v == 64) {
-    launch_sweep_t2<128, 0, true>(c, s, a);
   } else if (v == 50) {                 // one launch per sweep
     if (r <= 32) launch_sweep_ws<32>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64>(c, s, a);
     else launch_sweep_ws<128>(c, s, a);
-  } else if (v == 51) {                 // timing experiments: per-warp cycle profile into a.terms
-    launch_sweep_ws<128, true>(c, s, a);
-  } else if (v == 52) {
-    launch_sweep_ws<128, true, 1>(c, s, a);
-  } else if (v == 53) {
-    launch_sweep_ws<128, true, 2>(c, s, a);
-  } else if (v == 55) {                 // same, persistent: profile, no row pass, no DMMA, neither
-    launch_sweep_ws<128, true, 0, true>(c, s, a);
-  } else if (v == 56) {
-    launch_sweep_ws<128, true, 1, true>(c, s, a);
-  } else if (v == 57) {
-    launch_sweep_ws<128, true, 2, true>(c, s, a);
-  } else if (v == 58) {
-    launch_sweep_ws<128, true, 3, true>(c, s, a);
   } else {                              // default: persistent, one launch per inner solve
-    if (r <= 32) launch_sweep_ws<32, false, 0, true>(c, s, a);
-    else if (r <= 64) launch_sweep_ws<64, false, 0, true>(c, s, a);
-    else launch_sweep_ws<128, false, 0, true>(c, s, a);
+    if (r <= 32) launch_sweep_ws<32, true>(c, s, a);
+    else if (r <= 64) launch_sweep_ws<64, true>(c, s, a);
+    else launch_sweep_ws<128, true>(c, s, a);
   }
   CUK();
   c->launches++;
@@ -889,7 +823,9 @@ bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
   // rank's row / column block sizes multiples of 16)
   return env == 1 && prec == PREC_FAST && !c->sparse && (c->x || dist) &&
          (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072 &&
-         c->m % 16 == 0 && c->n % 16 == 0 && (!dist || (c->dist->mp % 16 == 0 && c->dist->np % 16 == 0));
+         c->m % 16 == 0 && c->n % 16 == 0 && (!dist || (c->dist->mp % 16 == 0 && c->dist->np % 16 == 0)) &&
+         // split_x reads X with 16-byte loads: a borrowed X (load_device) need only be 8-byte aligned
+         (dist ? ((((uintptr_t)c->dist->xc) | (uintptr_t)c->dist->xr) & 15) == 0 : ((uintptr_t)c->x & 15) == 0);
 }
 
 // digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph).
@@ -929,7 +865,8 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   const long nsum = by_row ? rows : cols;
   xd.sums.ensure((size_t)ozaki::SMAX * nsum);
   CU(cudaMemsetAsync(xd.sums.p, 0, (size_t)ozaki::SMAX * nsum * sizeof(int), s));
-  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols / 8 + 255) / 256, 8)), (unsigned)rows), 256,
+  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols / 8 + 255) / 256, 8)),
+                      (unsigned)std::min<long>(rows, 65535)), 256,
                     0, s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p, xd.sums.p);
   CUK();
   c->launches++;
@@ -970,9 +907,14 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
     off.q[q] = acc;
     acc += (long)Mq[q] * N;
   }
-  // one size for both products of this (m, n, r): no reallocation between captured launches
-  c->ocbuf.ensure(std::max((size_t)acc, ((size_t)(ozaki::SMAX * (ozaki::SMAX + 1) / 2) * r + 256) *
-                                            std::max(c->m, c->n)));
+  // one size for every product of this (m, n, r) — the largest stack layout (SMAX levels, short
+  // stacks padded to min(256, SMAX·r) rows) over the longest N: no reallocation between
+  // captured launches
+  size_t bound = 0;
+  for (int q = 0; q < ozaki::SMAX; ++q)
+    bound += (size_t)std::max((ozaki::SMAX - q) * r, std::min(256, ozaki::SMAX * r));
+  bound *= std::max(c->m, c->n);
+  c->ocbuf.ensure(std::max((size_t)acc, bound));
   if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
   c->amax.ensure((size_t)r);
   CU(cudaMemsetAsync(c->amax.p, 0, (size_t)r * sizeof(unsigned long long), s));
@@ -1069,16 +1011,7 @@ void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int sl
     a.Gf = gf;
     return;
   }
-  if (hals_variant() < 50 || hals_variant() > 64) return;
-  if (hals_variant() >= 60) {                        // sweep_t2: fragments without the tail split
-    if (a.r <= 32) hals::ws_prep<32, false><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
-    else if (a.r <= 64) hals::ws_prep<64, false><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
-    else hals::ws_prep<128, false><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
-    CUK();
-    c->launches++;
-    a.Gf = gf;
-    return;
-  }
+  if (hals_variant() != 50 && hals_variant() != 54) return;
   if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);

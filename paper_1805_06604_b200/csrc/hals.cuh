@@ -235,15 +235,6 @@ ENMF_DEV int ws_pos(int k, int c) {
 }
 
 ENMF_DEV void nb_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
-// clock64 after a shared-memory load that the hardware cannot issue before the preceding
-// barrier resolves (bar.sync defers its blocking; timing experiments only)
-ENMF_DEV long long clock_after_smem(const double* p) {
-  double v;
-  asm volatile("ld.volatile.shared.f64 %0, [%1];\n" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-  long long t;
-  asm volatile("{ .reg .pred q; setp.eq.f64 q, %1, %1; mov.u64 %0, %%clock64; }\n" : "=l"(t) : "d"(v) : "memory");
-  return t;
-}
 ENMF_DEV void nb_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" ::"r"(id) : "memory"); }
 
 ENMF_DEV double pos_part_ws(double t) {
@@ -313,9 +304,9 @@ ENMF_DEV void bar_arrive_n(int id) { asm volatile("bar.arrive %0, %1;\n" ::"r"(i
 
 // BT: threads on the hand-off barriers (64 = one product + one row warp; 128 = a team of
 // three product warps and their row warp, sweep_t2)
-template <int KS, int NB, int NT, bool PROF, int SKIP, int BT = 64>
+template <int KS, int NB, int NT, int BT = 64>
 ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf, int gi, int gt, int bx0, int bx1,
-                                int idS, int idH, long long* pw) {
+                                int idS, int idH) {
   double A0[KS], A1[KS];
 #pragma unroll
   for (int s = 0; s < KS; s += 2) {
@@ -326,25 +317,19 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
   }
 #pragma unroll 1
   for (int b = 0; b < NB; b += 2) {
-    const long long c0 = PROF ? clock64() : 0;
     if (b > 0) bar_sync_n<BT>(idH);                // rows of block b-1 are final in the tile
-    const long long c1 = PROF ? clock_after_smem(Ss) : 0;
-    if (PROF) pw[0] += c1 - c0;
     double acc0[4][2], acc1[4][2];
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc0[t][0] = acc0[t][1] = acc1[t][0] = acc1[t][1] = 0.0;
-    if (!(SKIP & 2)) {
 #pragma unroll
-      for (int j = 0; j < KS / 2; ++j) {   // (block b's fragments of A1 are zero: see ws_prep)
-        double2 p[4];
-        ws_ldb<NT>(Hs, j, gt, bx0, bx1, p);
-        ws_mma2<NT>(acc0, A0[2 * j], A0[2 * j + 1], p);
-        ws_mma2<NT>(acc1, A1[2 * j], A1[2 * j + 1], p);
-      }
+    for (int j = 0; j < KS / 2; ++j) {     // (block b's fragments of A1 are zero: see ws_prep)
+      double2 p[4];
+      ws_ldb<NT>(Hs, j, gt, bx0, bx1, p);
+      ws_mma2<NT>(acc0, A0[2 * j], A0[2 * j + 1], p);
+      ws_mma2<NT>(acc1, A1[2 * j], A1[2 * j + 1], p);
     }
     ws_store_s(Ss, gi, gt, acc0);
     bar_arrive_n<BT>(idS);                          // S_b ready: the row warp solves block b
-    if (PROF) pw[2] += clock64() - c1;
     // while it does: this pair's tail fragments and the next pair's Gram fragments
     const double2 tl = gf[(16 * KS * KS + (b >> 1) * 64) / 2];   // Gf tails (ws_prep)
     if (b + 2 < NB) {
@@ -356,18 +341,14 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
         A1[s] = f1.x; A1[s + 1] = f1.y;
       }
     }
-    const long long c3 = PROF ? clock64() : 0;
     bar_sync_n<BT>(idH);                            // block b solved
-    const long long c2 = PROF ? clock_after_smem(Ss) : 0;
-    if (PROF) pw[0] += c2 - c3;
-    if (!(SKIP & 2)) {
+    {
       double2 p[4];
       ws_ldb<NT>(Hs, b, gt, bx0, bx1, p);
       ws_mma2<NT>(acc1, tl.x, tl.y, p);
     }
     ws_store_s(Ss, gi, gt, acc1);
     bar_arrive_n<BT>(idS);                          // S_{b+1} ready
-    if (PROF) pw[2] += clock64() - c2;
   }
 }
 
@@ -380,9 +361,15 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
   const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);   // gains are accumulated halved
   const int bnf = __syncthreads_or(nf);
   const unsigned target = (unsigned)(sw + 1) * gridDim.x;
+  // partials double-buffered by sweep parity: a CTA that has already decided sweep sw and
+  // runs ahead writes its sweep sw+1 partial into the other half, never into the one a slower
+  // CTA may still be summing (it can only come back to this half after every CTA has arrived
+  // at sweep sw+1, i.e. after every CTA finished reading sweep sw's partials)
+  double* part = a.part + (sw & 1) * gridDim.x;
+  int* part_nf = a.part_nf + (sw & 1) * gridDim.x;
   if (threadIdx.x == 0) {
-    a.part[blockIdx.x] = bg;
-    a.part_nf[blockIdx.x] = bnf;
+    part[blockIdx.x] = bg;
+    part_nf[blockIdx.x] = bnf;
     __threadfence();
     const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
     s_dec = prev == target - 1 ? 1 : 0;      // this CTA arrived last (used when sharded)
@@ -398,8 +385,8 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
     double v = 0.0;
     int f = 0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-      v = __dadd_rn(v, __ldcg(a.part + b));
-      f |= __ldcg(a.part_nf + b);
+      v = __dadd_rn(v, __ldcg(part + b));
+      f |= __ldcg(part_nf + b);
     }
     const double total = block_reduce_sum_any(v, red);
     f = __syncthreads_or(f);
@@ -416,8 +403,8 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
     double v = 0.0;
     int f = 0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-      v = __dadd_rn(v, __ldcg(a.part + b));
-      f |= __ldcg(a.part_nf + b);
+      v = __dadd_rn(v, __ldcg(part + b));
+      f |= __ldcg(part_nf + b);
     }
     double total = block_reduce_sum_any(v, red);
     f = __syncthreads_or(f);
@@ -440,8 +427,6 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
   return s_dec;
 }
 
-// PROF (timing experiment): per-warp cycles [barrier wait, tile load, total, DMMA / row phase] into a.terms;
-// SKIP (timing experiment, wrong results): 1 = row warps skip the row pass, 2 = product warps skip the DMMAs
 // PERSIST: one launch runs every sweep of the solve.  Between sweeps the CTAs
 // meet at a grid-wide decision point (the last CTA to arrive sums the per-CTA
 // gains in fixed order, applies the stall rule — after the cross-GPU gain
@@ -449,12 +434,10 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
 // alternate direction so the tile a pair finished a sweep with is the one it
 // starts the next sweep with, already in shared memory.  Requires all CTAs to be
 // co-resident (cooperative launch, one CTA per SM).
-template <int RMAX, bool PROF = false, int SKIP = 0, bool PERSIST = false>
+template <int RMAX, bool PERSIST = false>
 __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   constexpr int NB = RMAX / 8;
   constexpr int KS = RMAX / 4;
-  const long long tk0 = PROF ? clock64() : 0;
-  long long pw[4] = {0, 0, 0, 0};
   if (sweep_skipped(a)) return;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[256 + 33];
@@ -508,7 +491,6 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
     const long ta = tq0 + (long)rd * cnt / rounds;
     const int nt = (int)(tq0 + (long)(rd + 1) * cnt / rounds - ta);
     const long col0 = ta * 8;
-    const long long tl0 = PROF ? clock64() : 0;
     // stage this round's 32 columns of H (zero outside r × N and past nt tiles);
     // persistent: the first round of a later sweep is still in shared memory
     nb_sync(idP);                           // previous round done with the tiles
@@ -526,14 +508,13 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
       asm volatile("cp.async.wait_all;\n" ::);
     }
     nb_sync(idP);
-    if (PROF) pw[1] += clock64() - tl0;
 
     if (producer) {
       switch (nt) {
-        case 4: ws_producer_round<KS, NB, 4, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
-        case 3: ws_producer_round<KS, NB, 3, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
-        case 2: ws_producer_round<KS, NB, 2, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
-        default: ws_producer_round<KS, NB, 1, PROF, SKIP>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw); break;
+        case 4: ws_producer_round<KS, NB, 4>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH); break;
+        case 3: ws_producer_round<KS, NB, 3>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH); break;
+        case 2: ws_producer_round<KS, NB, 2>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH); break;
+        default: ws_producer_round<KS, NB, 1>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH); break;
       }
     } else {
       // predicated loads / stores with running row pointers (no branches, no per-row 64-bit
@@ -568,10 +549,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
             gc[2 * j + 1] = v.y;
           }
         }
-        const long long c0 = PROF ? clock64() : 0;
         nb_sync(idS);
-        const long long c1 = PROF ? clock_after_smem(Ss + lane) : 0;
-        if (PROF) pw[0] += c1 - c0;
         double* hrow = Hs + 8 * b * 32;
         double x[8];
 #pragma unroll
@@ -583,7 +561,7 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
         }
         double hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < ((SKIP & 1) ? 0 : 8); ++i) {
+        for (int i = 0; i < 8; ++i) {
           const double h = pos_part_ws(bb[i]);
           hv[i] = h;
 #pragma unroll
@@ -594,7 +572,6 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
           gain = fma(__dmul_rn(u, gc[28 + i]), fma(-2.0, bb[i], v), gain);
         }
         if (b + 1 < NB) nb_arrive(idH);
-        if (PROF) pw[2] += clock64() - c1;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (valid && 8 * b + i < r) hp[i * ld] = hv[i];
@@ -608,364 +585,18 @@ __global__ void __launch_bounds__(256, 1) sweep_ws(Args a, long ntiles) {
   }
   if (!PERSIST) break;
   // ---- grid-wide end of sweep `sw`: stall rule on the total gain ----
-  const long long tg0 = PROF ? clock64() : 0;
   {
     const int cont = grid_decision(a, gain, nf, sw, first_total, red);
-    if (PROF) pw[3] += clock64() - tg0;
     if (!cont) break;
     gain = 0.0;
     nf = 0;
     src = a.H;
   }
-  }
-  if (PROF && lane == 0) {
-    double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 8;
-    o[0] = (double)pw[0];
-    o[1] = (double)pw[1];
-    o[2] = (double)(clock64() - tk0);
-    o[3] = (double)pw[2];
-    o[4] = (double)pw[3];
   }
   if (!PERSIST) {
     const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);
     nf = __syncthreads_or(nf);
     last_block_reduce_n<256>(a, bg, nf, red);
-  }
-}
-
-// The product warp's part of one round in sweep_t2 (left-looking with one block of look-ahead).
-// S_b = F_b + G[b, block b-1]·H_new[b-1]: F_b (every column block but b-1; the diagonal block's
-// strict upper triangle against the old rows of b) needs only blocks <= b-2 final, so it is
-// formed while the row warp still solves block b-1; after the hand-off only the 2·NT tail
-// DMMAs remain.  The row warp runs on another sub-partition, so the DMMA stream does not slow it.
-// shared-memory loads the compiler keeps in program order relative to the DMMAs (asm volatile):
-// without them it hoists every B fragment of the unrolled loop and runs out of registers
-ENMF_DEV double2 lds2_v(const double* p) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return v;
-}
-template <int NT>
-ENMF_DEV void t2_ldb(const double* Hs, int j, int gt, int bx0, int bx1, double2 (&p)[4]) {
-  const int k0 = 8 * j + gt, k1 = k0 + 4;
-  p[0] = lds2_v(Hs + k0 * 32 + bx0);
-  if (NT > 2) p[1] = lds2_v(Hs + k0 * 32 + bx1);
-  p[2] = lds2_v(Hs + k1 * 32 + bx0);
-  if (NT > 2) p[3] = lds2_v(Hs + k1 * 32 + bx1);
-}
-
-// acc[t] += a0 · B(k-step 2j) + a1 · B(k-step 2j+1) for the NT tiles, predicated on `on`
-// (uniform across the warp): a guarded DMMA instead of a branch around .aligned MMAs
-ENMF_DEV void dmma884_p(double& c0, double& c1, double a, double b, int on) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.s32 q, %4, 0;\n"
-               " @q mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n}\n"
-               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b), "r"(on));
-}
-// (k-step 2j into acc, 2j+1 into acc2: 2·NT independent accumulator chains)
-template <int NT>
-ENMF_DEV void ws_mma2_p(double (&acc)[4][2], double (&acc2)[4][2], double a0, double a1, const double2 (&p)[4],
-                        int on) {
-  dmma884_p(acc[0][0], acc[0][1], a0, p[0].x, on);
-  if (NT > 1) dmma884_p(acc[1][0], acc[1][1], a0, p[0].y, on);
-  if (NT > 2) dmma884_p(acc[2][0], acc[2][1], a0, p[1].x, on);
-  if (NT > 3) dmma884_p(acc[3][0], acc[3][1], a0, p[1].y, on);
-  dmma884_p(acc2[0][0], acc2[0][1], a1, p[2].x, on);
-  if (NT > 1) dmma884_p(acc2[1][0], acc2[1][1], a1, p[2].y, on);
-  if (NT > 2) dmma884_p(acc2[2][0], acc2[2][1], a1, p[3].x, on);
-  if (NT > 3) dmma884_p(acc2[3][0], acc2[3][1], a1, p[3].y, on);
-}
-
-// C_b in accumulator layout (row 8b + gi, columns t·8 + 2gt + e of the group), negated; zero
-// outside r rows / the group's valid columns
-template <int NT>
-ENMF_DEV void t2_ldc(const double* Cg, long ld, int row, int r, int ncols, int gt, double (&c)[4][2]) {
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int ct = t * 8 + 2 * gt + e;
-      c[t][e] = (t < NT && row < r && ct < ncols) ? -Cg[(long)row * ld + ct] : 0.0;
-    }
-}
-
-template <int KS, int NB, int NT, int SKIP = 0, bool PROF = false>
-ENMF_DEV void t2_producer_round(const double* Hs, double* Ss, const double2* gf, int gi, int gt, int bx0, int bx1,
-                                int idS, int idH, long long* pw, const double* Cg, long ld, int r, int ncols) {
-  double A[KS];
-#pragma unroll
-  for (int s = 0; s < KS; s += 2) {
-    const double2 f = gf[(s / 2) * 32];
-    A[s] = f.x;
-    A[s + 1] = f.y;
-  }
-  double cn[4][2];                           // -C of the next block (accumulator start)
-  t2_ldc<NT>(Cg, ld, gi, r, ncols, gt, cn);
-#pragma unroll 1
-  for (int b = 0; b < NB; ++b) {
-    const double2 tl = b > 0 ? gf[(b * KS / 2 + (b - 1)) * 32] : make_double2(0.0, 0.0);
-    // S'_b = G[b,:]·H - C_b accumulated from -C_b: the row warp takes bb = -S'_b
-    double acc[4][2], acc2[4][2];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      acc[t][0] = cn[t][0];
-      acc[t][1] = cn[t][1];
-      acc2[t][0] = acc2[t][1] = 0.0;
-    }
-    if (b + 1 < NB) t2_ldc<NT>(Cg, ld, 8 * (b + 1) + gi, r, ncols, gt, cn);
-    const long long c0 = PROF ? clock64() : 0;
-    // rolling prefetch: once fragment pair j of this block has gone into its DMMAs, its
-    // registers take pair j of the next block (a whole block of DMMAs to arrive)
-    double2 p[2][4];
-    t2_ldb<NT>(Hs, 0, gt, bx0, bx1, p[0]);
-#pragma unroll
-    for (int j = 0; j < KS / 2; ++j) {
-      if (j + 1 < KS / 2) t2_ldb<NT>(Hs, j + 1, gt, bx0, bx1, p[(j + 1) & 1]);
-      if (!(SKIP & 2)) ws_mma2_p<NT>(acc, acc2, A[2 * j], A[2 * j + 1], p[j & 1], j != b - 1);
-      if (b + 1 < NB) {
-        const double2 f = gf[((b + 1) * KS / 2 + j) * 32];
-        A[2 * j] = f.x;
-        A[2 * j + 1] = f.y;
-      }
-    }
-    const long long c1 = PROF ? clock64() : 0;
-    if (PROF) pw[3] += c1 - c0;
-    if (b > 0) {
-      bar_sync_n<128>(idH);                  // block b-1 solved: its new rows are in the tile
-      if (PROF) pw[0] += clock_after_smem(Ss) - c1;
-      double2 p[4];
-      t2_ldb<NT>(Hs, b - 1, gt, bx0, bx1, p);
-      ws_mma2_p<NT>(acc, acc2, tl.x, tl.y, p, 1);
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      acc[t][0] = __dadd_rn(acc[t][0], acc2[t][0]);
-      acc[t][1] = __dadd_rn(acc[t][1], acc2[t][1]);
-    }
-    ws_store_s(Ss, gi, gt, acc);
-    bar_arrive_n<128>(idS);                  // S'_b ready
-  }
-}
-
-// ---- two-team sweep: the row passes on their own sub-partition (default at large N) ----
-//
-// Scalar FP64 on an SM sub-partition whose DMMA pipe is streaming is starved (a dependent
-// chain runs 3-4x slower, profiles/r01_pipe_probe.txt), but scalar FP64 on a sub-partition
-// WITHOUT DMMA work is unaffected by DMMA streams on the other three
-// (tools/probe/xsmsp_probe.cu, profiles/r01_xsmsp_probe.txt).  sweep_ws must therefore
-// serialise each block's row pass with its DMMA products on one sub-partition (the DMMA
-// pipe idles during every row pass).  sweep_t2 splits the CTA into two TEAMS:
-//   * warps 0,1,2 / 4,5,6 (sub-partitions 0-2): product warps, one 32-column group each,
-//     the same paired block products as sweep_ws (ws_producer_round);
-//   * warp 3 / 7 (sub-partition 3): the team's row warp, three columns per lane (one per
-//     group of its team), all row passes on the DMMA-free sub-partition.
-// Each DMMA pipe is shared by two product warps of different teams: while one team's row
-// warp solves a block, the other team's product warp keeps the pipe busy.  The cost is
-// one sub-partition's DMMA pipe; the gain is that no row pass or hand-off sits between
-// DMMAs.  Gauss-Seidel order, the block products and the stall rule are sweep_ws's.
-constexpr int T2_GROUPS = 6;                 // 32-column groups per CTA (2 teams x 3)
-
-template <int RMAX>
-constexpr int t2_smem_bytes() {
-  return (T2_GROUPS * (RMAX * 32 + 8 * WS_SLD) + (RMAX / 8) * 48) * 8;
-}
-
-// SKIP (timing experiment, wrong results): 1 = row warps skip the block solve, 2 = product
-// warps skip the DMMAs
-// PROF (timing experiment): per-warp cycles [hand-off wait, tile load, total, F-loop / block
-// solve, grid decision] into a.terms
-template <int RMAX, int SKIP = 0, bool PROF = false>
-__global__ void __launch_bounds__(256, 1) sweep_t2(Args a, long ntiles) {
-  constexpr int NB = RMAX / 8;
-  constexpr int KS = RMAX / 4;
-  const long long tk0 = PROF ? clock64() : 0;
-  long long pw[5] = {0, 0, 0, 0, 0};
-  if (sweep_skipped(a)) return;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[256 + 33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int team = warp >> 2, wi = warp & 3;
-  const bool producer = wi < 3;
-  double* Gc = sm + T2_GROUPS * (RMAX * 32 + 8 * WS_SLD);
-  const int r = a.r;
-  for (int e = threadIdx.x; e < NB * 48; e += 256) {
-    const int b = e / 48, j = e % 48;
-    double v = 0.0;
-    if (j < 28) {
-      int l = 1;
-      while (l * (l + 1) / 2 <= j) ++l;
-      const int i = j - l * (l - 1) / 2, k = 8 * b + l, c = 8 * b + i;
-      v = (k < r && c < r) ? a.G[(long)k * r + c] : 0.0;
-    } else if (j < 44) {
-      const int k = 8 * b + ((j - 28) & 7);
-      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
-      v = j < 36 ? __dmul_rn(0.5, d) : __ddiv_rn(1.0, d);
-    }
-    Gc[e] = v;
-  }
-  __syncthreads();
-
-  const int idS = 1 + team, idH = 3 + team, idP = 5 + team;
-  // groups: q = 6·block + 3·team + j; a team's rounds follow its largest group
-  const long P = (long)gridDim.x * T2_GROUPS;
-  const long qt = (long)blockIdx.x * T2_GROUPS + 3 * team;
-  long tq0[3], cnt[3];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    tq0[j] = (qt + j) * ntiles / P;
-    cnt[j] = (qt + j + 1) * ntiles / P - tq0[j];
-  }
-  long cmax = 0;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) cmax = cnt[j] > cmax ? cnt[j] : cmax;
-  const int rounds = (int)((cmax + 3) / 4);
-  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
-  double gain = 0.0;
-  int nf = 0;
-  double first_total = 0.0;
-  const int gi = lane >> 2, gt = lane & 3;
-  const int swz = ((gt & 1) << 2) | (gt >> 1);
-  const int bx0 = 2 * ((2 * gi) ^ swz), bx1 = 2 * ((2 * gi + 1) ^ swz);
-  const double2* gf = reinterpret_cast<const double2*>(a.Gf) + lane;
-  int hoff[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) hoff[j] = ws_pos(j, lane) - j * 32;
-  double* Hs0 = sm + (3 * team) * (RMAX * 32);
-  double* Ss0 = sm + T2_GROUPS * RMAX * 32 + (3 * team) * 8 * WS_SLD;
-
-  for (int sw = 0;; ++sw) {
-    for (int i = 0; i < (rounds > 0 ? rounds : 1); ++i) {
-      const int rd = (sw & 1) ? rounds - 1 - i : i;
-      long ta[3];
-      int nt[3];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        ta[j] = rounds ? tq0[j] + (long)rd * cnt[j] / rounds : tq0[j];
-        nt[j] = rounds ? (int)(tq0[j] + (long)(rd + 1) * cnt[j] / rounds - ta[j]) : 0;
-      }
-      // stage the team's three 32-column tiles (zero outside r × N and past nt tiles); a later
-      // sweep's first round is still in shared memory
-      const long long tl0 = PROF ? clock64() : 0;
-      bar_sync_n<128>(idP);
-      if (!(sw > 0 && i == 0)) {
-#pragma unroll 1
-        for (int j = 0; j < 3; ++j) {
-          const int c = lane;
-          const long col = ta[j] * 8 + c;
-          const bool okc = c < nt[j] * 8 && col < a.N;
-          const double* sp = src + col;
-          double* Hs = Hs0 + j * (RMAX * 32);
-          for (int k = wi; k < RMAX; k += 4) {
-            const bool ok = okc && k < r;
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(Hs + ws_pos(k, c));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
-                         "l"(ok ? sp + (long)k * a.ld : src), "r"(ok ? 8 : 0));
-          }
-        }
-        asm volatile("cp.async.wait_all;\n" ::);
-      }
-      bar_sync_n<128>(idP);
-      if (PROF) pw[1] += clock_after_smem(Gc) - tl0;
-
-      if (producer) {
-        const double* Hs = Hs0 + wi * (RMAX * 32);
-        double* Ss = Ss0 + wi * 8 * WS_SLD;
-        const long col0 = ta[wi] * 8;
-        const int ncols = (int)max(0L, min((long)nt[wi] * 8, (long)a.N - col0));
-        const double* Cg = a.C + (ncols > 0 ? col0 : 0);
-        switch (nt[wi]) {
-          case 4: t2_producer_round<KS, NB, 4, SKIP, PROF>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw, Cg, a.ld, r, ncols); break;
-          case 3: t2_producer_round<KS, NB, 3, SKIP, PROF>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw, Cg, a.ld, r, ncols); break;
-          case 2: t2_producer_round<KS, NB, 2, SKIP, PROF>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw, Cg, a.ld, r, ncols); break;
-          default: t2_producer_round<KS, NB, 1, SKIP, PROF>(Hs, Ss, gf, gi, gt, bx0, bx1, idS, idH, pw, Cg, a.ld, r, ncols); break;
-        }
-      } else {
-        // row warp: lane = column `lane` of each of the team's three groups.  C is folded into
-        // the product (S' = G·H - C), the stores are predicated (no branches): invalid lanes
-        // store nothing; rows past r (padding of RMAX) are uniform.
-        bool vl[3];
-        double* hb[3];                         // H at row 8b of this lane's column
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const long col = ta[j] * 8 + lane;
-          vl[j] = lane < nt[j] * 8 && col < a.N;
-          hb[j] = a.H + (vl[j] ? col : 0);
-        }
-        const long ld = a.ld, ld8 = 8 * ld;
-        int hmax = 0;                           // high words of the stored h (>= 0): +inf is 0x7FF00000
-#pragma unroll 1
-        for (int b = 0; b < NB; ++b) {
-          double bb[3][8];
-          double gc[44];
-          {
-            const double2* gb = reinterpret_cast<const double2*>(Gc + b * 48);
-#pragma unroll
-            for (int j = 0; j < 22; ++j) {
-              const double2 v = gb[j];
-              gc[2 * j] = v.x;
-              gc[2 * j + 1] = v.y;
-            }
-          }
-          const long long r0 = PROF ? clock64() : 0;
-          bar_sync_n<128>(idS);                 // S_b of all three groups
-          const long long r1 = PROF ? clock_after_smem(Ss0 + lane) : 0;
-          if (PROF) pw[0] += r1 - r0;
-          double x[3][8];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const double* Ss = Ss0 + j * 8 * WS_SLD;
-            const double* hrow = Hs0 + j * (RMAX * 32) + 8 * b * 32;
-#pragma unroll
-            for (int i2 = 0; i2 < 8; ++i2) {
-              bb[j][i2] = -Ss[i2 * WS_SLD + lane];
-              x[j][i2] = hrow[i2 * 32 + hoff[i2 & 3]];
-            }
-          }
-          double hv[3][8] = {};
-#pragma unroll
-          for (int i2 = 0; i2 < ((SKIP & 1) ? 0 : 8); ++i2) {
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              double* hrow = Hs0 + j * (RMAX * 32) + 8 * b * 32;
-              const double t = __dmul_rn(bb[j][i2], gc[36 + i2]);
-              const double h = pos_part_ws(t);
-              hv[j][i2] = h;
-#pragma unroll
-              for (int l = i2 + 1; l < 8; ++l) bb[j][l] = fma(-gc[l * (l - 1) / 2 + i2], h, bb[j][l]);
-              hrow[i2 * 32 + hoff[i2 & 3]] = h;
-              const double u = __dsub_rn(x[j][i2], h), v = __dadd_rn(x[j][i2], h);
-              gain = fma(u, fma(gc[28 + i2], v, -bb[j][i2]), gain);
-            }
-          }
-          if (b + 1 < NB) bar_arrive_n<128>(idH);
-          if (PROF) pw[3] += clock64() - r1;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-#pragma unroll
-            for (int i2 = 0; i2 < 8; ++i2) {
-              if (vl[j] && 8 * b + i2 < r) hb[j][i2 * ld] = hv[j][i2];
-              hmax = max(hmax, __double2hiint(hv[j][i2]));
-            }
-            hb[j] += ld8;
-          }
-        }
-        nf |= hmax >= 0x7FF00000;
-      }
-    }
-    const long long tg0 = PROF ? clock64() : 0;
-    const int cont = grid_decision(a, gain, nf, sw, first_total, red);
-    if (PROF) pw[4] += clock64() - tg0;
-    if (!cont) break;
-    gain = 0.0;
-    nf = 0;
-    src = a.H;
-  }
-  if (PROF && lane == 0) {
-    double* o = a.terms + ((long)blockIdx.x * 8 + warp) * 8;
-    o[0] = (double)pw[0];
-    o[1] = (double)pw[1];
-    o[2] = (double)(clock64() - tk0);
-    o[3] = (double)pw[3];
-    o[4] = (double)pw[4];
   }
 }
 

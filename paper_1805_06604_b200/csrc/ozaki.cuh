@@ -132,9 +132,8 @@ __global__ void col_stats_final(const double* __restrict__ pmax, const double* _
 // by_row also adds the row's digit sums into sums[p·R + i] (zeroed by the caller).  Eight
 // consecutive elements per thread (K % 8 == 0, as the INT8 path requires 16-aligned shapes):
 // four 16-byte loads, one 8-byte store per digit plane.
-__global__ void split_x(const double* __restrict__ a, long R, long K, long lda, const int* __restrict__ e, int by_row,
-                        int8_t* __restrict__ out, int* __restrict__ sums) {
-  const long i = blockIdx.y;
+ENMF_DEV void split_x_row(const double* __restrict__ a, long i, long R, long K, long lda, const int* __restrict__ e,
+                         int by_row, int8_t* __restrict__ out, int* __restrict__ sums) {
   const double* row = a + i * lda;
   int8_t* o = out + i * K;
   const long dstride = R * K;
@@ -165,6 +164,11 @@ __global__ void split_x(const double* __restrict__ a, long R, long K, long lda, 
     for (int p = 0; p < SMAX; ++p) *reinterpret_cast<unsigned long long*>(o + p * dstride + k) = packed[p];
   }
   if (by_row) add_digit_sums(acc, sums + i, R);
+}
+// rows grid-strided over gridDim.y (≤ 65535)
+__global__ void split_x(const double* __restrict__ a, long R, long K, long lda, const int* __restrict__ e, int by_row,
+                        int8_t* __restrict__ out, int* __restrict__ sums) {
+  for (long i = blockIdx.y; i < R; i += gridDim.y) split_x_row(a, i, R, K, lda, e, by_row, out, sums);
 }
 
 // column sums of the SMAX digit planes of an R × K int8 matrix: sums[p·K + k] (zeroed by the

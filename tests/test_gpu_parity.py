@@ -579,33 +579,3 @@ def test_optimal_beta_linesearch_matches_reference():
         else:
             assert abs(got - beta) <= 1e-13 * abs(beta), (name, got, beta)
     ctx.close()
-
-
-@pytest.mark.gpu
-def test_two_team_sweep_variant_matches_oracle():
-    """The experimental two-team HALS sweep (ENMF_HALS_KERNEL=t2, hals.cuh::sweep_t2: row passes
-    on the DMMA-free sub-partition; profiles/r01_sweep_variants.md) is kept parity-tested: the
-    INT8-digit C5-like case through it, in a fresh process (the variant is read once per load)."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, paper_1805_06604_b200 as E\n"
-        "from oracle.oracle import Oracle, preset\n"
-        "port = Oracle('port'); m = n = 4096; r = 64\n"
-        "rng = np.random.default_rng(21)\n"
-        "x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))\n"
-        "w0, h0 = port.random_init(m, n, r, 22)\n"
-        "ref, wr, hr, _ = port.run_dense(x, w0, h0, preset('e-ahals-hp3', max_outer_iterations=4))\n"
-        "cfg = E.algorithm_config('e-ahals-hp3'); cfg.max_outer_iterations = 4\n"
-        "rec = E.Context(0).run(x, w0, h0, cfg, E.TimingMode.none)\n"
-        "assert np.array_equal(rec.column('restarted').astype(np.int32), ref['restarted'])\n"
-        "assert np.array_equal(rec.column('inner_h_count'), ref['inner_h'])\n"
-        "dev = np.max(np.abs(rec.column('error') - ref['error']) / ref['error'])\n"
-        "assert dev <= 1e-9, dev\n"
-        "assert np.max(np.abs(rec.factors.h - hr)) <= 1e-6 * np.max(np.abs(hr))\n"
-        "print('ok', dev)\n")
-    env = dict(os.environ, ENMF_HALS_KERNEL="t2")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
-                         timeout=600)
-    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr

@@ -194,3 +194,61 @@ def test_port_csr_vs_golden(port, golden, name):
     assert np.array_equal(rec["error"], g["error"])
     assert np.array_equal(rec["restarted"].astype(np.int32), g["restarted"].astype(np.int32))
     assert np.array_equal(w, g["w"]) and np.array_equal(h, g["h"]) and nx == float(g["norm_x"])
+
+
+# ------------------------------------------------ the multi-threaded replica (replica.c)
+def _replica(port, threads, fn):
+    old = port.threads
+    port.threads = threads
+    try:
+        return fn()
+    finally:
+        port.threads = old
+
+
+def _same(a, b, counts=False):
+    """Bitwise-equal runs; counts: also the sweep / BPP counts (the reference's IterationRecord has
+    none, engine.hpp:216-223 — oracle/_ref reports zeros)."""
+    keys = ("error", "beta", "restarted") + (("inner_h", "inner_w") if counts else ())
+    return (all(np.array_equal(a[0][k], b[0][k]) for k in keys)
+            and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3])
+
+
+@pytest.mark.parametrize("name", ["e-ahals-hp3", "e-ahals-hp1", "e-anls-hp1", "ahals"])
+def test_replica_bitwise_vs_reference_golden_c1(port, golden, name):
+    """The replica (oracle/replica.c, 4 threads) reproduces the reference's own C1 fixtures bit for bit."""
+    inp = golden.load("c1_inputs")
+    g = golden.load(f"c1_{name}")
+    rec, w, h, nx = _replica(port, 4, lambda: port.run_dense(inp["x"], inp["w0"], inp["h0"],
+                                                             preset(name, max_outer_iterations=200)))
+    assert np.array_equal(rec["error"], g["error"]) and np.array_equal(rec["beta"], g["beta"])
+    assert np.array_equal(w, g["w"]) and np.array_equal(h, g["h"]) and nx == float(g["norm_x"])
+
+
+@pytest.mark.parametrize("shape", [(301, 257, 17), (517, 1303, 72), (1000, 777, 33), (64, 1000, 5), (130, 70, 128)])
+def test_replica_bitwise_vs_reference(port, ref, shape):
+    """Ragged shapes (tails of every vector block, r > the column block) vs oracle/_ref, bitwise."""
+    m, n, r = shape
+    rng = np.random.default_rng(m)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, 3)
+    cfg = preset("e-ahals-hp3", max_outer_iterations=12)
+    assert _same(_replica(port, 8, lambda: port.run_dense(x, w0, h0, cfg)), ref.run_dense(x, w0, h0, cfg))
+
+
+def test_replica_bitwise_vs_port_thread_counts(port):
+    """Any thread count gives the single-threaded port's bits (C2-shaped case, 15 iterations)."""
+    x = port.gen_config(2, 2000, 300, 24, 1)
+    w0, h0 = port.random_init(2000, 300, 24, 2)
+    cfg = preset("e-ahals-hp3", max_outer_iterations=15)
+    base = port.run_dense(x, w0, h0, cfg)
+    for t in (2, 3, 8):
+        assert _same(_replica(port, t, lambda: port.run_dense(x, w0, h0, cfg)), base, counts=True), t
+
+
+def test_tiled_generator_thread_independent(port):
+    """orc_gen_tiled: per-tile streams, identical bits for any thread count and tile-aligned blocks."""
+    a = port.gen_tiled(700, 900, 8, 5, tile=256, threads=1)
+    b = port.gen_tiled(700, 900, 8, 5, tile=256, threads=7)
+    assert np.array_equal(a, b)
+    assert np.all(a > 0) and a.shape == (700, 900)
