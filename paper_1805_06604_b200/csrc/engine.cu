@@ -32,6 +32,7 @@
 #include "misc.cuh"
 #include "sparse.cuh"
 #include "ozaki.cuh"
+#include "ozk.cuh"
 #include "sweep_tf32.cuh"
 
 namespace {
@@ -106,8 +107,11 @@ struct enmf_gpu_ctx {
     const double* src = nullptr;
     long rows = 0, cols = 0;
     bool ready = false, by_row = false;
-    int levels = 6;                        // digit levels used (ozaki::combine's S)
+    int levels = 6;                        // digit levels used (ozk's S)
+    long N = 0, K = 0;                     // digit operand: N rows (output columns) × K contracted
+    CUtensorMap tmap;                      // TMA map of the chunked digits (box: 32 B × 64 rows × S × 1)
   } xd_xt, xd_x, xd_cols, xd_rows;          // one GPU: X scaled per row (T·Xᵀ) / per column (W_yᵀX)
+  DBuf<double> ozws;                       // ozk unit partials
   DBuf<int8_t> adig;
   DBuf<int> aexp, asum;
   DBuf<unsigned long long> amax;
@@ -811,33 +815,78 @@ void lt_gemm(enmf_gpu_ctx* c, cudaStream_t s, const void* A, const void* Xd, voi
                     lt->ws, lt->ws_size, s));
 }
 
-// Use the INT8-digit products for the dense single-GPU FP64 path when the problem is
-// large enough to pay the one-time digit cut of X and K keeps the int32 sums exact.
+// ---- INT8-digit products on the tcgen05 kernels (ozk.cuh) ---------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// TMA map of a chunked digit operand [Kp/32][SMAX][rows][32 B]: box = 32 B × box_rows × S digits × 1 chunk
+CUtensorMap digit_tmap(const int8_t* base, long rows, long K, int S, int box_rows) {
+  CUtensorMap m;
+  const long nkc = (K + ozk::KC - 1) / ozk::KC;
+  const cuuint64_t dim[4] = {(cuuint64_t)ozk::KC, (cuuint64_t)rows, (cuuint64_t)ozk::SMAX, (cuuint64_t)nkc};
+  const cuuint64_t stride[3] = {(cuuint64_t)ozk::KC, (cuuint64_t)(rows * ozk::KC),
+                                (cuuint64_t)(rows * ozk::KC * ozk::SMAX)};
+  const cuuint32_t box[4] = {(cuuint32_t)ozk::KC, (cuuint32_t)box_rows, (cuuint32_t)S, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dim, stride, box,
+                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+constexpr int kOzkBN = 64;
+
+// Work split of one digit product (K contracted, N output columns, R factor rows): chunks per
+// K unit (≤ 256, so the level sums stay exact in int32) chosen to give ≥ 2 units per SM.
+struct OzkPlan { int nkc, unit_chunks, nkq, nmb, ntn; };
+OzkPlan ozk_plan(const enmf_gpu_ctx* c, long K, long N, long R) {
+  OzkPlan p;
+  p.nkc = (int)((K + ozk::KC - 1) / ozk::KC);
+  p.nmb = (int)((R + 127) / 128);
+  p.ntn = (int)((N + kOzkBN - 1) / kOzkBN);
+  const long want = (long)p.nkc * p.ntn * p.nmb / (2L * c->sms);
+  p.unit_chunks = (int)std::max(1L, std::min<long>(ozk::UNIT_CHUNKS, want));
+  p.nkq = (p.nkc + p.unit_chunks - 1) / p.unit_chunks;
+  return p;
+}
+
+// Use the INT8-digit products for the dense FP64 path when the problem is large enough to pay
+// the one-time digit cut of X (any shape: TMA fills the ragged tile edges with zero digits).
 bool ozaki_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
   static int env = -1;
   if (env < 0) {
     const char* e = std::getenv("ENMF_CROSS");
     env = (e && std::string(e) == "dmma") ? 0 : 1;
   }
-  // (cuBLASLt's int8 kernels need 16-aligned leading dimensions: m, n and, when sharded, the
-  // rank's row / column block sizes multiples of 16)
   return env == 1 && prec == PREC_FAST && !c->sparse && (c->x || dist) &&
-         (double)c->m * (double)c->n >= (double)(1 << 24) && std::max(c->m, c->n) < 131072 &&
-         c->m % 16 == 0 && c->n % 16 == 0 && (!dist || (c->dist->mp % 16 == 0 && c->dist->np % 16 == 0)) &&
-         // split_x reads X with 16-byte loads: a borrowed X (load_device) need only be 8-byte aligned
-         (dist ? ((((uintptr_t)c->dist->xc) | (uintptr_t)c->dist->xr) & 15) == 0 : ((uintptr_t)c->x & 15) == 0);
+         (double)c->m * (double)c->n >= (double)(1 << 24);
 }
 
 // digits of an X operand (rows × cols, row-major): once per loaded X (outside the iteration graph).
 // by_row: one exponent per X row (the operand of T·Xᵀ, whose output columns are X's rows);
 // otherwise one per X column (W_yᵀX) — so the product's precision follows each output
-// column's own scale, not X's global maximum.
+// column's own scale, not X's global maximum.  Written in ozk's chunked K-major layout: the
+// digit operand has N = rows (by_row) or cols rows, each contracted over the other index.
 void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, const double* x, long rows,
                      long cols, bool by_row) {
   if (xd.ready && xd.src == x && xd.rows == rows && xd.cols == cols && xd.by_row == by_row) return;
-  const long mn = rows * cols;
-  xd.d.ensure((size_t)ozaki::SMAX * mn);
-  xd.e.ensure((size_t)(by_row ? rows : cols));
+  const long N = by_row ? rows : cols, K = by_row ? cols : rows;
+  const long Kp = (K + ozk::KC - 1) / ozk::KC * ozk::KC;
+  xd.d.ensure((size_t)ozk::SMAX * Kp * N);
+  xd.e.ensure((size_t)N);
   // digit levels: the neglected terms of level S scale with K·max|a|·max|b| / |sum a·b|; the
   // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
   // along it stands in for both operands: 6 levels up to 2.5, 7 up to 16, beyond that the
@@ -862,20 +911,21 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   CU(cudaStreamSynchronize(s));
   xd.levels = ratio <= 2.5 ? 6 : ratio <= 16.0 ? 7 : 0;
   c->launches += by_row ? 1 : 2;
-  const long nsum = by_row ? rows : cols;
-  xd.sums.ensure((size_t)ozaki::SMAX * nsum);
-  CU(cudaMemsetAsync(xd.sums.p, 0, (size_t)ozaki::SMAX * nsum * sizeof(int), s));
-  ozaki::split_x<<<dim3((unsigned)std::max<long>(1, std::min<long>((cols / 8 + 255) / 256, 8)),
-                      (unsigned)std::min<long>(rows, 65535)), 256,
-                    0, s>>>(x, rows, cols, cols, xd.e.p, by_row ? 1 : 0, xd.d.p, xd.sums.p);
+  xd.sums.ensure((size_t)ozk::SMAX * N);
+  CU(cudaMemsetAsync(xd.sums.p, 0, (size_t)ozk::SMAX * N * sizeof(int), s));
+  const long nkc = Kp / ozk::KC;
+  const unsigned groups = (unsigned)std::max<long>(1, std::min<long>(nkc, std::max<long>(1, 4L * c->sms * 256 / N)));
+  if (by_row)
+    ozk::split_rows_chunked<<<dim3((unsigned)((N + 127) / 128), groups), 128, 0, s>>>(x, rows, cols, cols, xd.e.p,
+                                                                                     nullptr, xd.d.p, xd.sums.p, nullptr);
+  else
+    ozk::split_cols_chunked<<<dim3((unsigned)((N + 127) / 128), groups), 128, 0, s>>>(x, rows, cols, cols, xd.e.p,
+                                                                                     xd.d.p, xd.sums.p);
   CUK();
   c->launches++;
-  if (!by_row) {                           // column sums of the digit planes (W_yᵀX contracts X's rows)
-    ozaki::digit_colsums<<<dim3((unsigned)((cols / 4 + 255) / 256), kChunks), 256, 0, s>>>(xd.d.p, rows, cols,
-                                                                                           kChunks, xd.sums.p);
-    CUK();
-    c->launches++;
-  }
+  xd.N = N;
+  xd.K = K;
+  if (xd.levels) xd.tmap = digit_tmap(xd.d.p, N, K, xd.levels, kOzkBN);
   xd.by_row = by_row;
   xd.src = x;
   xd.rows = rows;
@@ -883,56 +933,63 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   xd.ready = true;
 }
 
-// out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · (tn ? Xdᵀ : Xd) in FP64 accuracy,
-// Xd = the digit-cut operand (tn: N = rows, K = cols; !tn: K = rows, N = cols).  Returns false
-// (nothing enqueued) when X's dynamic range puts this product on the DMMA GEMM instead.
+template <int S>
+void ozk_launch(enmf_gpu_ctx* c, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb, const OzkPlan& p,
+                long R, long N, const DevState* st) {
+  using Cf = ozk::Cfg<S, kOzkBN>;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)ozk::gemm_levels<S, kOzkBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            Cf::SMEM));
+    attr = true;
+  }
+  ozk::GemmArgs g{(int)R, (int)N, p.nkc, p.unit_chunks, p.nkq, p.nmb, p.ntn, c->ozws.p, st};
+  const int units = p.nkq * p.nmb * p.ntn;
+  ozk::gemm_levels<S, kOzkBN><<<(unsigned)std::min(units, c->sms), ozk::THREADS, Cf::SMEM, s>>>(ta, tb, g);
+}
+
+// out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · Xdᵀ in FP64 accuracy, Xd = the
+// digit operand (N × K).  Returns false (nothing enqueued) when X's dynamic range puts this
+// product on the DMMA GEMM instead.
 bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
                  const DevState* st, const enmf_gpu_ctx::XDig& xd) {
-  const long K = tn ? xd.cols : xd.rows, N = tn ? xd.rows : xd.cols;
-  const long mn = xd.rows * xd.cols;
+  (void)tn;
   const int S = xd.levels;
   if (S == 0) return false;
-  c->adig.ensure((size_t)ozaki::SMAX * r * K);
-  c->aexp.ensure((size_t)r);
-  c->asum.ensure((size_t)ozaki::SMAX * r);
-  // digit GEMM q: factor digits p = 0..S-1-q stacked ((S-q)·r rows); cuBLASLt's int8 kernels
-  // are slow below 256 rows with an N-contiguous B, so short stacks are padded with further
-  // (unused) digits there
-  ozaki::Offsets off{};
-  int Mq[ozaki::SMAX];
-  long acc = 0;
-  for (int q = 0; q < S; ++q) {
-    Mq[q] = (S - q) * r;
-    if (!tn && Mq[q] < 256) Mq[q] = std::min(256, ozaki::SMAX * r);
-    off.q[q] = acc;
-    acc += (long)Mq[q] * N;
-  }
-  // one size for every product of this (m, n, r) — the largest stack layout (SMAX levels, short
-  // stacks padded to min(256, SMAX·r) rows) over the longest N: no reallocation between
-  // captured launches
-  size_t bound = 0;
-  for (int q = 0; q < ozaki::SMAX; ++q)
-    bound += (size_t)std::max((ozaki::SMAX - q) * r, std::min(256, ozaki::SMAX * r));
-  bound *= std::max(c->m, c->n);
-  c->ocbuf.ensure(std::max((size_t)acc, bound));
   if (!xd.ready) throw Fail{ENMF_CUDA_ERROR, "internal: X digits not prepared"};
+  const long K = xd.K, N = xd.N;
+  const OzkPlan p = ozk_plan(c, K, N, r);
+  // sized once for every product of this context's shapes: no reallocation between captured launches
+  {
+    const long mx = (long)std::max(c->m, c->n), mxp = (mx + ozk::KC - 1) / ozk::KC * ozk::KC;
+    c->adig.ensure((size_t)ozk::SMAX * mxp * r);
+    const long dm = c->dist ? (long)c->dist->mp : (long)c->m, dn = c->dist ? (long)c->dist->np : (long)c->n;
+    const OzkPlan p1 = ozk_plan(c, (long)c->m, dn, r), p2 = ozk_plan(c, (long)c->n, dm, r);
+    c->ozws.ensure(std::max({(size_t)p1.nkq * r * dn, (size_t)p2.nkq * r * dm, (size_t)p.nkq * r * N}));
+  }
+  c->aexp.ensure((size_t)r);
+  c->asum.ensure((size_t)ozk::SMAX * r);
   c->amax.ensure((size_t)r);
   CU(cudaMemsetAsync(c->amax.p, 0, (size_t)r * sizeof(unsigned long long), s));
-  CU(cudaMemsetAsync(c->asum.p, 0, (size_t)ozaki::SMAX * r * sizeof(int), s));
+  CU(cudaMemsetAsync(c->asum.p, 0, (size_t)ozk::SMAX * r * sizeof(int), s));
   const unsigned kb = (unsigned)std::max<long>(1, std::min<long>((K + 2047) / 2048, 64));
   ozaki::row_absmax<<<dim3(kb, r), 256, 0, s>>>(A, K, lda, c->amax.p, st);
-  ozaki::split_rows<<<dim3(kb, r), 256, 0, s>>>(A, r, K, lda, c->amax.p, c->aexp.p, c->adig.p, c->asum.p, st);
+  const long nkc = p.nkc;
+  const unsigned groups = (unsigned)std::max<long>(1, std::min<long>(nkc, 4L * c->sms * 128 / std::max(r, 1)));
+  ozk::split_rows_chunked<<<dim3((unsigned)((r + 127) / 128), groups), 128, 0, s>>>(A, r, K, lda, c->aexp.p, c->amax.p,
+                                                                                   c->adig.p, c->asum.p, st);
   CUK();
-  c->launches += 2;
-  for (int q = 0; q < S; ++q)
-    lt_gemm(c, s, c->adig.p, xd.d.p + q * mn, c->ocbuf.p + off.q[q], Mq[q], (int)N, (int)K, tn, 0);
-  const dim3 cg((unsigned)std::max<long>(1, std::min<long>((N + 255) / 256, 64)), (unsigned)r);
+  const CUtensorMap ta = digit_tmap(c->adig.p, r, K, S, 128);
+  if (S == 6) ozk_launch<6>(c, s, ta, xd.tmap, p, r, N, st);
+  else ozk_launch<7>(c, s, ta, xd.tmap, p, r, N, st);
+  CUK();
+  const dim3 fg((unsigned)std::max<long>(1, std::min<long>((N + 255) / 256, 64)), (unsigned)r);
   if (S == 6)
-    ozaki::combine<6><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
+    ozk::finish<6><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
   else
-    ozaki::combine<7><<<cg, 256, 0, s>>>(c->ocbuf.p, off, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
+    ozk::finish<7><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
   CUK();
-  c->launches += 1 + S;
+  c->launches += 4;
   return true;
 }
 

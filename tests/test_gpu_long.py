@@ -17,16 +17,19 @@ norms for C4/C5).
 """
 import json
 import os
+import sys
 
 import numpy as np
 import pytest
 
 import paper_1805_06604_b200 as E
-from tests.golden.make_golden_long import CONFIGS, factor_summary, inputs
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+sys.path.insert(0, GOLDEN)
+from make_golden_long import CONFIGS, factor_summary, inputs  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 REL_ERR_TOL = 1e-9
 FACTOR_TOL = 1e-6
 
