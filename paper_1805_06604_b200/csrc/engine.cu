@@ -109,7 +109,6 @@ struct enmf_gpu_ctx {
     bool ready = false, by_row = false;
     int levels = 6;                        // digit levels used (ozk's S)
     long N = 0, K = 0;                     // digit operand: N rows (output columns) × K contracted
-    CUtensorMap tmap;                      // TMA map of the chunked digits (box: 32 B × 64 rows × S × 1)
   } xd_xt, xd_x, xd_cols, xd_rows;          // one GPU: X scaled per row (T·Xᵀ) / per column (W_yᵀX)
   DBuf<double> ozws;                       // ozk unit partials
   DBuf<int8_t> adig;
@@ -816,38 +815,7 @@ void lt_gemm(enmf_gpu_ctx* c, cudaStream_t s, const void* A, const void* Xd, voi
 }
 
 // ---- INT8-digit products on the tcgen05 kernels (ozk.cuh) ---------------------------
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !f)
-      throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
-    return reinterpret_cast<EncodeTiledFn>(f);
-  }();
-  return fn;
-}
-
-// TMA map of a chunked digit operand [Kp/32][SMAX][rows][32 B]: box = 32 B × box_rows × S digits × 1 chunk
-CUtensorMap digit_tmap(const int8_t* base, long rows, long K, int S, int box_rows) {
-  CUtensorMap m;
-  const long nkc = (K + ozk::KC - 1) / ozk::KC;
-  const cuuint64_t dim[4] = {(cuuint64_t)ozk::KC, (cuuint64_t)rows, (cuuint64_t)ozk::SMAX, (cuuint64_t)nkc};
-  const cuuint64_t stride[3] = {(cuuint64_t)ozk::KC, (cuuint64_t)(rows * ozk::KC),
-                                (cuuint64_t)(rows * ozk::KC * ozk::SMAX)};
-  const cuuint32_t box[4] = {(cuuint32_t)ozk::KC, (cuuint32_t)box_rows, (cuuint32_t)S, 1};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dim, stride, box,
-                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
-  return m;
-}
-
-constexpr int kOzkBN = 64;
+constexpr int kOzkBN = 128;
 
 // Work split of one digit product (K contracted, N output columns, R factor rows): chunks per
 // K unit (≤ 256, so the level sums stay exact in int32) chosen to give ≥ 2 units per SM.
@@ -857,7 +825,7 @@ OzkPlan ozk_plan(const enmf_gpu_ctx* c, long K, long N, long R) {
   p.nkc = (int)((K + ozk::KC - 1) / ozk::KC);
   p.nmb = (int)((R + 127) / 128);
   p.ntn = (int)((N + kOzkBN - 1) / kOzkBN);
-  const long want = (long)p.nkc * p.ntn * p.nmb / (2L * c->sms);
+  const long want = (long)p.nkc * p.ntn * p.nmb / (4L * (c->sms / 2));   // ≥ ~4 units per cluster
   p.unit_chunks = (int)std::max(1L, std::min<long>(ozk::UNIT_CHUNKS, want));
   p.nkq = (p.nkc + p.unit_chunks - 1) / p.unit_chunks;
   return p;
@@ -884,8 +852,9 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
                      long cols, bool by_row) {
   if (xd.ready && xd.src == x && xd.rows == rows && xd.cols == cols && xd.by_row == by_row) return;
   const long N = by_row ? rows : cols, K = by_row ? cols : rows;
-  const long Kp = (K + ozk::KC - 1) / ozk::KC * ozk::KC;
-  xd.d.ensure((size_t)ozk::SMAX * Kp * N);
+  const long Kp = (K + ozk::KC - 1) / ozk::KC * ozk::KC, Np = (N + ozk::TROWS - 1) / ozk::TROWS * ozk::TROWS;
+  xd.d.ensure((size_t)ozk::SMAX * Kp * Np);
+  CU(cudaMemsetAsync(xd.d.p, 0, (size_t)ozk::SMAX * Kp * Np, s));   // padding rows stay zero digits
   xd.e.ensure((size_t)N);
   // digit levels: the neglected terms of level S scale with K·max|a|·max|b| / |sum a·b|; the
   // factor rows inherit X's scales along the contracted index, so X's own max/mean ratio
@@ -925,7 +894,6 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   c->launches++;
   xd.N = N;
   xd.K = K;
-  if (xd.levels) xd.tmap = digit_tmap(xd.d.p, N, K, xd.levels, kOzkBN);
   xd.by_row = by_row;
   xd.src = x;
   xd.rows = rows;
@@ -933,19 +901,69 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   xd.ready = true;
 }
 
-template <int S>
-void ozk_launch(enmf_gpu_ctx* c, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb, const OzkPlan& p,
-                long R, long N, const DevState* st) {
-  using Cf = ozk::Cfg<S, kOzkBN>;
+// ENMF_OZK selects how the digit pairs are split over a cluster: "c2" (default: two CTAs, the
+// levels split 11/10 at S = 6) or "c3" (three CTAs, 7/7/7).
+int ozk_cluster() {
+  static int v = [] {
+    const char* e = std::getenv("ENMF_OZK");
+    return (e && std::string(e) == "c3") ? 3 : 2;
+  }();
+  return v;
+}
+
+template <int S, int CL>
+void ozk_launch_v(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* B, const OzkPlan& p, long R, long N,
+                  const DevState* st) {
+  using Cf = ozk::Cfg<S, CL, kOzkBN>;
+  auto kern = ozk::gemm_levels<S, CL, kOzkBN>;
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)ozk::gemm_levels<S, kOzkBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            Cf::SMEM));
+    CU(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
     attr = true;
   }
-  ozk::GemmArgs g{(int)R, (int)N, p.nkc, p.unit_chunks, p.nkq, p.nmb, p.ntn, c->ozws.p, st};
-  const int units = p.nkq * p.nmb * p.ntn;
-  ozk::gemm_levels<S, kOzkBN><<<(unsigned)std::min(units, c->sms), ozk::THREADS, Cf::SMEM, s>>>(ta, tb, g);
+  ozk::GemmArgs g{A, B, (int)((R + ozk::TROWS - 1) / ozk::TROWS), (int)((N + ozk::TROWS - 1) / ozk::TROWS),
+                  (int)R, (int)N, p.nkc, p.unit_chunks, p.nkq, p.nmb, p.ntn, c->ozws.p, st};
+  const long items = (long)p.nkq * p.nmb * p.ntn;
+  cudaLaunchConfig_t lc = {};
+  // persistent grid: exactly the clusters that can be co-resident (the GPCs' shapes can leave
+  // fewer than sms / CL of them; one more would run as a second wave)
+  static int maxc = [&] {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3((unsigned)(c->sms / CL * CL));
+    q.blockDim = dim3(ozk::THREADS);
+    q.dynamicSmemBytes = Cf::SMEM;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = CL;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &q) != cudaSuccess || n <= 0) n = c->sms / CL;
+    if (std::getenv("ENMF_OZK_DEBUG")) std::fprintf(stderr, "ozk: cluster %d, %d co-resident clusters\n", CL, n);
+    return std::min(n, c->sms / CL);
+  }();
+  const int grid = (int)std::min<long>(items, maxc) * CL;
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(ozk::THREADS);
+  lc.dynamicSmemBytes = Cf::SMEM;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&lc, kern, g));
+}
+
+template <int S>
+void ozk_launch(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* B, const OzkPlan& p, long R, long N,
+                const DevState* st) {
+  if (ozk_cluster() == 3) ozk_launch_v<S, 3>(c, s, A, B, p, R, N, st);
+  else ozk_launch_v<S, 2>(c, s, A, B, p, R, N, st);
 }
 
 // out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · Xdᵀ in FP64 accuracy, Xd = the
@@ -962,10 +980,15 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   // sized once for every product of this context's shapes: no reallocation between captured launches
   {
     const long mx = (long)std::max(c->m, c->n), mxp = (mx + ozk::KC - 1) / ozk::KC * ozk::KC;
-    c->adig.ensure((size_t)ozk::SMAX * mxp * r);
+    const size_t an = (size_t)ozk::SMAX * mxp * ((r + ozk::TROWS - 1) / ozk::TROWS * ozk::TROWS);
+    if (c->adig.n < an) {                 // tile rows past r stay zero digits (split writes rows < r only)
+      c->adig.ensure(an);
+      CU(cudaMemsetAsync(c->adig.p, 0, an, s));
+    }
     const long dm = c->dist ? (long)c->dist->mp : (long)c->m, dn = c->dist ? (long)c->dist->np : (long)c->n;
     const OzkPlan p1 = ozk_plan(c, (long)c->m, dn, r), p2 = ozk_plan(c, (long)c->n, dm, r);
-    c->ozws.ensure(std::max({(size_t)p1.nkq * r * dn, (size_t)p2.nkq * r * dm, (size_t)p.nkq * r * N}));
+    c->ozws.ensure((size_t)ozk_cluster() *
+                   std::max({(size_t)p1.nkq * r * dn, (size_t)p2.nkq * r * dm, (size_t)p.nkq * r * N}));
   }
   c->aexp.ensure((size_t)r);
   c->asum.ensure((size_t)ozk::SMAX * r);
@@ -979,15 +1002,15 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
   ozk::split_rows_chunked<<<dim3((unsigned)((r + 127) / 128), groups), 128, 0, s>>>(A, r, K, lda, c->aexp.p, c->amax.p,
                                                                                    c->adig.p, c->asum.p, st);
   CUK();
-  const CUtensorMap ta = digit_tmap(c->adig.p, r, K, S, 128);
-  if (S == 6) ozk_launch<6>(c, s, ta, xd.tmap, p, r, N, st);
-  else ozk_launch<7>(c, s, ta, xd.tmap, p, r, N, st);
+  // the factor's box: all S digit tiles at once, or one digit tile per (multicast) load in a cluster
+  if (S == 6) ozk_launch<6>(c, s, c->adig.p, xd.d.p, p, r, N, st);
+  else ozk_launch<7>(c, s, c->adig.p, xd.d.p, p, r, N, st);
   CUK();
   const dim3 fg((unsigned)std::max<long>(1, std::min<long>((N + 255) / 256, 64)), (unsigned)r);
   if (S == 6)
-    ozk::finish<6><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
+    ozk::finish<6><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq * ozk_cluster(), r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
   else
-    ozk::finish<7><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq, r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
+    ozk::finish<7><<<fg, 256, 0, s>>>(c->ozws.p, p.nkq * ozk_cluster(), r, N, K, c->aexp.p, xd.e.p, c->asum.p, xd.sums.p, out, ldo, st);
   CUK();
   c->launches += 4;
   return true;
