@@ -14,7 +14,6 @@
 // GEMM writes its result straight into the r×m layout the sweep consumes;
 // H r×n as given.  W is transposed only at entry and exit.
 #include <cuda_runtime.h>
-#include <cublasLt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -33,6 +32,7 @@
 #include "sparse.cuh"
 #include "ozaki.cuh"
 #include "ozk.cuh"
+#include "tf32k.cuh"
 #include "sweep_tf32.cuh"
 
 namespace {
@@ -114,9 +114,7 @@ struct enmf_gpu_ctx {
   DBuf<int8_t> adig;
   DBuf<int> aexp, asum;
   DBuf<unsigned long long> amax;
-  DBuf<int> ocbuf;
   DBuf<double> opart;
-  void* lt = nullptr;                     // LtCache (cuBLASLt handle, workspace, per-shape plans)
   // TF32 variant: FP32 copy of X (once per load), FP32 factor / product staging
   bool xf_ready = false;
   DBuf<float> xf, af, cf;
@@ -732,88 +730,6 @@ void sparse_wx(enmf_gpu_ctx* c, cudaStream_t s, bool exact, const double* WyT, i
 // ---- FP64 cross products on INT8 tensor cores (ozaki.cuh) ----------------------
 // int8 × int8 → int32 digit GEMMs through cuBLASLt (plain library GEMMs); the
 // splitting and the FP64 recombination are ours.
-struct LtCache {
-  cublasLtHandle_t h = nullptr;
-  void* ws = nullptr;
-  size_t ws_size = 64u << 20;
-  struct Entry {
-    int M, N, K, tn, kind;           // kind 0: int8 → int32, 1: fp32 (TF32 tensor cores) → fp32
-    cublasLtMatmulDesc_t op;
-    cublasLtMatrixLayout_t la, lb, lc;
-    cublasLtMatmulAlgo_t algo;
-  };
-  std::vector<Entry> e;
-};
-
-#define LT(x)                                                                                           \
-  do {                                                                                                  \
-    cublasStatus_t st_ = (x);                                                                           \
-    if (st_ != CUBLAS_STATUS_SUCCESS) throw Fail{ENMF_CUDA_ERROR, std::string("cuBLASLt: ") + #x + " = " + \
-                                                                      std::to_string((int)st_)};       \
-  } while (0)
-
-void lt_free(enmf_gpu_ctx* c) {
-  auto* lt = static_cast<LtCache*>(c->lt);
-  if (!lt) return;
-  for (auto& e : lt->e) {
-    cublasLtMatrixLayoutDestroy(e.la); cublasLtMatrixLayoutDestroy(e.lb); cublasLtMatrixLayoutDestroy(e.lc);
-    cublasLtMatmulDescDestroy(e.op);
-  }
-  if (lt->ws) cudaFree(lt->ws);
-  if (lt->h) cublasLtDestroy(lt->h);
-  delete lt;
-  c->lt = nullptr;
-}
-
-// C (M×N int32, row-major) = A (M×K int8, row-major) · B, where B = Xdᵀ with Xd
-// N×K row-major (tn) or B = Xd with Xd K×N row-major (!tn).  Column-major call:
-// Cᵀ (N×M) = op(Xd') · Aᵀ.
-void lt_gemm(enmf_gpu_ctx* c, cudaStream_t s, const void* A, const void* Xd, void* C, int M, int N, int K, bool tn,
-             int kind) {
-  if (!c->lt) {
-    auto* nl = new LtCache();
-    c->lt = nl;
-    LT(cublasLtCreate(&nl->h));
-    CU(cudaMalloc(&nl->ws, nl->ws_size));
-  }
-  LtCache* lt = static_cast<LtCache*>(c->lt);
-  LtCache::Entry* en = nullptr;
-  for (auto& e : lt->e)
-    if (e.M == M && e.N == N && e.K == K && e.tn == (int)tn && e.kind == kind) en = &e;
-  if (!en) {
-    LtCache::Entry e{};
-    e.M = M; e.N = N; e.K = K; e.tn = tn; e.kind = kind;
-    const cudaDataType_t ab = kind ? CUDA_R_32F : CUDA_R_8I, cd = kind ? CUDA_R_32F : CUDA_R_32I;
-    if (kind) LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F));
-    else LT(cublasLtMatmulDescCreate(&e.op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
-    const cublasOperation_t ta = tn ? CUBLAS_OP_T : CUBLAS_OP_N, tb = CUBLAS_OP_N;
-    LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta));
-    LT(cublasLtMatmulDescSetAttribute(e.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb));
-    if (tn) LT(cublasLtMatrixLayoutCreate(&e.la, ab, K, N, K));
-    else LT(cublasLtMatrixLayoutCreate(&e.la, ab, N, K, N));
-    LT(cublasLtMatrixLayoutCreate(&e.lb, ab, K, M, K));
-    LT(cublasLtMatrixLayoutCreate(&e.lc, cd, N, M, N));
-    cublasLtMatmulPreference_t pref;
-    LT(cublasLtMatmulPreferenceCreate(&pref));
-    LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt->ws_size,
-                                            sizeof lt->ws_size));
-    cublasLtMatmulHeuristicResult_t res[1] = {};
-    int found = 0;
-    LT(cublasLtMatmulAlgoGetHeuristic(lt->h, e.op, e.la, e.lb, e.lc, e.lc, pref, 1, res, &found));
-    cublasLtMatmulPreferenceDestroy(pref);
-    if (!found) throw Fail{ENMF_CUDA_ERROR, "cuBLASLt: no algorithm for the cross-product GEMM"};
-    e.algo = res[0].algo;
-    lt->e.push_back(e);
-    en = &lt->e.back();
-  }
-  const int ialpha = 1, ibeta = 0;
-  const float falpha = 1.f, fbeta = 0.f;
-  const void* alpha = kind ? (const void*)&falpha : (const void*)&ialpha;
-  const void* beta = kind ? (const void*)&fbeta : (const void*)&ibeta;
-  LT(cublasLtMatmul(lt->h, en->op, alpha, Xd, en->la, A, en->lb, beta, C, en->lc, C, en->lc, &en->algo,
-                    lt->ws, lt->ws_size, s));
-}
-
 // ---- INT8-digit products on the tcgen05 kernels (ozk.cuh) ---------------------------
 constexpr int kOzkBN = 128;
 
@@ -1017,60 +933,71 @@ bool ozaki_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int
 }
 
 // ---- TF32 variant of the cross products (ENMF_PRECISION_TF32) -----------------
-// X is kept in FP32 (one copy per load), the factor rounded to FP32 per product, the
-// product on the TF32 tensor cores (cuBLASLt, FP32 accumulation) and widened to FP64;
-// everything else (Grams, sweeps, error, decisions) stays FP64.
-__global__ void to_f32(const double* __restrict__ in, long rows, long cols, long ld, float* __restrict__ out,
-                       const DevState* st) {
-  if (st && !dev_active(st)) return;
-  const long total = rows * cols;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const long r_ = i / cols, c_ = i - r_ * cols;
-    // round to the nearest TF32 value here: the tensor cores drop the low 13 bits of an FP32
-    // operand (a bias of half a TF32 ulp that the trace-identity error would amplify)
-    const float f = (float)in[r_ * ld + c_];
-    unsigned t;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(f));
-    out[i] = __uint_as_float(t);
-  }
-}
-__global__ void to_f64(const float* __restrict__ in, long rows, long cols, double* __restrict__ out, long ldo,
-                       const DevState* st) {
-  if (st && !dev_active(st)) return;
-  const long total = rows * cols;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const long r_ = i / cols, c_ = i - r_ * cols;
-    out[r_ * ldo + c_] = (double)in[i];
-  }
-}
-
+// X packed once per load into the TF32 tile images of both products (tf32k.cuh), the factor
+// per product; the products on the tcgen05 TF32 kernel (FP32 accumulation); everything else
+// (Grams, sweeps, error, decisions) stays FP64.
 bool tf32_enabled(const enmf_gpu_ctx* c, int prec, bool dist) {
   return prec == PREC_TF32 && !dist && !c->sparse && c->x;
 }
 
+size_t tf32_img_elems(long rows, long K, int RT) {
+  return (size_t)((K + tf32k::KE - 1) / tf32k::KE * tf32k::KE) * (size_t)((rows + RT - 1) / RT * RT);
+}
+
 void tf32_prepare_x(enmf_gpu_ctx* c, cudaStream_t s) {
   if (c->xf_ready) return;
-  const long mn = (long)c->m * (long)c->n;
-  c->xf.ensure((size_t)mn);
-  to_f32<<<(unsigned)std::min<long>((mn + 255) / 256, (long)c->sms * 64), 256, 0, s>>>(c->x, (long)c->m,
-                                                                                       (long)c->n, (long)c->n,
-                                                                                       c->xf.p, nullptr);
+  const long m = (long)c->m, n = (long)c->n;
+  const size_t er = tf32_img_elems(m, n, tf32k::BROWS), ec = tf32_img_elems(n, m, tf32k::BROWS);
+  c->xf.ensure(er + ec);                    // [rows image (N = m, K = n) | columns image (N = n, K = m)]
+  CU(cudaMemsetAsync(c->xf.p, 0, (er + ec) * sizeof(float), s));
+  const unsigned g = (unsigned)std::min<long>((m * n + 255) / 256, (long)c->sms * 64);
+  tf32k::pack_rows<<<g, 256, 0, s>>>(c->x, m, n, n, tf32k::BROWS, c->xf.p, nullptr);
+  tf32k::pack_cols<<<g, 256, 0, s>>>(c->x, m, n, tf32k::BROWS, c->xf.p + er);
   CUK();
-  c->launches++;
+  c->launches += 2;
   c->xf_ready = true;
 }
 
 void tf32_cross(enmf_gpu_ctx* c, cudaStream_t s, const double* A, long lda, int r, bool tn, double* out, long ldo,
                 const DevState* st) {
-  const long K = tn ? (long)c->n : (long)c->m, N = tn ? (long)c->m : (long)c->n;
-  c->af.ensure((size_t)r * std::max(c->m, c->n));
-  c->cf.ensure((size_t)r * std::max(c->m, c->n));
-  to_f32<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(A, r, K, lda,
-                                                                                                c->af.p, st);
+  const long m = (long)c->m, n = (long)c->n;
+  const long K = tn ? n : m, N = tn ? m : n;
+  const float* B = c->xf.p + (tn ? 0 : tf32_img_elems(m, n, tf32k::BROWS));
+  const size_t an = tf32_img_elems(r, std::max(m, n), tf32k::AROWS);
+  if (c->af.n < an) {                       // padding rows past r stay zero
+    c->af.ensure(an);
+    CU(cudaMemsetAsync(c->af.p, 0, an * sizeof(float), s));
+  }
+  tf32k::pack_rows<<<(unsigned)std::min<long>(((long)r * K + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
+      A, r, K, lda, tf32k::AROWS, c->af.p, st);
   CUK();
-  lt_gemm(c, s, c->af.p, c->xf.p, c->cf.p, r, (int)N, (int)K, tn, 1);
-  to_f64<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(c->cf.p, r, N, out,
-                                                                                                ldo, st);
+  tf32k::Args g{};
+  g.A = c->af.p; g.B = B;
+  g.nta = (r + tf32k::AROWS - 1) / tf32k::AROWS; g.ntb = (int)((N + tf32k::BROWS - 1) / tf32k::BROWS);
+  g.R = r; g.N = (int)N; g.nkc = (int)((K + tf32k::KE - 1) / tf32k::KE);
+  const long tiles = (long)g.nta * g.ntb;
+  g.nks = (int)std::max(1L, std::min<long>(g.nkc, (4L * c->sms + tiles - 1) / tiles));   // ≥ ~4 items per SM
+  g.split_chunks = (g.nkc + g.nks - 1) / g.nks;
+  g.nks = (g.nkc + g.split_chunks - 1) / g.split_chunks;
+  // partials sized once for both products (no reallocation between captured launches)
+  {
+    const long tl = (long)((std::max(m, n) + tf32k::BROWS - 1) / tf32k::BROWS) * g.nta;
+    const long nkcm = (std::max(m, n) + tf32k::KE - 1) / tf32k::KE;
+    const long ks = std::min<long>(nkcm, (4L * c->sms + tl - 1) / tl) + 1;
+    c->cf.ensure(std::max((size_t)g.nks * r * N, (size_t)ks * r * std::max(m, n)));
+  }
+  g.part = c->cf.p;
+  g.st = st;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)tf32k::gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, tf32k::SMEM));
+    attr = true;
+  }
+  const long items = (long)g.nks * tiles;
+  tf32k::gemm<<<(unsigned)std::min<long>(items, c->sms), tf32k::THREADS, tf32k::SMEM, s>>>(g);
+  CUK();
+  tf32k::finish<<<(unsigned)std::min<long>(((long)r * N + 255) / 256, (long)c->sms * 16), 256, 0, s>>>(
+      c->cf.p, g.nks, r, N, out, ldo, st);
   CUK();
   c->launches += 3;
 }
