@@ -2,27 +2,34 @@
 """bench.py — E-A-HALS outer iterations/s on the BASELINE.json headline config.
 
 Workload (BASELINE.json configs[4], "C5"): dense synthetic m = n = 32768,
-r = 128, X = W0·H0 + |N(0, 0.01²)| with W0, H0 ~ U[0,1), E-A-HALS hp = 3
-(beta0 .5, eta 1.5, gamma 1.01, gamma_bar 1.005), FP64.  One step = one outer
-iteration (engine.hpp:309-440) of the B200 path on HBM-resident data.
+r = 128, X = W0·H0 + |N(0, 0.01²)| with W0, H0 ~ U[0,1) (the tiled generator,
+csrc/io.cpp enmf_gen_tiled, seed 1), initial factors random_init(seed 2),
+E-A-HALS hp = 3 (beta0 .5, eta 1.5, gamma 1.01, gamma_bar 1.005), FP64.  One step
+= one outer iteration (engine.hpp:309-440).  The timed window is iterations
+1..K of that trajectory in every arm (the warm-up runs W iterations of the same
+problem beforehand and is discarded), so our arm, our end-to-end call and the
+reference arm do exactly the same work — the same iterations with the same
+inner sweep counts (tests/test_gpu_long.py pins the trajectory to the
+reference).
 
-Our arm prints one JSON line with value (device-timed it/s), e2e (the C-ABI
-enmf_gpu_run_dense call on pinned host buffers, copies included), roofline (the
-dominant FP64 DMMA GEMM, timed with CUDA events on the engine's stream),
-cpu_baseline (the reference's enmf::step on a bounded sample on the host
-cores), clocks and gpu_launches.
+Our arm prints one JSON line with value (device-timed it/s, HBM-resident X), e2e
+(the C-ABI enmf_gpu_run_dense call on pinned host buffers, copies included),
+roofline (the dominant kernel, timed with CUDA events on the engine's stream),
+cpu_baseline (the reference path on a bounded sample on the host cores), clocks
+and gpu_launches.
 
---impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified headers compiled in place; the C restatement if _ref is absent) on
-the host cores, same metric/config, each step a bounded sample.
+--impl reference: the reference's own CPU implementation of the path on all host
+cores — the bit-exact multi-threaded replica of enmf::run/step (oracle/replica.c,
+pinned bitwise to the unmodified reference, tests/test_oracle.py and
+tests/golden/golden_long.json "c5check") — on the same data, timing the same
+window of iterations 1..K.
 
 Multi-GPU (torchrun, N > 1): ONE C5 problem sharded over the ranks (SURVEY
 §8(e), paper_1805_06604_b200/dist.py): rank p holds X[:, J_p] and X[I_p, :] and
 the factor shards; the engine exchanges factor shards, r×r partials and one
 scalar per HALS sweep through CUDA-IPC peer memory (csrc/dist.cuh).  Strong
 scaling: value = K / (max over ranks of the device time of K iterations).
-X is defined tile-wise (4096² tiles, each from its own seeded generator) so
-every rank builds exactly its blocks of the same matrix.
+The tiled generator builds exactly each rank's blocks of the same matrix.
 """
 from __future__ import annotations
 
@@ -48,8 +55,11 @@ FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEAS
 # DRAM bytes per HALS sweep inside sweep_ws: ncu --set full of one 24-sweep launch,
 # dram__bytes_read.sum + dram__bytes_write.sum = 72.60 + 9.72 MB (profiles/r01_sweep_ncu.txt)
 SWEEP_DRAM_BYTES = (72.602368e6 + 9.718272e6) / 24
-INT8_PEAK_TOPS = 3216.0      # best cuBLASLt int8 GEMM measured on this pool's B200 (profiles/r01_int8_probe.txt)
-INT8_PEAK_SRC = "measured cuBLASLt int8 GEMM, M=1024 K=N=32768 (profiles/r01_int8_probe.txt); nominal dense 4500"
+# tcgen05 kind::i8 floor: 8192 MAC/cycle/SM (M=128 N≥128 MMAs at 100% in profiles/r02_umma_rate.txt)
+INT8_PEAK_TOPS = 2 * 8192 * 148 * 1.965e9 / 1e12
+INT8_PEAK_SRC = ("tcgen05 kind::i8 MMA floor measured on this pool's B200 (M=128, N>=128: 8192 MAC/cycle/SM, "
+                 "profiles/r02_umma_rate.txt) at the 1965 MHz max SM clock; nominal dense 4500")
+SEED_DATA, SEED_INIT = 1, 2
 
 
 def cfg_c5(iters):
@@ -117,72 +127,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-SAMPLE_L = 2048
-
-
-def _load_cpu(kind_pref="reference"):
-    from oracle.oracle import Oracle
-    try:
-        if kind_pref == "reference":
-            return Oracle("reference"), "reference"
-    except Exception:
-        pass
-    return Oracle("port"), "port"
-
-
-def cpu_reference_throughput(threads, steps_per_thread, seed=11):
-    """Runs the reference's enmf::step on SAMPLE_L² r=128 sub-problems of C5,
-    one independent problem per host thread (run_suite's parallelism,
-    bench.hpp:273-292), and converts to C5-equivalent outer it/s by the m·n
-    ratio (per-iteration cost ∝ m·n·r; at this sample size the HALS sweeps weigh
-    ~30% more than at C5, so the estimate is conservative for the CPU)."""
-    import ctypes as C
-    import numpy as np
-    from oracle.oracle import Config, preset
-    orc, kind = _load_cpu("reference")
-    fn = getattr(orc.lib, "ref_time_steps" if kind == "reference" else "orc_time_steps")
-    dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    fn.argtypes = [dp, C.c_size_t, C.c_size_t, dp, dp, C.c_size_t, C.POINTER(Config), C.c_size_t,
-                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
-    fn.restype = C.c_int
-    L = SAMPLE_L
-    cfg = preset("e-ahals-hp3", max_outer_iterations=steps_per_thread)
-    problems = []
-    for t in range(threads):
-        rng = np.random.default_rng(seed + t)
-        w0 = rng.random((L, R))
-        h0 = rng.random((R, L))
-        x = w0 @ h0 + 0.01 * np.abs(rng.standard_normal((L, L)))
-        wi, hi = rng.random((L, R)), rng.random((R, L))
-        problems.append((np.ascontiguousarray(x), wi, hi))
-    secs = [0.0] * threads
-    errs = [0] * threads
-
-    def work(i):
-        x, wi, hi = problems[i]
-        s = C.c_double()
-        e = C.c_double()
-        errs[i] = fn(x, L, L, wi, hi, R, C.byref(cfg), steps_per_thread, C.byref(s), C.byref(e))
-        secs[i] = s.value
-
-    t0 = time.perf_counter()
-    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    wall = time.perf_counter() - t0
-    if any(errs):
-        raise RuntimeError(f"reference CPU run failed: {errs}")
-    units = threads * steps_per_thread * (L * L) / (M * N)   # C5-equivalent outer iterations
-    span = max(secs)
-    return {"value": units / span, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": (f"{threads} thread(s) x {steps_per_thread} enmf::step on independent {L}x{L} r={R} "
-                       f"E-A-HALS hp3 sub-problems of C5 (1/{(M * N) // (L * L)} of its m·n); C5-equivalent it/s "
-                       f"= sample it/s x {L * L}/{M * N}"),
-            "seconds": span, "wall_seconds": wall}
-
-
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -190,61 +134,81 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def replica_window(threads, nskip, nsteps, world=1):
+    """The reference path (the bit-exact multi-threaded replica of enmf::run/step,
+    oracle/replica.c) on C5 itself: the seeded data, `nskip` untimed iterations, then `nsteps`
+    timed ones; returns it/s of the timed window and its inner sweep counts."""
+    import ctypes as C
+    import numpy as np
+    from oracle.oracle import Config, Iter, Oracle, preset
+    orc = Oracle("port")
+    fn = orc.lib.orc_time_window
+    dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+    fn.argtypes = [dp, C.c_size_t, C.c_size_t, dp, dp, C.c_size_t, C.POINTER(Config), C.c_size_t, C.c_size_t,
+                   C.POINTER(C.c_double), C.POINTER(Iter)]
+    fn.restype = C.c_int
+    x = orc.gen_tiled(M, N, R, SEED_DATA, threads=threads)
+    w0, h0 = orc.random_init(M, N, R, SEED_INIT)
+    cfg = preset("e-ahals-hp3", max_outer_iterations=nskip + nsteps)
+    recs = (Iter * max(nsteps, 1))()
+    sec = C.c_double()
+    orc.threads = threads
+    try:
+        rc = fn(x, M, N, w0, h0, R, C.byref(cfg), nskip, nsteps, C.byref(sec), recs)
+    finally:
+        orc.threads = 1
+    if rc:
+        raise RuntimeError(f"replica run failed: {rc}")
+    return {"value": nsteps / sec.value, "unit": UNIT, "cores": threads, "kind": "port",
+            "seconds": sec.value,
+            "sweeps_h": [recs[i].inner_h_count for i in range(nsteps)],
+            "sweeps_w": [recs[i].inner_w_count for i in range(nsteps)],
+            "last_relative_error": recs[nsteps - 1].relative_error if nsteps else None}
+
+
+REPLICA_NOTE = ("the bit-exact multi-threaded replica of the reference's enmf::run/step (oracle/replica.c: every "
+                "output element in the reference's summation order, OpenMP over independent elements; pinned bitwise "
+                "to the unmodified reference compiled from /root/reference — tests/test_oracle.py, and on C5 "
+                "iteration 1 in tests/golden/golden_long.json) — the reference itself is single-threaded "
+                "(SPEC.md:303) at ~370 s per C5 iteration")
+
+
 # --------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     threads = host_threads()
-    total_units = 0.0
-    total_sec = 0.0
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference_throughput(threads, 1, seed=100 + i)
-        if i >= args.warmup:
-            total_units += res["value"] * res["seconds"]
-            total_sec += res["seconds"]
-    value = total_units / total_sec
+    res = replica_window(threads, 0, args.steps)
+    value = res["value"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_sec / args.steps * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds"] / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_block(args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": res["kind"],
-                             "sample": res["sample"]},
+            "data": "synthetic (the seeded tiled C5 generator, the same matrix as our arm)",
+            "config": dict(config_block(args, world), window=f"outer iterations 1..{args.steps} of the seeded C5 run",
+                           host_threads=threads),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"C5 itself, outer iterations 1..{args.steps} (the window our arm times), "
+                                       f"on {threads} host threads: " + REPLICA_NOTE},
+            "sweeps": {"h": res["sweeps_h"], "w": res["sweeps_w"]},
+            "last_relative_error": res["last_relative_error"],
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------- our arm
-TILE = 4096
-
-
-def gen_factors(device, seed):
-    """W0 (m×r), H0 (r×n) of X and the initial factors Wi, Hi (full, same on every rank)."""
-    import torch
-    g = torch.Generator(device=device).manual_seed(seed)
-    w0 = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
-    h0 = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
-    wi = torch.rand(M, R, device=device, dtype=torch.float64, generator=g)
-    hi = torch.rand(R, N, device=device, dtype=torch.float64, generator=g)
-    return w0, h0, wi, hi
-
-
-def gen_block(w0, h0, r0, r1, c0, c1, seed):
-    """X[r0:r1, c0:c1] of X = W0·H0 + |N(0, 0.01²)|, the noise drawn per TILE² tile."""
-    import torch
-    dev = w0.device
-    out = torch.empty((r1 - r0, c1 - c0), device=dev, dtype=torch.float64)
-    for bi in range(r0 // TILE, (r1 + TILE - 1) // TILE):
-        for bj in range(c0 // TILE, (c1 + TILE - 1) // TILE):
-            g = torch.Generator(device=dev).manual_seed(seed * 1000003 + bi * 4099 + bj)
-            t = torch.randn(TILE, TILE, device=dev, dtype=torch.float64, generator=g)
-            i0, i1 = max(r0, bi * TILE), min(r1, (bi + 1) * TILE)
-            j0, j1 = max(c0, bj * TILE), min(c1, (bj + 1) * TILE)
-            blk = t[i0 - bi * TILE:i1 - bi * TILE, j0 - bj * TILE:j1 - bj * TILE].abs_().mul_(0.01)
-            blk.addmm_(w0[i0:i1], h0[:, j0:j1])
-            out[i0 - r0:i1 - r0, j0 - c0:j1 - c0] = blk
-            del t
-    return out
+def gen_data(rank, world):
+    """This rank's X block(s) (product generator, csrc/io.cpp enmf_gen_tiled — the oracle's
+    streams bit for bit) and initial factor shards, as host arrays."""
+    from paper_1805_06604_b200 import data as Dt
+    from paper_1805_06604_b200 import dist as D
+    wi, hi = Dt.random_init(M, N, R, SEED_INIT)
+    if world == 1:
+        return (Dt.gen_tiled(M, N, R, SEED_DATA),), wi, hi
+    r0, mp, c0, np_ = D.shard_bounds_py(M, N, rank, world)
+    xs = (Dt.gen_tiled(M, N, R, SEED_DATA, cols=slice(c0, c0 + np_)),
+          Dt.gen_tiled(M, N, R, SEED_DATA, rows=slice(r0, r0 + mp)))
+    return xs, wi[r0:r0 + mp].copy(), hi[:, c0:c0 + np_].copy()
 
 
 def direct_rel_error(x, w, h, rows=2048):
@@ -275,24 +239,21 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    seed = 1234
-    w0, h0, wi, hi = gen_factors(dev, seed)
-    r0, mp, c0, np_ = D.shard_bounds_py(M, N, rank, world)
-    if world == 1:
-        xs = (gen_block(w0, h0, 0, M, 0, N, seed),)
-        wi_s, hi_s = wi, hi
-    else:
-        xs = (gen_block(w0, h0, 0, M, c0, c0 + np_, seed), gen_block(w0, h0, r0, r0 + mp, 0, N, seed))
-        wi_s = wi[r0:r0 + mp].contiguous()
-        hi_s = hi[:, c0:c0 + np_].contiguous()
-    del w0, h0
+    xh_np, wi_np, hi_np = gen_data(rank, world)
+    xs = tuple(torch.from_numpy(x).to(dev) for x in xh_np)
+    wi_s, hi_s = torch.from_numpy(wi_np).to(dev), torch.from_numpy(hi_np).to(dev)
     torch.cuda.synchronize()
     exchange = D.torch_exchange() if world > 1 else None
     ctx = _make_context(E, D, local_rank, rank, world, xs, exchange)
-    prof_steps = 2
-    cfg = cfg_c5(args.warmup + args.steps + prof_steps)
-    ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg)
+    # warm-up: W iterations of the same problem, discarded; the timed window is iterations 1..K
+    # of a fresh begin (the window the reference arm and the end-to-end call time)
+    ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg_c5(args.warmup))
     ctx.step(args.warmup)
+    ctx.sync()
+    ctx.end()
+    prof_steps = 2
+    cfg = cfg_c5(args.steps + prof_steps)
+    ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg)
     ctx.sync()
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -316,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    timed = recs[args.warmup + 1: args.warmup + 1 + args.steps]
+    timed = recs[1: 1 + args.steps]
     sweeps_h = [r.inner_h_count for r in timed]
     sweeps_w = [r.inner_w_count for r in timed]
     # dominant kernel: FP64 DMMA GEMM, timed per phase with CUDA events on the engine stream
@@ -333,10 +294,15 @@ def run_ours(args, rank, world, local_rank):
     # products on TF32 tensor cores; reported next to the FP64 line, not as its value
     tf32 = None
     if world == 1 and not args.no_tf32:
-        cfg_t = cfg_c5(args.warmup + args.steps + prof_steps)
+        cfg_t = cfg_c5(args.warmup)
+        cfg_t.precision = E.Precision.tf32
+        ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg_t)   # warm-up (discarded)
+        ctx.step(args.warmup)
+        ctx.sync()
+        ctx.end()
+        cfg_t = cfg_c5(args.steps + prof_steps)
         cfg_t.precision = E.Precision.tf32
         ctx.begin_device(wi_s.data_ptr(), hi_s.data_ptr(), R, cfg_t)
-        ctx.step(args.warmup)
         ctx.sync()
         t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -382,10 +348,10 @@ def run_ours(args, rank, world, local_rank):
     # enmf_gpu_run_dense; sharded: load_sharded/begin/step/sync/end of this rank's blocks)
     e2e = None
     if not args.no_e2e:
-        pin = lambda t: torch.empty(t.shape, dtype=torch.float64, pin_memory=True).copy_(t)
-        xh = [pin(x) for x in xs]
-        wh, hh = pin(wi_s), pin(hi_s)
-        del xs
+        pin = lambda a: torch.empty(a.shape, dtype=torch.float64, pin_memory=True).copy_(torch.from_numpy(a))
+        xh = [pin(x) for x in xh_np]
+        wh, hh = pin(wi_np), pin(hi_np)
+        del xs, xh_np
         torch.cuda.empty_cache()
         cfg2 = cfg_c5(args.steps)
         if world == 1:
@@ -430,7 +396,13 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_throughput(min(host_threads(), args.cpu_threads), 1)
+            th = min(host_threads(), args.cpu_threads)
+            res = replica_window(th, 0, 1)
+            cpu = {"value": res["value"], "unit": UNIT, "cores": th, "kind": "port",
+                   "sample": ("C5 itself, outer iteration 1 only (bounded sample; its sweeps "
+                              f"{res['sweeps_h'][0]}+{res['sweeps_w'][0]} are fewer than a later iteration's), on "
+                              f"{th} host threads: " + REPLICA_NOTE + "; bench.py --impl reference times the full window"),
+                   "seconds": res["seconds"]}
         except Exception as ex:  # reported, never fatal for the GPU number
             cpu = {"error": str(ex)}
 
@@ -438,8 +410,10 @@ def run_ours(args, rank, world, local_rank):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": iter_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded torch generators on device, tile-wise)",
-                "config": config_block(args, world),
+                "data": "synthetic (the seeded tiled C5 generator, csrc/io.cpp enmf_gen_tiled)",
+                "config": dict(config_block(args, world),
+                               window=f"outer iterations 1..{args.steps} of the seeded C5 run (after a discarded "
+                                      f"{args.warmup}-iteration warm-up run)"),
                 "roofline": {"bound": "tensor",
                              "kernel": "hals::sweep_ws (persistent FP64 DMMA HALS sweeps, one launch per "
                                        "inner solve; 2·r²·N flop per sweep)",
@@ -450,10 +424,10 @@ def run_ours(args, rank, world, local_rank):
                                              "so it is far below the 2·r·N·8 B per sweep the iterate and C occupy",
                              "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
                              "cross_products": {
-                                 "kernel": "FP64-accurate W_yᵀX / X·Tᵀ: X and the factor cut into S 8-bit "
-                                           "digit planes, S int8 digit GEMMs (cuBLASLt) over S(S+1)/2 digit "
-                                           "pairs, exact rank-one offset corrections, truncation-bias "
-                                           "estimate, FP64 recombination (ozaki.cuh)",
+                                 "kernel": "FP64-accurate W_yᵀX / X·Tᵀ on the hand-written tcgen05 kind::i8 "
+                                           "kernel (ozk.cuh): S 8-bit digits per operand, the S(S+1)/2 digit "
+                                           "pairs summed per level in TMEM over CTA pairs, exact offset "
+                                           "corrections, truncation-bias estimate, FP64 recombination",
                                  "digit_levels": list(levels), "digit_products": digit_gemms,
                                  "ms": cross_ms, "fp64_equiv_tflops": cross_flops / (cross_ms * 1e-3) / 1e12,
                                  "int8_tops": (digit_gemms * cross_flops / (cross_ms * 1e-3) / 1e12

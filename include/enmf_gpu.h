@@ -271,6 +271,11 @@ int enmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* w, dou
 int enmf_lowrank_factors(size_t m, size_t n, size_t r, uint64_t seed, double* w, double* h);
 int enmf_gen_lowrank(size_t m, size_t n, size_t r, uint64_t seed, double* x);   /* X = W·H */
 int enmf_gen_fullrank(size_t m, size_t n, uint64_t seed, double* x);
+/* BASELINE configs[4] data on T×T tiles with per-tile streams (T = 0: 4096): the block rows
+ * [row0, row0+rows) × cols [col0, col0+cols) of X = W0·H0 + 0.01·|N(0,1)| (multi-threaded;
+ * identical bits for any thread count or blocking). */
+int enmf_gen_tiled(size_t m, size_t n, size_t r, uint64_t seed, size_t T, size_t row0, size_t rows, size_t col0,
+                   size_t cols, double* x);
 
 #ifdef __cplusplus
 }

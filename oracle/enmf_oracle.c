@@ -773,6 +773,46 @@ int orc_time_steps(const double* x, size_t m, size_t n, const double* w0, const 
   return rc;
 }
 
+/* run()'s prologue, `nskip` untimed step() calls, then `nsteps` timed ones: *seconds = the time
+ * inside those nsteps (the reference arm of bench.py times the same iteration window as the GPU
+ * arm); recs (nsteps entries) receive their records. */
+int orc_time_window(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                    const enmf_gpu_config* cfg, size_t nskip, size_t nsteps, double* seconds, enmf_gpu_iter* recs) {
+  int rc = orc_config_validate(cfg);
+  if (rc) return rc;
+  xmat X = {0, x, NULL, NULL, NULL, m, n, m * n};
+  const double nx2 = orc_frob_norm_sq(x, m * n);
+  ext_state st;
+  const size_t wsz = m * r, hsz = r * n;
+  double* buf = (double*)malloc(sizeof(double) * (3 * wsz + 3 * hsz + 4 * r * r + r * n + 5 * m * r));
+  st.w = buf; st.w_y = st.w + wsz; st.w_n = st.w_y + wsz;
+  st.h = st.w_n + wsz; st.h_y = st.h + hsz; st.h_n = st.h_y + hsz;
+  double* ws = st.h_n + hsz;
+  memcpy(st.w, w0, sizeof(double) * wsz); memcpy(st.w_y, w0, sizeof(double) * wsz);
+  memcpy(st.h, h0, sizeof(double) * hsz); memcpy(st.h_y, h0, sizeof(double) * hsz);
+  st.schedule.beta = cfg->beta0; st.schedule.beta_bar = 1.0; st.schedule.beta_prev = cfg->beta0;
+  st.schedule.gamma = cfg->gamma; st.schedule.gamma_bar = cfg->gamma_bar; st.schedule.eta = cfg->eta;
+  st.restarted = 0;
+  if (g_orc_threads > 1) rep_gram_rows(h0, r, n, ws);
+  else orc_gram_rows(h0, r, n, ws);
+  x_cross_xht(&X, h0, r, ws + r * r);
+  st.err_prev = orc_fast_error(nx2, w0, ws + r * r, ws, m, r);
+  enmf_gpu_iter rec;
+  memset(&rec, 0, sizeof rec);
+  uint64_t k = 1;
+  for (; k <= nskip && rc == ENMF_OK; ++k) rc = step(&X, nx2, &st, cfg, r, k, &rec, ws);
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (size_t i = 0; i < nsteps && rc == ENMF_OK; ++i, ++k) {
+    rc = step(&X, nx2, &st, cfg, r, k, &rec, ws);
+    if (recs) recs[i] = rec;
+  }
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+  free(buf);
+  return rc;
+}
+
 int orc_run_dense(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
                   const enmf_gpu_config* cfg, enmf_gpu_iter* iters, size_t iters_cap,
                   size_t* n_iters, double* w_out, double* h_out, double* norm_x) {

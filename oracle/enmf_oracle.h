@@ -81,6 +81,10 @@ int orc_run_csr(const uint64_t* off, const uint64_t* cidx, const double* vals, s
 int orc_time_steps(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
                    const enmf_gpu_config* cfg, size_t nsteps, double* seconds, double* last_rel_err);
 
+/* prologue + nskip untimed steps + nsteps timed steps (their records into recs) */
+int orc_time_window(const double* x, size_t m, size_t n, const double* w0, const double* h0, size_t r,
+                    const enmf_gpu_config* cfg, size_t nskip, size_t nsteps, double* seconds, enmf_gpu_iter* recs);
+
 /* BASELINE.json config generators (new; not in the reference) */
 int orc_gen_config(int which, size_t m, size_t n, size_t r, uint64_t seed, double* x);
 int orc_gen_docs(size_t m, size_t n, double zipf_s, uint64_t seed, uint64_t** off, uint64_t** cidx,

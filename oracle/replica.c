@@ -50,51 +50,60 @@ int orc_get_threads(void) { return g_orc_threads; }
 /* ------------------------------------------------------------- cross_wx */
 /* out (r×n) = wᵀx, linalg.hpp:67-83.  Per element the sum runs over i ascending from 0.0. */
 void rep_cross_wx(const double* w, const double* x, size_t m, size_t n, size_t r, double* out) {
-  const size_t JB = 64, IC = 256;
+  /* the x rows of a chunk sit n·8 bytes apart — the same L1 sets for every row — so each
+   * (row chunk, column block) is first copied into a contiguous per-thread buffer */
+  enum { JB = 64, IC = 64 };
   const size_t nblk = (n + JB - 1) / JB;
   memset(out, 0, sizeof(double) * r * n);
-#pragma omp parallel for schedule(dynamic, 1) num_threads(g_orc_threads)
-  for (size_t b = 0; b < nblk; ++b) {
-    const size_t j0 = b * JB, j1 = j0 + JB < n ? j0 + JB : n;
-    for (size_t i0 = 0; i0 < m; i0 += IC) {
-      const size_t i1 = i0 + IC < m ? i0 + IC : m;
-      size_t k = 0;
-      for (; k + 4 <= r; k += 4) {
-        size_t j = j0;
-        for (; j + 8 <= j1; j += 8) {
-          v4d a00 = v_load(out + (k + 0) * n + j), a01 = v_load(out + (k + 0) * n + j + 4);
-          v4d a10 = v_load(out + (k + 1) * n + j), a11 = v_load(out + (k + 1) * n + j + 4);
-          v4d a20 = v_load(out + (k + 2) * n + j), a21 = v_load(out + (k + 2) * n + j + 4);
-          v4d a30 = v_load(out + (k + 3) * n + j), a31 = v_load(out + (k + 3) * n + j + 4);
-          for (size_t i = i0; i < i1; ++i) {
-            const double* xi = x + i * n + j;
-            const double* wi = w + i * r + k;
-            const v4d x0 = v_load(xi), x1 = v_load(xi + 4);
-            v4d s;
-            s = v_bcast(wi[0]); a00 = a00 + s * x0; a01 = a01 + s * x1;
-            s = v_bcast(wi[1]); a10 = a10 + s * x0; a11 = a11 + s * x1;
-            s = v_bcast(wi[2]); a20 = a20 + s * x0; a21 = a21 + s * x1;
-            s = v_bcast(wi[3]); a30 = a30 + s * x0; a31 = a31 + s * x1;
+#pragma omp parallel num_threads(g_orc_threads)
+  {
+    double* xb = (double*)aligned_alloc(64, sizeof(double) * IC * JB);
+#pragma omp for schedule(dynamic, 1)
+    for (size_t b = 0; b < nblk; ++b) {
+      const size_t j0 = b * JB, j1 = j0 + JB < n ? j0 + JB : n, jw = j1 - j0;
+      for (size_t i0 = 0; i0 < m; i0 += IC) {
+        const size_t i1 = i0 + IC < m ? i0 + IC : m;
+        for (size_t i = i0; i < i1; ++i) memcpy(xb + (i - i0) * JB, x + i * n + j0, sizeof(double) * jw);
+        size_t k = 0;
+        for (; k + 4 <= r; k += 4) {
+          size_t j = 0;
+          for (; j + 8 <= jw; j += 8) {
+            double* o = out + j0 + j;
+            v4d a00 = v_load(o + (k + 0) * n), a01 = v_load(o + (k + 0) * n + 4);
+            v4d a10 = v_load(o + (k + 1) * n), a11 = v_load(o + (k + 1) * n + 4);
+            v4d a20 = v_load(o + (k + 2) * n), a21 = v_load(o + (k + 2) * n + 4);
+            v4d a30 = v_load(o + (k + 3) * n), a31 = v_load(o + (k + 3) * n + 4);
+            for (size_t i = i0; i < i1; ++i) {
+              const double* xi = xb + (i - i0) * JB + j;
+              const double* wi = w + i * r + k;
+              const v4d x0 = v_load(xi), x1 = v_load(xi + 4);
+              v4d s;
+              s = v_bcast(wi[0]); a00 = a00 + s * x0; a01 = a01 + s * x1;
+              s = v_bcast(wi[1]); a10 = a10 + s * x0; a11 = a11 + s * x1;
+              s = v_bcast(wi[2]); a20 = a20 + s * x0; a21 = a21 + s * x1;
+              s = v_bcast(wi[3]); a30 = a30 + s * x0; a31 = a31 + s * x1;
+            }
+            v_store(o + (k + 0) * n, a00); v_store(o + (k + 0) * n + 4, a01);
+            v_store(o + (k + 1) * n, a10); v_store(o + (k + 1) * n + 4, a11);
+            v_store(o + (k + 2) * n, a20); v_store(o + (k + 2) * n + 4, a21);
+            v_store(o + (k + 3) * n, a30); v_store(o + (k + 3) * n + 4, a31);
           }
-          v_store(out + (k + 0) * n + j, a00); v_store(out + (k + 0) * n + j + 4, a01);
-          v_store(out + (k + 1) * n + j, a10); v_store(out + (k + 1) * n + j + 4, a11);
-          v_store(out + (k + 2) * n + j, a20); v_store(out + (k + 2) * n + j + 4, a21);
-          v_store(out + (k + 3) * n + j, a30); v_store(out + (k + 3) * n + j + 4, a31);
+          for (; j < jw; ++j)
+            for (size_t kk = k; kk < k + 4; ++kk) {
+              double a = out[kk * n + j0 + j];
+              for (size_t i = i0; i < i1; ++i) a += w[i * r + kk] * xb[(i - i0) * JB + j];
+              out[kk * n + j0 + j] = a;
+            }
         }
-        for (; j < j1; ++j)
-          for (size_t kk = k; kk < k + 4; ++kk) {
-            double a = out[kk * n + j];
-            for (size_t i = i0; i < i1; ++i) a += w[i * r + kk] * x[i * n + j];
-            out[kk * n + j] = a;
+        for (; k < r; ++k)
+          for (size_t j = 0; j < jw; ++j) {
+            double a = out[k * n + j0 + j];
+            for (size_t i = i0; i < i1; ++i) a += w[i * r + k] * xb[(i - i0) * JB + j];
+            out[k * n + j0 + j] = a;
           }
       }
-      for (; k < r; ++k)
-        for (size_t j = j0; j < j1; ++j) {
-          double a = out[k * n + j];
-          for (size_t i = i0; i < i1; ++i) a += w[i * r + k] * x[i * n + j];
-          out[k * n + j] = a;
-        }
     }
+    free(xb);
   }
 }
 
@@ -212,54 +221,68 @@ int rep_hals_solve(const double* gram, const double* cross, const double* h0, si
     }
   if (h != h0) memcpy(h, h0, sizeof(double) * r * n);
   double* term = (double*)malloc(sizeof(double) * r * n);
+  /* (the local column-block copy holds r <= 128 rows; larger r sweeps h in place) */
   double* rowg = (double*)malloc(sizeof(double) * r);
-  const size_t CB = 128;
+  const size_t CB = 32;
   const size_t nblk = (n + CB - 1) / CB;
   double first_gain = 0.0;
   uint64_t sweep;
   for (sweep = 1;; ++sweep) {
-#pragma omp parallel for schedule(dynamic, 1) num_threads(g_orc_threads)
-    for (size_t b = 0; b < nblk; ++b) {
-      const size_t t0 = b * CB, t1 = t0 + CB < n ? t0 + CB : n;
-      double s[128];
-      for (size_t k = 0; k < r; ++k) {
-        const double gkk = gram[k * r + k];
-        const double* ck = cross + k * n;
-        size_t t = t0;
-        for (; t + 16 <= t1; t += 16) {
-          v4d a0 = v_load(ck + t), a1 = v_load(ck + t + 4), a2 = v_load(ck + t + 8), a3 = v_load(ck + t + 12);
-          for (size_t j = 0; j < r; ++j) {
-            if (j == k) continue;
-            const double gkj = gram[k * r + j];
-            if (gkj == 0.0) continue;
-            const double* hj = h + j * n + t;
-            const v4d g = v_bcast(gkj);
-            a0 = a0 - g * v_load(hj); a1 = a1 - g * v_load(hj + 4);
-            a2 = a2 - g * v_load(hj + 8); a3 = a3 - g * v_load(hj + 12);
+#pragma omp parallel num_threads(g_orc_threads)
+    {
+      /* the column block's rows of h sit n·8 bytes apart (the same L1 sets): the sweep runs on a
+       * contiguous copy hb[j][0..CB) and writes it back */
+      double hb[128 * 32];
+      double s[32];
+#pragma omp for schedule(dynamic, 1)
+      for (size_t b = 0; b < nblk; ++b) {
+        const size_t t0 = b * CB, t1 = t0 + CB < n ? t0 + CB : n, tw = t1 - t0;
+        const int local = r <= 128;
+        if (local)
+          for (size_t j = 0; j < r; ++j) memcpy(hb + j * CB, h + j * n + t0, sizeof(double) * tw);
+        for (size_t k = 0; k < r; ++k) {
+          const double gkk = gram[k * r + k];
+          const double* ck = cross + k * n + t0;
+          const double* hbase = local ? hb : h + t0;
+          const size_t hs = local ? CB : n;
+          size_t t = 0;
+          if (tw == 32) {
+            v4d a[8];
+            for (int u = 0; u < 8; ++u) a[u] = v_load(ck + 4 * u);
+            for (size_t j = 0; j < r; ++j) {
+              if (j == k) continue;
+              const double gkj = gram[k * r + j];
+              if (gkj == 0.0) continue;
+              const double* hj = hbase + j * hs;
+              const v4d g = v_bcast(gkj);
+              for (int u = 0; u < 8; ++u) a[u] = a[u] - g * v_load(hj + 4 * u);
+            }
+            for (int u = 0; u < 8; ++u) v_store(s + 4 * u, a[u]);
+            t = 32;
           }
-          v_store(s + (t - t0), a0); v_store(s + (t - t0) + 4, a1);
-          v_store(s + (t - t0) + 8, a2); v_store(s + (t - t0) + 12, a3);
-        }
-        for (; t < t1; ++t) {
-          double a = ck[t];
-          for (size_t j = 0; j < r; ++j) {
-            if (j == k) continue;
-            const double gkj = gram[k * r + j];
-            if (gkj == 0.0) continue;
-            a -= gkj * h[j * n + t];
+          for (; t < tw; ++t) {
+            double a = ck[t];
+            for (size_t j = 0; j < r; ++j) {
+              if (j == k) continue;
+              const double gkj = gram[k * r + j];
+              if (gkj == 0.0) continue;
+              a -= gkj * hbase[j * hs + t];
+            }
+            s[t] = a;
           }
-          s[t - t0] = a;
+          double* hk = (double*)hbase + k * hs;
+          double* tk = term + k * n + t0;
+          for (t = 0; t < tw; ++t) {
+            const double target = s[t] / gkk;
+            const double next = target > 0.0 ? target : 0.0;
+            const double d_old = hk[t] - target;
+            const double d_new = next - target;
+            tk[t] = d_old * d_old - d_new * d_new;
+            hk[t] = next;
+          }
         }
-        double* hk = h + k * n;
-        double* tk = term + k * n;
-        for (t = t0; t < t1; ++t) {
-          const double target = s[t - t0] / gkk;
-          const double next = target > 0.0 ? target : 0.0;
-          const double d_old = hk[t] - target;
-          const double d_new = next - target;
-          tk[t] = d_old * d_old - d_new * d_new;
-          hk[t] = next;
-        }
+        if (local)
+          for (size_t j = 0; j < r; ++j) memcpy(h + j * n + t0, hb + j * CB, sizeof(double) * tw);
       }
     }
 #pragma omp parallel for schedule(static) num_threads(g_orc_threads)

@@ -74,7 +74,7 @@ EXPORTS = [
     "enmf_io_matrix_offsets", "enmf_io_matrix_col_indices", "enmf_io_matrix_values",
     "enmf_io_matrix_free", "enmf_io_write_matrix_market", "enmf_io_write_dense_csv",
     "enmf_io_write_run_csv", "enmf_io_format_double", "enmf_mix_seed", "enmf_uniform_matrix",
-    "enmf_random_init", "enmf_lowrank_factors", "enmf_gen_lowrank", "enmf_gen_fullrank",
+    "enmf_random_init", "enmf_lowrank_factors", "enmf_gen_lowrank", "enmf_gen_fullrank", "enmf_gen_tiled",
 ]
 
 #: entry points that do not return an ENMF_* status
@@ -166,6 +166,7 @@ def load() -> C.CDLL:
     L.enmf_random_init.argtypes = [sz, sz, sz, C.c_uint64, dp, dp]
     L.enmf_lowrank_factors.argtypes = [sz, sz, sz, C.c_uint64, dp, dp]
     L.enmf_gen_lowrank.argtypes = [sz, sz, sz, C.c_uint64, dp]
+    L.enmf_gen_tiled.argtypes = [sz, sz, sz, C.c_uint64, sz, sz, sz, sz, sz, dp]
     L.enmf_gen_fullrank.argtypes = [sz, sz, C.c_uint64, dp]
     for name in EXPORTS:
         fn = getattr(L, name)

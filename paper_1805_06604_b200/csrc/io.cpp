@@ -715,4 +715,71 @@ int enmf_gen_lowrank(size_t m, size_t n, size_t r, uint64_t seed, double* x) {
 
 int enmf_gen_fullrank(size_t m, size_t n, uint64_t seed, double* x) { return enmf_uniform_matrix(m, n, seed, x); }
 
+// BASELINE configs[4] (C5) data, X = W0·H0 + 0.01·|N(0,1)| on T×T tiles with per-tile streams, so
+// any rank can build any block of the same matrix and the result is identical for any thread
+// count (the stream layout of oracle/replica.c orc_gen_tiled, which the tests pin bitwise):
+//   W0 row block bi: uniform, row-major, mt19937_64(mix_seed(seed, 1, bi));
+//   H0 column block bj: uniform, for k: for j in the block, mt19937_64(mix_seed(seed, 2, bj));
+//   X tile (bi, bj): Σ_k W0(i,k)·H0(k,j) (k ascending from 0.0) + 0.01·|Box–Muller normal|, one
+//   normal per entry row-major in the tile, mt19937_64(mix_seed(seed, 3, bi·nbj + bj)).
+// Writes the block rows [row0, row0+rows) × columns [col0, col0+cols) into x (row stride cols).
+int enmf_gen_tiled(size_t m, size_t n, size_t r, uint64_t seed, size_t T, size_t row0, size_t rows, size_t col0,
+                   size_t cols, double* x) {
+  return io_guard([&] {
+    if (!x) throw IoFail{ENMF_INVALID_ARGUMENT, "null argument", 0};
+    if (T == 0) T = 4096;
+    if (row0 + rows > m || col0 + cols > n || rows == 0 || cols == 0 || r == 0)
+      throw IoFail{ENMF_INVALID_ARGUMENT, "gen_tiled: block outside the matrix", 0};
+    const size_t nbj = (n + T - 1) / T;
+    const size_t bi0 = row0 / T, bi1 = (row0 + rows - 1) / T, bj0 = col0 / T, bj1 = (col0 + cols - 1) / T;
+    const size_t ni = bi1 - bi0 + 1, nj = bj1 - bj0 + 1;
+    std::vector<double> w(ni * T * r), h(r * nj * T);   // the W0 row blocks / H0 column blocks touched
+    parallel_for(std::min<size_t>(host_threads(), ni + nj), [&](size_t t) {
+      const size_t P = std::min<size_t>(host_threads(), ni + nj);
+      for (size_t q = t; q < ni + nj; q += P) {
+        if (q < ni) {
+          const size_t bi = bi0 + q, i1 = std::min(m, (bi + 1) * T);
+          std::mt19937_64 g(enmf_mix_seed(seed, 1, bi));
+          for (size_t i = bi * T; i < i1; ++i)
+            for (size_t k = 0; k < r; ++k) w[((i - bi0 * T)) * r + k] = static_cast<double>(g() >> 11) * 0x1.0p-53;
+        } else {
+          const size_t bj = bj0 + (q - ni), j1 = std::min(n, (bj + 1) * T);
+          std::mt19937_64 g(enmf_mix_seed(seed, 2, bj));
+          for (size_t k = 0; k < r; ++k)
+            for (size_t j = bj * T; j < j1; ++j) h[k * (nj * T) + (j - bj0 * T)] = static_cast<double>(g() >> 11) * 0x1.0p-53;
+        }
+      }
+    });
+    const size_t tiles = ni * nj, P = std::min<size_t>(host_threads(), tiles);
+    parallel_for(P, [&](size_t t) {
+      std::vector<double> rowbuf(T);
+      for (size_t q = t; q < tiles; q += P) {
+        const size_t bi = bi0 + q / nj, bj = bj0 + q % nj;
+        const size_t ti0 = bi * T, ti1 = std::min(m, ti0 + T), tj0 = bj * T, tj1 = std::min(n, tj0 + T);
+        std::mt19937_64 g(enmf_mix_seed(seed, 3, bi * nbj + bj));
+        auto unif = [&g] { return static_cast<double>(g() >> 11) * 0x1.0p-53; };
+        for (size_t i = ti0; i < ti1; ++i) {
+          const bool keep_row = i >= row0 && i < row0 + rows;
+          // the tile's normals are drawn row by row whether or not this block keeps the row
+          for (size_t j = tj0; j < tj1; ++j) {
+            const double u1 = unif(), u2 = unif();
+            rowbuf[j - tj0] = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(6.283185307179586 * u2);
+          }
+          if (!keep_row) continue;
+          const double* wi = w.data() + (i - bi0 * T) * r;
+          const size_t c0 = std::max(tj0, col0), c1 = std::min(tj1, col0 + cols);
+          double* xo = x + (i - row0) * cols - col0;
+          for (size_t j = c0; j < c1; ++j) xo[j] = 0.0;
+          for (size_t k = 0; k < r; ++k) {
+            const double a = wi[k];
+            const double* hk = h.data() + k * (nj * T) - bj0 * T;
+            for (size_t j = c0; j < c1; ++j) xo[j] += a * hk[j];
+          }
+          for (size_t j = c0; j < c1; ++j) xo[j] += 0.01 * std::fabs(rowbuf[j - tj0]);
+        }
+      }
+    });
+  });
+}
+
 }  // extern "C"

@@ -32,7 +32,7 @@ from .enmf import (InvalidArgument, IoError, ParseError, RunRecord, UnsupportedF
 __all__ = [
     "SparseMatrix", "ParseError", "UnsupportedFormat", "IoError", "format_double",
     "read_matrix_market", "write_matrix_market", "read_dense_csv", "write_dense_csv",
-    "write_run_csv", "mix_seed", "uniform_matrix", "lowrank_factors", "gen_lowrank",
+    "write_run_csv", "mix_seed", "uniform_matrix", "lowrank_factors", "gen_lowrank", "gen_tiled",
     "gen_fullrank", "random_init",
 ]
 
@@ -197,6 +197,16 @@ def gen_lowrank(m: int, n: int, r: int, seed: int) -> np.ndarray:
     """enmf::gen_lowrank (data.hpp:74-80): X = W·H, rounded as the reference's multiply."""
     x = np.empty((m, n)) if m and n else np.empty(0)
     _check(L.load().enmf_gen_lowrank(m, n, r, seed, x.ctypes.data))
+    return x
+
+
+def gen_tiled(m: int, n: int, r: int, seed: int, rows=None, cols=None, tile: int = 4096) -> np.ndarray:
+    """BASELINE configs[4] (C5) data, X = W0·H0 + 0.01·|N(0,1)| on tiles with per-tile streams
+    (csrc/io.cpp enmf_gen_tiled): the block rows × cols (slices; default the whole matrix)."""
+    r0, r1 = (0, m) if rows is None else (rows.start or 0, rows.stop if rows.stop is not None else m)
+    c0, c1 = (0, n) if cols is None else (cols.start or 0, cols.stop if cols.stop is not None else n)
+    x = np.empty((r1 - r0, c1 - c0))
+    _check(L.load().enmf_gen_tiled(m, n, r, seed, tile, r0, r1 - r0, c0, c1 - c0, x.ctypes.data))
     return x
 
 

@@ -252,3 +252,14 @@ def test_tiled_generator_thread_independent(port):
     b = port.gen_tiled(700, 900, 8, 5, tile=256, threads=7)
     assert np.array_equal(a, b)
     assert np.all(a > 0) and a.shape == (700, 900)
+
+
+def test_product_tiled_generator_matches_oracle(port):
+    """The product's C5 data generator (csrc/io.cpp enmf_gen_tiled, used by bench.py's GPU arm)
+    draws the oracle's streams bit for bit, whole matrix and rank blocks alike."""
+    from paper_1805_06604_b200 import data
+    m, n, r, T = 700, 900, 8, 256
+    full = port.gen_tiled(m, n, r, 5, tile=T, threads=3)
+    assert np.array_equal(data.gen_tiled(m, n, r, 5, tile=T), full)
+    assert np.array_equal(data.gen_tiled(m, n, r, 5, rows=slice(256, 700), tile=T), full[256:])
+    assert np.array_equal(data.gen_tiled(m, n, r, 5, cols=slice(100, 613), tile=T), full[:, 100:613])
