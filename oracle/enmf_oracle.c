@@ -334,15 +334,18 @@ static void cholesky_solve(const double* l, size_t f, double* b) {
  * are functions of the passive set alone, so solving each column on its own is
  * identical.  The exchange limit 3·r·n is a global count; it trips
  * iff the total exchange count exceeds it, independent of processing order. */
-int orc_active_set_solve(const double* gram, const double* cross, const double* h0, size_t r,
-                         size_t n, double* h, int32_t* rounds) {
+/* cmax_all / n_all: max|cross| and column count of the WHOLE problem when this call solves a
+ * shard of its columns (the sharded model, oracle/sharded_model.py); < 0 / 0 = this call's own. */
+int orc_active_set_solve_shard(const double* gram, const double* cross, const double* h0, size_t r, size_t n,
+                               double cmax_all, size_t n_all, double* h, int32_t* rounds, uint64_t* exch_out) {
   for (size_t i = 0; i < r * n; ++i)
     if (!isfinite(h0[i])) { set_err("active_set_solve: warm start must be finite"); return ENMF_INVALID_ARGUMENT; }
   double cmax = 0.0;
   for (size_t i = 0; i < r * n; ++i) cmax = (cmax < fabs(cross[i])) ? fabs(cross[i]) : cmax;
+  if (cmax_all >= 0.0) cmax = cmax_all;
   const double feas_tol = 1e-12 * (1.0 + cmax);
   const double pivot_floor = 1e-12 * max_diagonal(gram, r);
-  const uint64_t exchange_limit = 3ULL * r * n;
+  const uint64_t exchange_limit = 3ULL * r * (n_all ? n_all : n);
   uint64_t exchanges = 0;
   int32_t max_rounds = 0;
 
@@ -430,7 +433,21 @@ int orc_active_set_solve(const double* gram, const double* cross, const double* 
   free(passive); free(banned); free(fidx); free(infeas); free(cff); free(lfac);
   free(df); free(xf); free(resid);
   if (rounds) *rounds = max_rounds;
+  if (exch_out) *exch_out = exchanges;
   return rc;
+}
+
+/* active_set_solve, nnls.hpp:259-406 */
+int orc_active_set_solve(const double* gram, const double* cross, const double* h0, size_t r,
+                         size_t n, double* h, int32_t* rounds) {
+  return orc_active_set_solve_shard(gram, cross, h0, r, n, -1.0, 0, h, rounds, NULL);
+}
+
+/* `count` uniform_unit draws (rng.hpp:47-49) of mt19937_64(seed) — the reinit stream */
+void orc_uniform_stream(uint64_t seed, size_t count, double* out) {
+  orc_mt64 g;
+  orc_mt64_seed(&g, seed);
+  for (size_t i = 0; i < count; ++i) out[i] = orc_uniform_unit(&g);
 }
 
 /* --------------------------------------------------------------- engine.hpp */

@@ -61,6 +61,10 @@ int orc_hals_solve(const double* gram, const double* cross, const double* h0, si
 /* active_set_solve (nnls.hpp:259-406): returns ENMF_OK / ENMF_NO_CONVERGENCE. */
 int orc_active_set_solve(const double* gram, const double* cross, const double* h0, size_t r,
                          size_t n, double* h, int32_t* rounds);
+/* the same on a shard of the columns, with the whole problem's max|cross| and column count */
+int orc_active_set_solve_shard(const double* gram, const double* cross, const double* h0, size_t r, size_t n,
+                               double cmax_all, size_t n_all, double* h, int32_t* rounds, uint64_t* exch_out);
+void orc_uniform_stream(uint64_t seed, size_t count, double* out);
 uint64_t orc_derive_max_sweeps(double setup_flops, double sweep_flops, double ratio);  /* :79-87 */
 
 /* ---- engine.hpp ---- */

@@ -9,7 +9,14 @@ HALS sweep.  Sums are formed by all-gathering the partials and adding them in
 rank order, as the device mailbox does, so every rank takes the same
 decisions.  tests/test_dist_gloo.py runs it on 2 gloo ranks and checks it
 against the C oracle (engine.hpp:309-521 restated in oracle/enmf_oracle.c).
-HALS only (the inner solver of the headline config); no column reinit.
+
+Both inner solvers: HALS (stall rule on the all-reduced gain) and the exact
+BPP (per column on the rank's columns, with the WHOLE problem's max|cross| for
+the feasibility tolerance and its column count for the exchange limit —
+nnls.hpp:271-283 — the quantities the device exchanges in bpp_check_dist), and
+the dead-column reinit (engine.hpp:268-296): the Gram diagonal check on the
+all-reduced Gram, every rank drawing the full redraw stream of
+mt19937_64(mix_seed(seed, salt, attempt)) and keeping its own slice.
 """
 from __future__ import annotations
 
@@ -71,6 +78,64 @@ def hals(comm, G, Cm, H0, max_sweeps, stall):
             return H, sweeps
 
 
+def _orc():
+    from oracle.oracle import Oracle
+    return Oracle("port")
+
+
+def bpp(comm, G, Cm, H0, n_all):
+    """active_set_solve on this rank's columns with the global max|C| and column count."""
+    import ctypes as C
+    orc = _orc()
+    fn = orc.lib.orc_active_set_solve_shard
+    dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+    fn.argtypes = [dp, dp, dp, C.c_size_t, C.c_size_t, C.c_double, C.c_size_t, dp, C.POINTER(C.c_int32),
+                   C.POINTER(C.c_uint64)]
+    fn.restype = C.c_int
+    cmax = float(np.max(np.abs(Cm))) if Cm.size else 0.0
+    cmax = max(float(v[0]) for v in comm.gather(np.array([cmax])))
+    r, n = H0.shape
+    H = np.zeros((r, n))
+    rounds, exch = C.c_int32(), C.c_uint64()
+    rc = fn(np.ascontiguousarray(G), np.ascontiguousarray(Cm), np.ascontiguousarray(H0), r, n, cmax, n_all, H,
+            C.byref(rounds), C.byref(exch))
+    assert rc == 0, rc
+    total = int(comm.sum(np.array([float(exch.value)]))[0])
+    assert total <= 3 * r * n_all, "NoConvergence (exchange limit)"
+    return H
+
+
+def gram_with_reinit(comm, A, off, total, seed, salt, by_rows):
+    """engine.hpp:279-296 on a shard.  A: this rank's slice of the factor whose Gram is formed —
+    by_rows: W_y rows (A is mp × r, the columns of W_y have `total` = m entries); otherwise
+    T's columns (A is r × np, the rows of T have total = n entries).  Returns (G, A, redrawn)."""
+    orc = _orc()
+    import ctypes as C
+    orc.lib.orc_uniform_stream.argtypes = [C.c_uint64, C.c_size_t,
+                                           np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")]
+    r = A.shape[1] if by_rows else A.shape[0]
+    A = A.copy()
+    redrawn = False
+    for attempt in range(r + 4):
+        G = comm.sum(A.T @ A if by_rows else A @ A.T)
+        floor = 1e-16 * max(0.0, float(np.max(np.diag(G))))
+        bad = [k for k in range(r) if not (G[k, k] > floor)]
+        if not bad:
+            return G, A, redrawn
+        assert attempt <= r + 2, "NoConvergence (degenerate column persists)"
+        stream = np.empty(len(bad) * total)
+        orc.lib.orc_uniform_stream(orc.mix_seed(seed, salt, attempt), stream.size, stream)
+        cnt = A.shape[0] if by_rows else A.shape[1]
+        for q, k in enumerate(bad):
+            vals = stream[q * total + off: q * total + off + cnt]
+            if by_rows:
+                A[:, k] = vals
+            else:
+                A[k, :] = vals
+        redrawn = True
+    raise AssertionError("unreachable")
+
+
 def update_beta(s, dec):
     used = s["beta"]
     if dec:
@@ -83,9 +148,9 @@ def update_beta(s, dec):
 
 
 def run_sharded(comm, X, W0, H0, iters, hp=3, beta0=0.5, gamma=1.01, gamma_bar=1.005, eta=1.5, ratio=0.5,
-                stall=0.01, extrapolation=True):
-    """E-A-HALS run() on this rank's shards of the full X / W0 / H0 (only the
-    shards are read).  Returns (errors, restarted, W shard, H shard)."""
+                stall=0.01, extrapolation=True, inner_h="hals", inner_w="hals", reinit_seed=0, max_sweeps=0):
+    """run() (engine.hpp:447-521) on this rank's shards of the full X / W0 / H0 (only the shards
+    are read).  Returns (errors, restarted, W shard, H shard, ||X||, reinit events)."""
     m, n = X.shape
     r = W0.shape[1]
     p, P = comm.rank, comm.world
@@ -97,8 +162,8 @@ def run_sharded(comm, X, W0, H0, iters, hp=3, beta0=0.5, gamma=1.01, gamma_bar=1
     H = H0[:, c0:c0 + np_].copy()
     Wy, Hy = W.copy(), H.copy()
     setup = float(m) * float(n) * float(r)
-    ms_h = 1 + int(math.floor(ratio * setup / (float(n) * r * r)))
-    ms_w = 1 + int(math.floor(ratio * setup / (float(m) * r * r)))
+    ms_h = max_sweeps or 1 + int(math.floor(ratio * setup / (float(n) * r * r)))
+    ms_w = max_sweeps or 1 + int(math.floor(ratio * setup / (float(m) * r * r)))
     nx2 = float(comm.sum(np.array([np.sum(Xr * Xr)]))[0])
     nx = math.sqrt(nx2)
 
@@ -108,26 +173,37 @@ def run_sharded(comm, X, W0, H0, iters, hp=3, beta0=0.5, gamma=1.01, gamma_bar=1
         v = nx2 - 2.0 * dot + float(np.sum(gwn * GW))
         return math.sqrt(max(0.0, v))
 
+    def solve(kind, G, Cm, H0_, n_all, ms):
+        return bpp(comm, G, Cm, H0_, n_all) if kind == "exact" else hals(comm, G, Cm, H0_, ms, stall)[0]
+
     GW = comm.sum(H @ H.T)
     Hfull = np.concatenate(comm.gather(H), axis=1)
     e_prev = err(W, Xr @ Hfull.T, GW)
-    errors, restarted = [e_prev], [0]
+    errors, restarted, reinit = [e_prev], [0], [0]
     sch = dict(beta=beta0, beta_bar=1.0, beta_prev=beta0, gamma=gamma, gamma_bar=gamma_bar, eta=eta)
-    for _ in range(iters):
+    for k in range(1, iters + 1):
         beta = sch["beta"] if extrapolation else 0.0
+        ev = 0
+        GH, Wy, red = gram_with_reinit(comm, Wy, r0, m, reinit_seed, 2 * k, True)
+        ev |= 1 if red else 0
         Wyfull = np.concatenate(comm.gather(Wy), axis=0)
-        GH = comm.sum(Wy.T @ Wy)
         CH = Wyfull.T @ Xc
-        Hn, _ = hals(comm, GH, CH, Hy, ms_h, stall)
+        Hn = solve(inner_h, GH, CH, Hy, n, ms_h)
         if hp >= 2:
             Hy = Hn + beta * (Hn - H) if extrapolation else Hn.copy()
             if hp == 3:
                 Hy = np.where(Hy > 0.0, Hy, 0.0)
         T = Hy if hp >= 2 else Hn
+        GW, T, red = gram_with_reinit(comm, T, c0, n, reinit_seed, 2 * k + 1, False)
+        if red:
+            ev |= 2
+            if hp >= 2:
+                Hy = T
+            else:
+                Hn = T
         Tfull = np.concatenate(comm.gather(T), axis=1)
-        GW = comm.sum(T @ T.T)
         Pm = Xr @ Tfull.T
-        WnT, _ = hals(comm, GW, Pm.T.copy(), Wy.T.copy(), ms_w, stall)
+        WnT = solve(inner_w, GW, Pm.T.copy(), Wy.T.copy(), m, ms_w)
         Wn = WnT.T.copy()
         Wy = Wn + beta * (Wn - W) if extrapolation else Wn.copy()
         if hp == 1:
@@ -143,4 +219,5 @@ def run_sharded(comm, X, W0, H0, iters, hp=3, beta0=0.5, gamma=1.01, gamma_bar=1
             update_beta(sch, e <= e_prev)
         e_prev = e
         errors.append(e)
-    return np.array(errors), np.array(restarted), W, H, nx
+        reinit.append(ev)
+    return np.array(errors), np.array(restarted), W, H, nx, np.array(reinit)

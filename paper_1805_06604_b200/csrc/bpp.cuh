@@ -14,7 +14,9 @@
 //   refinement     nnls.hpp:349-359  (rows lane-parallel, sequential b-loop)
 //   feasibility    nnls.hpp:362-373  (lane-parallel, sequential a-loop)
 //   exchange rules nnls.hpp:384-400  (full flip / backup(3) / largest index)
-// Passive/banned/infeasible sets are 64-bit masks, so r <= 64.
+// Passive/banned/infeasible sets are bit masks of RM/64 64-bit words (Bits<W>), r <= RM <= 128;
+// at RM = 128 the per-warp factor is stored packed lower-triangular so G and L fit the
+// shared memory of one warp per block.
 #pragma once
 
 #include "common.cuh"
@@ -22,7 +24,43 @@
 
 namespace bpp {
 
-constexpr int MAXR = 64;
+constexpr int MAXR = 128;
+
+// fixed-size bit set over r <= 64·W indices
+template <int W>
+struct Bits {
+  unsigned long long w[W];
+  ENMF_DEV void clear() {
+#pragma unroll
+    for (int i = 0; i < W; ++i) w[i] = 0;
+  }
+  ENMF_DEV bool test(int i) const { return (w[i >> 6] >> (i & 63)) & 1ULL; }
+  ENMF_DEV void set(int i) { w[i >> 6] |= 1ULL << (i & 63); }
+  ENMF_DEV void reset(int i) { w[i >> 6] &= ~(1ULL << (i & 63)); }
+  ENMF_DEV void flip(int i) { w[i >> 6] ^= 1ULL << (i & 63); }
+  ENMF_DEV void xor_with(const Bits& o) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) w[i] ^= o.w[i];
+  }
+  ENMF_DEV bool any() const {
+    unsigned long long v = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) v |= w[i];
+    return v != 0;
+  }
+  ENMF_DEV int count() const {
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) c += __popcll(w[i]);
+    return c;
+  }
+  ENMF_DEV int highest() const {   // largest set index (any() must hold)
+#pragma unroll
+    for (int i = W - 1; i >= 0; --i)
+      if (w[i]) return 64 * i + 63 - __clzll(w[i]);
+    return -1;
+  }
+};
 
 struct Args {
   const double* G;        // r×r
@@ -39,17 +77,33 @@ struct Args {
   int* nonfinite;                 // set if a non-finite value is written
 };
 
+template <int RM>
+__host__ __device__ constexpr int l_elems() { return RM <= 64 ? RM * (RM + 1) : RM * (RM + 1) / 2; }   // L storage per warp
+
 template <int RM, int WPB>
 constexpr int smem_bytes() {
   // G (RM×(RM+1), odd row stride) + per warp: L (RM×(RM+1): the odd row stride keeps the
-  // lane-per-row loads of the factorization off one bank), x/d/res (3×RM), fidx (RM ints)
-  return RM * (RM + 1) * 8 + WPB * (RM * (RM + 1) * 8 + 3 * RM * 8 + RM * 4);
+  // lane-per-row loads of the factorization off one bank; packed triangle at RM = 128),
+  // x/d/res (3×RM), fidx (RM ints)
+  return RM * (RM + 1) * 8 + WPB * (l_elems<RM>() * 8 + 3 * RM * 8 + RM * 4);
 }
 
 ENMF_DEV unsigned long long warp_or64(unsigned long long v) {
   const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)(v & 0xffffffffULL));
   const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(v >> 32));
   return ((unsigned long long)hi << 32) | lo;
+}
+template <int W>
+ENMF_DEV Bits<W> warp_or(Bits<W> b) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) b.w[i] = warp_or64(b.w[i]);
+  return b;
+}
+template <int W>
+ENMF_DEV Bits<W> shfl0(Bits<W> b) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) b.w[i] = __shfl_sync(0xffffffffu, b.w[i], 0);
+  return b;
 }
 
 template <int RM, int WPB>
@@ -59,12 +113,16 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
   const int r = a.r;
   double* Gs = sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int W = (RM + 63) / 64;
   constexpr int LDL = RM + 1;             // row stride of L (bank spread for lane-per-row access)
-  double* L = sm + RM * LDL + warp * (RM * LDL + 3 * RM);
-  double* xf = L + RM * LDL;
+  constexpr int LE = l_elems<RM>();
+  // L(i, p), p <= i: strided rows, or the packed lower triangle at RM = 128
+  auto LI = [](int i, int p) { return RM <= 64 ? i * LDL + p : i * (i + 1) / 2 + p; };
+  double* L = sm + RM * LDL + warp * (LE + 3 * RM);
+  double* xf = L + LE;
   double* df = xf + RM;
   double* rs = df + RM;
-  int* fidx = reinterpret_cast<int*>(sm + RM * LDL + WPB * (RM * LDL + 3 * RM)) + warp * RM;
+  int* fidx = reinterpret_cast<int*>(sm + RM * LDL + WPB * (LE + 3 * RM)) + warp * RM;
 
   const int gld = r | 1;                   // odd row stride of the Gram copy (bank spread)
   for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
@@ -77,10 +135,12 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
   const unsigned long long limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
 
   for (int col = blockIdx.x * WPB + warp; col < a.N; col += gridDim.x * WPB) {
-    unsigned long long P = 0, B = 0;
+    Bits<W> P, B;
+    P.clear();
+    B.clear();
     for (int i = lane; i < r; i += 32)
-      if (a.H0[(long)i * a.ld + col] > 0.0) P |= 1ULL << i;
-    P = warp_or64(P);
+      if (a.H0[(long)i * a.ld + col] > 0.0) P.set(i);
+    P = warp_or(P);
     int best_inf = 0x7fffffff, backup = 3, solves = 0;
     unsigned long long exch = 0;
     int f = 0;
@@ -90,7 +150,7 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
       f = 0;
       if (lane == 0)
         for (int i = 0; i < r; ++i)
-          if ((P >> i) & 1ULL) fidx[f++] = i;
+          if (P.test(i)) fidx[f++] = i;
       f = __shfl_sync(0xffffffffu, f, 0);
       __syncwarp();
       // factor G[F,F], dropping and banning variables whose pivot collapses
@@ -102,11 +162,11 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
           int ok = 1;
           if (lane == 0) {
             double d = Gs[fidx[j] * gld + fidx[j]];
-            for (int p = 0; p < j; ++p) d = __dsub_rn(d, __dmul_rn(L[j * LDL + p], L[j * LDL + p]));
+            for (int p = 0; p < j; ++p) d = __dsub_rn(d, __dmul_rn(L[LI(j, p)], L[LI(j, p)]));
             ok = (d > pivot_floor) ? 1 : 0;
             if (ok) {
               ljj = __dsqrt_rn(d);
-              L[j * LDL + j] = ljj;
+              L[LI(j, j)] = ljj;
             }
           }
           ok = __shfl_sync(0xffffffffu, ok, 0);
@@ -115,20 +175,20 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
           __syncwarp();
           for (int i = j + 1 + lane; i < f; i += 32) {
             double s = Gs[fidx[i] * gld + fidx[j]];
-            for (int p = 0; p < j; ++p) s = __dsub_rn(s, __dmul_rn(L[i * LDL + p], L[j * LDL + p]));
-            L[i * LDL + j] = __ddiv_rn(s, ljj);
+            for (int p = 0; p < j; ++p) s = __dsub_rn(s, __dmul_rn(L[LI(i, p)], L[LI(j, p)]));
+            L[LI(i, j)] = __ddiv_rn(s, ljj);
           }
           __syncwarp();
         }
         if (bad == f) break;
         if (lane == 0) {
           const int var = fidx[bad];
-          P &= ~(1ULL << var);
-          B |= 1ULL << var;
+          P.reset(var);
+          B.set(var);
           for (int q = bad; q + 1 < f; ++q) fidx[q] = fidx[q + 1];
         }
-        P = __shfl_sync(0xffffffffu, P, 0);
-        B = __shfl_sync(0xffffffffu, B, 0);
+        P = shfl0(P);
+        B = shfl0(B);
         --f;
         __syncwarp();
       }
@@ -139,13 +199,13 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
         if (lane == 0) {
           for (int i = 0; i < f; ++i) {
             double s = b[i];
-            for (int p = 0; p < i; ++p) s = __dsub_rn(s, __dmul_rn(L[i * LDL + p], b[p]));
-            b[i] = __ddiv_rn(s, L[i * LDL + i]);
+            for (int p = 0; p < i; ++p) s = __dsub_rn(s, __dmul_rn(L[LI(i, p)], b[p]));
+            b[i] = __ddiv_rn(s, L[LI(i, i)]);
           }
           for (int ii = f - 1; ii >= 0; --ii) {
             double s = b[ii];
-            for (int p = ii + 1; p < f; ++p) s = __dsub_rn(s, __dmul_rn(L[p * LDL + ii], b[p]));
-            b[ii] = __ddiv_rn(s, L[ii * LDL + ii]);
+            for (int p = ii + 1; p < f; ++p) s = __dsub_rn(s, __dmul_rn(L[LI(p, ii)], b[p]));
+            b[ii] = __ddiv_rn(s, L[LI(ii, ii)]);
           }
         }
         __syncwarp();
@@ -165,28 +225,29 @@ __global__ void __launch_bounds__(WPB * 32) solve(Args a) {
         __syncwarp();
       }
       // infeasible set
-      unsigned long long I = 0;
+      Bits<W> I;
+      I.clear();
       for (int q = lane; q < f; q += 32)
-        if (xf[q] < -feas_tol) I |= 1ULL << fidx[q];
+        if (xf[q] < -feas_tol) I.set(fidx[q]);
       for (int i = lane; i < r; i += 32) {
-        if (((P | B) >> i) & 1ULL) continue;
+        if (P.test(i) || B.test(i)) continue;
         double y = -a.C[(long)i * a.ld + col];
         for (int q = 0; q < f; ++q) y = __dadd_rn(y, __dmul_rn(Gs[i * gld + fidx[q]], xf[q]));
-        if (y < -feas_tol) I |= 1ULL << i;
+        if (y < -feas_tol) I.set(i);
       }
-      I = warp_or64(I);
-      if (I == 0) break;
+      I = warp_or(I);
+      if (!I.any()) break;
       if (++exch > limit) break;  // the total exceeds the global limit too
-      const int count = __popcll(I);
+      const int count = I.count();
       if (count < best_inf) {
         best_inf = count;
         backup = 3;
-        P ^= I;
+        P.xor_with(I);
       } else if (backup > 0) {
         --backup;
-        P ^= I;
+        P.xor_with(I);
       } else {
-        P ^= 1ULL << (63 - __clzll(I));
+        P.flip(I.highest());
       }
     }
     // write the column: max(x, 0) on F, zero elsewhere

@@ -214,6 +214,7 @@ void set_attrs_once() {
   big((const void*)bpp::solve<32, 8>, bpp::smem_bytes<32, 8>());
   big((const void*)bpp::solve_fast<8>, bpp::fast_smem_bytes<8>());
   big((const void*)bpp::solve<64, 4>, bpp::smem_bytes<64, 4>());
+  big((const void*)bpp::solve<128, 1>, bpp::smem_bytes<128, 1>());
   done = true;
 }
 
@@ -491,8 +492,10 @@ void bpp_launch(enmf_gpu_ctx* c, cudaStream_t s, const bpp::Args& a, const dist:
     bpp::solve_fast<8><<<(a.N + 7) / 8, 256, bpp::fast_smem_bytes<8>(), s>>>(a);
   } else if (r <= 32) {
     bpp::solve<32, 8><<<(a.N + 7) / 8, 256, bpp::smem_bytes<32, 8>(), s>>>(a);
-  } else {
+  } else if (r <= 64) {
     bpp::solve<64, 4><<<(a.N + 3) / 4, 128, bpp::smem_bytes<64, 4>(), s>>>(a);
+  } else {                               // 64 < r <= 128: two-word masks, one warp per block
+    bpp::solve<128, 1><<<a.N, 32, bpp::smem_bytes<128, 1>(), s>>>(a);
   }
   CUK();
   if (dv) {
@@ -1321,8 +1324,8 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   if (!w0 || !h0) throw Fail{ENMF_INVALID_ARGUMENT, "run: null initial factor"};
   if (m > (size_t)INT32_MAX || n > (size_t)INT32_MAX || r > 4096)
     throw Fail{ENMF_INVALID_ARGUMENT, "run: shape exceeds the device path's limits (m,n < 2^31, r <= 4096)"};
-  if ((cfg->inner_h == ENMF_INNER_EXACT || cfg->inner_w == ENMF_INNER_EXACT) && r > 64)
-    throw Fail{ENMF_INVALID_ARGUMENT, "active_set_solve on device supports r <= 64"};
+  if ((cfg->inner_h == ENMF_INNER_EXACT || cfg->inner_w == ENMF_INNER_EXACT) && r > bpp::MAXR)
+    throw Fail{ENMF_INVALID_ARGUMENT, "active_set_solve on device supports r <= 128"};
   if ((cfg->inner_h == ENMF_INNER_HALS || cfg->inner_w == ENMF_INNER_HALS) && r > 1024)
     throw Fail{ENMF_INVALID_ARGUMENT, "hals_solve on device supports r <= 1024"};
   if (cfg->max_outer_iterations > (1ULL << 24))

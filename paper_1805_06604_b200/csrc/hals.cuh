@@ -64,8 +64,11 @@ ENMF_DEV void finish_sweep(const Args& a, double gain, int nonfinite) {
   const double fg = c->first_gain;
   const bool stop = (s >= a.max_sweeps) || (gain <= __dmul_rn(a.stall, fg < 0.0 ? 0.0 : fg));
   c->cont = stop ? 0 : 1;
-  c->nonfinite = nonfinite;
-  if (stop && nonfinite && a.st) {
+  // sticky over the sweeps of a solve: the block products form 0·h for the zeroed Gram entries
+  // the reference skips (nnls.hpp:121, gkj == 0), so an overflowed row (+inf) turns into NaN and
+  // then 0 in the next sweep instead of staying +inf as in the reference
+  c->nonfinite |= nonfinite;
+  if (stop && c->nonfinite && a.st) {
     // NaN guard on the finished iterate (engine.hpp:334-337 / 380-383)
     if (a.st->active) {
       a.st->error_code = ENMF_NON_FINITE;

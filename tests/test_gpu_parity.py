@@ -390,6 +390,35 @@ def test_eanls_bpp_paths_parity(ctx, port, r):
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=True)
 
 
+@pytest.mark.parametrize("r", [65, 96, 128])
+def test_bpp_wide_ranks_bitwise(ctx, port, r):
+    """active_set_solve (nnls.hpp:259-406) for 64 < r <= 128 (two-word passive / banned /
+    infeasible masks, packed factor): bitwise against the oracle, incl. a rank-deficient Gram."""
+    rng = np.random.default_rng(r)
+    w = rng.random((r + 30, r))
+    if r == 96:
+        w[:, 95] = w[:, 0] + w[:, 70]            # pivot drop + ban in the upper mask word
+    G, Cm = port.gram(w), port.cross_wx(w, rng.random((r + 30, 40)) - 0.3)
+    h0 = np.maximum(rng.random((r, 40)) - 0.5, 0)
+    a, ra = ctx.active_set_solve(G, Cm, h0)
+    b, rb = port.active_set_solve(G, Cm, h0)
+    assert np.array_equal(a, b) and ra == rb
+
+
+@pytest.mark.parametrize("r", [96, 128])
+def test_eanls_wide_rank_engine_parity(ctx, port, r):
+    """E-ANLS through the engine at r = 96 and 128 (previously rejected above 64): vs the oracle."""
+    m, n = 500, 420
+    rng = np.random.default_rng(r + 1)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.05 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, r + 2)
+    ref = port.run_dense(x, w0, h0, preset("e-anls-hp1", max_outer_iterations=4))
+    rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 4), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=True)
+    rec = ctx.run(x, w0, h0, _cfg("e-anls-hp1", 4, E.Precision.fp64_exact), E.TimingMode.none)
+    assert np.array_equal(rec.column("error"), ref[0]["error"])   # bitwise in the reference-order mode
+
+
 @pytest.mark.parametrize("r", [7, 21, 40])
 def test_csr_gather_paths_parity(ctx, port, r):
     """CSR gathers in FP64 mode across their paths: 512-entry chunks with split term rows and

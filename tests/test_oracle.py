@@ -263,3 +263,13 @@ def test_product_tiled_generator_matches_oracle(port):
     assert np.array_equal(data.gen_tiled(m, n, r, 5, tile=T), full)
     assert np.array_equal(data.gen_tiled(m, n, r, 5, rows=slice(256, 700), tile=T), full[256:])
     assert np.array_equal(data.gen_tiled(m, n, r, 5, cols=slice(100, 613), tile=T), full[:, 100:613])
+
+
+def test_reference_raises_non_finite_on_overflow(port, ref):
+    """The NonFiniteIterate case of tests/test_gpu_boundary.py: X near the top of the FP64 range,
+    W_yᵀX overflows, the reference throws in iteration 1 (engine.hpp:334-337) — port and reference."""
+    rng = np.random.default_rng(1)
+    x, w0, h0 = rng.random((40, 30)) * 1.5e308, rng.random((40, 4)), rng.random((4, 30))
+    for o in (port, ref):
+        with pytest.raises(OracleError, match="non-finite"):
+            o.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=5))
