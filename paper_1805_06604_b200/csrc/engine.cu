@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "hals.cuh"
+#include "hals_tm.cuh"
 #include "misc.cuh"
 #include "sparse.cuh"
 #include "ozaki.cuh"
@@ -207,6 +208,7 @@ void set_attrs_once() {
   big((const void*)hals::sweep_ws<32, true>, hals::ws_smem_bytes<32>());
   big((const void*)hals::sweep_ws<64, true>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128, true>, hals::ws_smem_bytes<128>());
+  big((const void*)hals::sweep_tm<128>, hals::tm_smem_bytes<128>());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -360,14 +362,15 @@ void gram_launch(enmf_gpu_ctx* c, cudaStream_t s, int prec, const double* A, lon
 
 // ---- inner solvers ------------------------------------------------------------
 int hals_variant() {
-  // ENMF_HALS_KERNEL: "" / "wsp" persistent paired-warp kernel (default), "ws" one launch per
-  // sweep, "fma" CUDA-core kernel.  Retired variants, the timing-experiment builds and their
+  // ENMF_HALS_KERNEL: "" persistent paired-warp kernels (default: sweep_tm with the iterate in
+  // tensor memory for 64 < r <= 128, sweep_ws below), "wsp" sweep_ws for every r, "ws" one launch
+  // per sweep, "fma" CUDA-core kernel.  Retired variants, the timing-experiment builds and their
   // measurements: profiles/r01_sweep_variants.md (the experiment builds are not in the product).
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("ENMF_HALS_KERNEL");
     const std::string s = e ? e : "";
-    v = s == "fma" ? 1 : s == "ws" ? 50 : 54;
+    v = s == "fma" ? 1 : s == "ws" ? 50 : s == "wsp" ? 55 : 54;
   }
   return v;
 }
@@ -431,11 +434,30 @@ void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   hals::sweep_ws<R_><<<grid, 256, hals::ws_smem_bytes<R_>(), s>>>(a, ntiles);
 }
 
+// Persistent TMEM-resident sweep (hals_tm.cuh): 4 column tiles per CTA at least, so small N
+// still spreads over the SMs; one CTA per SM (cooperative) for the grid-wide decision.
+template <int R_>
+void launch_sweep_tm(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  const long ntiles = ((long)a.N + 7) / 8;
+  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, (ntiles + 3) / 4));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = hals::tm_smem_bytes<R_>();
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&lc, hals::sweep_tm<R_>, a, ntiles));
+}
+
 bool hals_use_fma() { return hals_variant() == 1; }
 
 // The persistent sweep kernel runs a whole inner solve in one launch.
 bool hals_persistent(int prec, int r) {
-  return prec != PREC_EXACT && r <= 128 && hals_variant() == 54;
+  return prec != PREC_EXACT && r <= 128 && (hals_variant() == 54 || hals_variant() == 55);
 }
 
 void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
@@ -449,7 +471,7 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
     return;
   }
   const int v = hals_variant();
-  if (prec == PREC_TF32 && v == 54) {  // TF32 variant: block products on the TF32 tensor cores
+  if (prec == PREC_TF32 && (v == 54 || v == 55)) {  // TF32 variant: block products on the TF32 tensor cores
     if (r <= 32) launch_sweep_tf32<32>(c, s, a);
     else if (r <= 64) launch_sweep_tf32<64>(c, s, a);
     else launch_sweep_tf32<128>(c, s, a);
@@ -469,7 +491,8 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   } else {                              // default: persistent, one launch per inner solve
     if (r <= 32) launch_sweep_ws<32, true>(c, s, a);
     else if (r <= 64) launch_sweep_ws<64, true>(c, s, a);
-    else launch_sweep_ws<128, true>(c, s, a);
+    else if (v == 55) launch_sweep_ws<128, true>(c, s, a);
+    else launch_sweep_tm<128>(c, s, a);
   }
   CUK();
   c->launches++;
@@ -1011,7 +1034,7 @@ void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int sl
   constexpr size_t kGf = 128 * 128 + 64 * 64;   // fragments + tails (ws_prep)
   c->Gf.ensure(3 * kGf);
   double* gf = c->Gf.p + slot * kGf;
-  if (prec == PREC_TF32 && hals_variant() == 54) {   // TF32 variant's sweep: m16n8k8 fragments (tf_prep)
+  if (prec == PREC_TF32 && (hals_variant() == 54 || hals_variant() == 55)) {   // TF32 variant's sweep: m16n8k8 fragments (tf_prep)
     auto* gf4 = reinterpret_cast<float4*>(gf);
     if (a.r <= 32) hals::tf_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf4, a.st, a.ctl);
     else if (a.r <= 64) hals::tf_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf4, a.st, a.ctl);
@@ -1021,7 +1044,7 @@ void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int sl
     a.Gf = gf;
     return;
   }
-  if (hals_variant() != 50 && hals_variant() != 54) return;
+  if (hals_variant() != 50 && hals_variant() != 54 && hals_variant() != 55) return;
   if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);

@@ -608,3 +608,20 @@ def test_optimal_beta_linesearch_matches_reference():
         else:
             assert abs(got - beta) <= 1e-13 * abs(beta), (name, got, beta)
     ctx.close()
+
+
+@pytest.mark.parametrize("shape", [(1500, 2100, 128), (700, 900, 97), (256, 40000, 128)])
+def test_tmem_sweep_parity(ctx, port, shape):
+    """hals::sweep_tm (iterate held in tensor memory, 64 < r <= 128; hals_tm.cuh): E-A-HALS hp3
+    vs the oracle with identical sweep counts.  256×40000 gives the H update more columns than
+    fit in tensor memory at once (> 256 per SM), so sub-partitions sweep in two staged rounds."""
+    m, n, r = shape
+    rng = np.random.default_rng(m * 7 + n + r)
+    x = rng.random((m, r)) @ rng.random((r, n)) + np.abs(0.01 * rng.standard_normal((m, n)))
+    w0, h0 = port.random_init(m, n, r, 5)
+    it = 3 if n > 10000 else 6
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=it))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", it), E.TimingMode.none)
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
