@@ -36,11 +36,35 @@
 
 namespace hals {
 
-constexpr int TM_SLD = 40;   // S / partial tile row stride (conflict-free 16-byte fragment stores)
+constexpr int TM_SLD = 40;
 
+// Per-warp phase clock (built only with -DENMF_SWEEP_PROF, tools/gpu_sweep_prof.sh: cycles per
+// sweep and phase printed by CTA 0; the product library compiles it away).
+struct SwProf {
+#ifdef ENMF_SWEEP_PROF
+  long long t[8] = {};
+  long long last = 0;
+  ENMF_DEV void start() { last = clock64(); }
+  ENMF_DEV void mark(int i) {
+    const long long n = clock64();
+    t[i] += n - last;
+    last = n;
+  }
+#else
+  ENMF_DEV void start() {}
+  ENMF_DEV void mark(int) {}
+#endif
+};   // S / partial tile row stride (conflict-free 16-byte fragment stores)
+
+// shared memory: Gram fragments (ws_prep order, RMAX² + tails) | S hand-off [pair][group][8][TM_SLD]
+// | row-pass constants [NB][48]
+template <int RMAX>
+__host__ __device__ constexpr int tm_gf_doubles() {
+  return RMAX * RMAX + (RMAX / 16) * 64;
+}
 template <int RMAX>
 constexpr int tm_smem_bytes() {
-  return (2 * 4 * 2 * 8 * TM_SLD + (RMAX / 8) * 48) * 8;
+  return (tm_gf_doubles<RMAX>() + 4 * 2 * 8 * TM_SLD + (RMAX / 8) * 48) * 8;
 }
 
 // 16 lanes × 256 bits, twice along the columns: thread (g, t) gets lane g's words [c+2t, c+2t+1]
@@ -49,15 +73,6 @@ ENMF_DEV void tm_ld_frag(uint32_t ta, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(ta));
-}
-// tcgen05.wait::ld that also "rewrites" the destination registers of the loads it waits for, so
-// the compiler cannot read them before the wait
-ENMF_DEV void tm_wait_ld8(uint32_t (&u)[8], uint32_t (&w)[8]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
-                 "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7])
-               :
-               : "memory");
 }
 // 32 lanes × 16 consecutive 32-bit columns (thread i ↔ lane i of this warp's quarter)
 ENMF_DEV void tm_ld_rows(uint32_t ta, uint32_t (&v)[16]) {
@@ -86,128 +101,136 @@ ENMF_DEV void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" :::
 
 ENMF_DEV double tm_d(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
 
-// B fragments of k-steps (2j, 2j+1) for tiles 0..3 from the two 16-lane loads (see ws_mma2's p[])
-ENMF_DEV void tm_frags(const uint32_t (&u)[8], const uint32_t (&w)[8], double2 (&p)[4]) {
-  p[0] = make_double2(tm_d(u[0], u[1]), tm_d(u[2], u[3]));
-  p[2] = make_double2(tm_d(u[4], u[5]), tm_d(u[6], u[7]));
-  p[1] = make_double2(tm_d(w[0], w[1]), tm_d(w[2], w[3]));
-  p[3] = make_double2(tm_d(w[4], w[5]), tm_d(w[6], w[7]));
+// tcgen05.wait::ld over the four fragment loads of one k-step pair; it also "rewrites" their
+// destination registers, so the compiler cannot read them before the wait
+ENMF_DEV void tm_wait_ld32(uint32_t (&f)[4][8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(f[0][0]), "+r"(f[0][1]), "+r"(f[0][2]), "+r"(f[0][3]), "+r"(f[0][4]), "+r"(f[0][5]),
+                 "+r"(f[0][6]), "+r"(f[0][7]), "+r"(f[1][0]), "+r"(f[1][1]), "+r"(f[1][2]), "+r"(f[1][3]),
+                 "+r"(f[1][4]), "+r"(f[1][5]), "+r"(f[1][6]), "+r"(f[1][7]), "+r"(f[2][0]), "+r"(f[2][1]),
+                 "+r"(f[2][2]), "+r"(f[2][3]), "+r"(f[2][4]), "+r"(f[2][5]), "+r"(f[2][6]), "+r"(f[2][7]),
+                 "+r"(f[3][0]), "+r"(f[3][1]), "+r"(f[3][2]), "+r"(f[3][3]), "+r"(f[3][4]), "+r"(f[3][5]),
+                 "+r"(f[3][6]), "+r"(f[3][7])
+               :
+               : "memory");
 }
 
-// One group's joint two-block product: acc0 = S_b, acc1 = S_{b+1} without block b's columns;
-// tg = TMEM address of the group (this warp's lane quarter, column 0 of the group).
-template <int KS, int NT>
-ENMF_DEV void tm_products(uint32_t tg, const double (&A0)[KS], const double (&A1)[KS], double* Sg, double* Pg, int gi,
-                          int gt) {
-  double acc0[4][2], acc1[4][2];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) acc0[t][0] = acc0[t][1] = acc1[t][0] = acc1[t][1] = 0.0;
-  uint32_t u[2][8], w[2][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) w[0][i] = w[1][i] = 0u;
-  tm_ld_frag(tg, u[0]);
-  if (NT > 2) tm_ld_frag(tg + (16u << 16), w[0]);
-  tm_wait_ld8(u[0], w[0]);
-#pragma unroll
-  for (int j = 0; j < KS / 2; ++j) {
-    const int c = j & 1;
-    if (j + 1 < KS / 2) {           // next k-step pair in flight while this one's DMMAs issue
-      tm_ld_frag(tg + 16 * (j + 1), u[c ^ 1]);
-      if (NT > 2) tm_ld_frag(tg + (16u << 16) + 16 * (j + 1), w[c ^ 1]);
-    }
-    double2 p[4];
-    tm_frags(u[c], w[c], p);
-    ws_mma2<NT>(acc0, A0[2 * j], A0[2 * j + 1], p);
-    ws_mma2<NT>(acc1, A1[2 * j], A1[2 * j + 1], p);
-    if (j + 1 < KS / 2) tm_wait_ld8(u[c ^ 1], w[c ^ 1]);
-  }
-  ws_store_s(Sg, gi, gt, acc0);
-  ws_store_s(Pg, gi, gt, acc1);
-}
-
-// S_{b+1} += G[b+1 rows, block b columns] · (block b's new rows); partial from Pg, result to Sg
+// Fragment loads of rows [8j, 8j+8) (k-steps 2j, 2j+1) for the tiles in use: load q covers tiles
+// 2q, 2q+1 (q = 0, 1: group A lanes 0-15 / 16-31; q = 2, 3: group B)
 template <int NT>
-ENMF_DEV void tm_tail(uint32_t tg, int b, double2 tl, double* Sg, const double* Pg, int gi, int gt) {
-  uint32_t u[8], w[8];
+ENMF_DEV void tm_issue(const uint32_t (&la)[4], int j, uint32_t (&f)[4][8]) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = 0u;
-  tm_ld_frag(tg + 16 * b, u);
-  if (NT > 2) tm_ld_frag(tg + (16u << 16) + 16 * b, w);
-  double acc[4][2];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const double2 v = *reinterpret_cast<const double2*>(Pg + gi * TM_SLD + t * 8 + 2 * gt);
-    acc[t][0] = v.x;
-    acc[t][1] = v.y;
-  }
-  tm_wait_ld8(u, w);
-  double2 p[4];
-  tm_frags(u, w, p);
-  ws_mma2<NT>(acc, tl.x, tl.y, p);
-  ws_store_s(Sg, gi, gt, acc);
+  for (int q = 0; q < 4; ++q)
+    if (2 * q < NT) tm_ld_frag(la[q] + 16 * j, f[q]);
 }
 
-template <int KS>
-ENMF_DEV void tm_products_nt(int nt, uint32_t tg, const double (&A0)[KS], const double (&A1)[KS], double* Sg,
-                             double* Pg, int gi, int gt) {
-  switch (nt) {
-    case 4: tm_products<KS, 4>(tg, A0, A1, Sg, Pg, gi, gt); break;
-    case 3: tm_products<KS, 3>(tg, A0, A1, Sg, Pg, gi, gt); break;
-    case 2: tm_products<KS, 2>(tg, A0, A1, Sg, Pg, gi, gt); break;
-    default: tm_products<KS, 1>(tg, A0, A1, Sg, Pg, gi, gt); break;
-  }
-}
-ENMF_DEV void tm_tail_nt(int nt, uint32_t tg, int b, double2 tl, double* Sg, const double* Pg, int gi, int gt) {
-  switch (nt) {
-    case 4: tm_tail<4>(tg, b, tl, Sg, Pg, gi, gt); break;
-    case 3: tm_tail<3>(tg, b, tl, Sg, Pg, gi, gt); break;
-    case 2: tm_tail<2>(tg, b, tl, Sg, Pg, gi, gt); break;
-    default: tm_tail<1>(tg, b, tl, Sg, Pg, gi, gt); break;
-  }
+// B fragment of tile t, k-step 2j (k = 0) or 2j+1 (k = 1): load t/2, lane half t%2
+template <int K>
+ENMF_DEV double tm_b(const uint32_t (&f)[4][8], int t) {
+  return tm_d(f[t >> 1][4 * K + 2 * (t & 1)], f[t >> 1][4 * K + 2 * (t & 1) + 1]);
 }
 
-// The product warp's part of one round (groups A and B of this sub-partition).
-template <int KS, int NB>
-ENMF_DEV void tm_producer_round(uint32_t tq, int ntA, int ntB, double* Ss, double* Ps, const double2* gf, int gi,
-                                int gt, int idS, int idH) {
+// c0[t] += A0 · B(t), c1[t] += A1 · B(t) over k-steps 2j, 2j+1; every accumulator's two DMMAs are
+// 2·NT instructions apart (≥ 32 cycles > the 26.5-cycle DMMA latency)
+template <int NT>
+ENMF_DEV void tm_mma_j(double (&c0)[8][2], double (&c1)[8][2], double2 a0, double2 a1, const uint32_t (&f)[4][8]) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t) dmma884(c0[t][0], c0[t][1], a0.x, tm_b<0>(f, t));
+#pragma unroll
+  for (int t = 0; t < NT; ++t) dmma884(c1[t][0], c1[t][1], a1.x, tm_b<0>(f, t));
+#pragma unroll
+  for (int t = 0; t < NT; ++t) dmma884(c0[t][0], c0[t][1], a0.y, tm_b<1>(f, t));
+#pragma unroll
+  for (int t = 0; t < NT; ++t) dmma884(c1[t][0], c1[t][1], a1.y, tm_b<1>(f, t));
+}
+
+// accumulator tiles → the S hand-off rows (tiles 0-3: group A, 4-7: group B)
+template <int NT>
+ENMF_DEV void tm_store_s(double* Ss, int gi, int gt, const double (&c)[8][2]) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    *reinterpret_cast<double2*>(Ss + (t >> 2) * 8 * TM_SLD + gi * TM_SLD + (t & 3) * 8 + 2 * gt) =
+        make_double2(c[t][0], c[t][1]);
+}
+
+// The product warp's part of one round: every tile of the round (both groups) in one pass per
+// block pair.  Row blocks in pairs (b, b+1): one pass over H feeds S_b over every row block and
+// S_{b+1} over every block but b (whose columns come in as the "tail" once the row warp has solved
+// block b; S_{b+1}'s accumulators stay in registers across the hand-off).  Gram fragments stream
+// from shared memory (gfs, ws_prep order) next to the TMEM fragment loads, one k-step pair ahead.
+template <int KS, int NB, int NT>
+ENMF_DEV void tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS, int idH,
+                                SwProf& pf) {
   constexpr uint32_t GC = 8 * KS;   // TMEM columns per group (2 words × RMAX rows)
-  double A0[KS], A1[KS];
+  const uint32_t la[4] = {tq, tq + (16u << 16), tq + GC, tq + GC + (16u << 16)};
+  uint32_t f[2][4][8];
 #pragma unroll
-  for (int s = 0; s < KS; s += 2) {
-    const double2 f0 = gf[(s / 2) * 32];
-    const double2 f1 = gf[(KS / 2 + s / 2) * 32];
-    A0[s] = f0.x; A0[s + 1] = f0.y;
-    A1[s] = f1.x; A1[s + 1] = f1.y;
-  }
-  double* SA = Ss;
-  double* SB = Ss + 8 * TM_SLD;
-  double* PA = Ps;
-  double* PB = Ps + 8 * TM_SLD;
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[0][q][i] = f[1][q][i] = 0u;
 #pragma unroll 1
   for (int b = 0; b < NB; b += 2) {
     if (b > 0) {
       bar_sync_n<64>(idH);                       // rows of block b-1 are final in TMEM
       tc::fence_after();
+      pf.mark(2);
     }
-    tm_products_nt<KS>(ntA, tq, A0, A1, SA, PA, gi, gt);
-    if (ntB > 0) tm_products_nt<KS>(ntB, tq + GC, A0, A1, SB, PB, gi, gt);
-    bar_arrive_n<64>(idS);                       // S_b ready (both groups): the row warp solves block b
-    // while it does: this pair's tail fragments and the next pair's Gram fragments
-    const double2 tl = gf[(16 * KS * KS + (b >> 1) * 64) / 2];
-    if (b + 2 < NB) {
+    double c0[8][2], c1[8][2];
 #pragma unroll
-      for (int s = 0; s < KS; s += 2) {
-        const double2 f0 = gf[(((b + 2) * KS / 2) + s / 2) * 32];
-        const double2 f1 = gf[(((b + 3) * KS / 2) + s / 2) * 32];
-        A0[s] = f0.x; A0[s + 1] = f0.y;
-        A1[s] = f1.x; A1[s + 1] = f1.y;
+    for (int t = 0; t < 8; ++t) c0[t][0] = c0[t][1] = c1[t][0] = c1[t][1] = 0.0;
+    const double2* g0 = gfs + (b * KS / 2) * 32;         // block b's fragments, k-step pair j at j·32
+    const double2* g1 = gfs + ((b + 1) * KS / 2) * 32;   // block b+1's (without block b's columns)
+    tm_issue<NT>(la, 0, f[0]);
+    double2 a0 = g0[0], a1 = g1[0];
+    tm_wait_ld32(f[0]);
+#pragma unroll
+    for (int j = 0; j < KS / 2; ++j) {
+      const int cur = j & 1;
+      double2 n0, n1;
+      if (j + 1 < KS / 2) {                      // next k-step pair in flight while these DMMAs issue
+        tm_issue<NT>(la, j + 1, f[cur ^ 1]);
+        n0 = g0[(j + 1) * 32];
+        n1 = g1[(j + 1) * 32];
+      }
+      tm_mma_j<NT>(c0, c1, a0, a1, f[cur]);
+      if (j + 1 < KS / 2) {
+        tm_wait_ld32(f[cur ^ 1]);
+        a0 = n0;
+        a1 = n1;
       }
     }
+    tm_store_s<NT>(Ss, gi, gt, c0);
+    pf.mark(0);
+    bar_arrive_n<64>(idS);                       // S_b ready (both groups): the row warp solves block b
+    const double2 tl = gfs[(16 * KS * KS + (b >> 1) * 64) / 2];
+    pf.mark(1);
     bar_sync_n<64>(idH);                         // block b solved
     tc::fence_after();
-    tm_tail_nt(ntA, tq, b, tl, SA, PA, gi, gt);
-    if (ntB > 0) tm_tail_nt(ntB, tq + GC, b, tl, SB, PB, gi, gt);
+    pf.mark(2);
+    tm_issue<NT>(la, b, f[0]);                   // block b's new rows
+    tm_wait_ld32(f[0]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) dmma884(c1[t][0], c1[t][1], tl.x, tm_b<0>(f[0], t));
+#pragma unroll
+    for (int t = 0; t < NT; ++t) dmma884(c1[t][0], c1[t][1], tl.y, tm_b<1>(f[0], t));
+    tm_store_s<NT>(Ss, gi, gt, c1);
     bar_arrive_n<64>(idS);                       // S_{b+1} ready
+    pf.mark(3);
+  }
+}
+
+template <int KS, int NB>
+ENMF_DEV void tm_producer_round_nt(int nt, uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS,
+                                   int idH, SwProf& pf) {
+  switch (nt) {
+    case 8: tm_producer_round<KS, NB, 8>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 7: tm_producer_round<KS, NB, 7>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 6: tm_producer_round<KS, NB, 6>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 5: tm_producer_round<KS, NB, 5>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 4: tm_producer_round<KS, NB, 4>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 3: tm_producer_round<KS, NB, 3>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 2: tm_producer_round<KS, NB, 2>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    default: tm_producer_round<KS, NB, 1>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
   }
 }
 
@@ -243,12 +266,17 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp & 3;
   const bool producer = warp < 4;
-  double* Ss = sm + pair * (2 * 8 * TM_SLD);                      // [group][8][TM_SLD]: S hand-off
-  double* Ps = sm + 4 * 2 * 8 * TM_SLD + pair * (2 * 8 * TM_SLD);  // product warp's S_{b+1} partials
+  double* Gfs = sm;                                               // Gram fragments (ws_prep order)
+  double* Ss = sm + tm_gf_doubles<RMAX>() + pair * (2 * 8 * TM_SLD); // [group][8][TM_SLD]: S hand-off
   // per row block: lower triangle G[8b+l][8b+i] / G_ll (i < l) at l(l-1)/2 + i, G_kk/2 at 28 + l,
   // 1/G_kk at 36 + l (padding rows: unit diagonal)
-  double* Gc = sm + 2 * 4 * 2 * 8 * TM_SLD;
+  double* Gc = sm + tm_gf_doubles<RMAX>() + 4 * 2 * 8 * TM_SLD;
   const int r = a.r;
+  {
+    const double2* g = reinterpret_cast<const double2*>(a.Gf);
+    double2* d = reinterpret_cast<double2*>(Gfs);
+    for (int i = threadIdx.x; i < tm_gf_doubles<RMAX>() / 2; i += 256) d[i] = g[i];
+  }
   for (int e = threadIdx.x; e < NB * 48; e += 256) {
     const int b = e / 48, j = e % 48;
     double v = 0.0;
@@ -279,13 +307,15 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   int nf = 0;
   double first_total = 0.0;
   const int gi = lane >> 2, gt = lane & 3;
-  const double2* gf = reinterpret_cast<const double2*>(a.Gf) + lane;
+  const double2* gfs = reinterpret_cast<const double2*>(Gfs) + lane;
+  SwProf pf;
+  pf.start();
 
   for (int sw = 0;; ++sw) {
     for (int i = 0; i < rounds; ++i) {
       const long ta = tq0 + (long)i * cnt / rounds;
       const int nt = (int)(tq0 + (long)(i + 1) * cnt / rounds - ta);
-      const int ntA = (nt + 1) / 2, ntB = nt - ntA;
+      const int ntA = nt < 4 ? nt : 4, ntB = nt - ntA;   // tiles 0-3: group A, 4-7: group B
       const long colA = ta * 8, colB = (ta + ntA) * 8;
       if (!(sw > 0 && rounds == 1)) {            // resident: staged once per solve
         tc::fence_before();
@@ -297,9 +327,10 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         tc::fence_before();
         nb_sync(idP);
         tc::fence_after();
+        pf.mark(5);
       }
       if (producer) {
-        tm_producer_round<KS, NB>(tq, ntA, ntB, Ss, Ps, gf, gi, gt, idS, idH);
+        tm_producer_round_nt<KS, NB>(nt, tq, Ss, gfs, gi, gt, idS, idH, pf);
       } else {
         // two columns per lane: cA in group A, cB in group B (predicated, no branches)
         const long ld = a.ld, ld8 = 8 * ld;
@@ -347,12 +378,18 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
           }
           tm_wait_ld16(xa);
           tm_wait_ld16(xb);
+          pf.mark(0);
           bar_sync_n<64>(idS);
+          pf.mark(1);
           double x[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            bb[i] = __dmul_rn(__dsub_rn(bb[i], SA[i * TM_SLD + lane]), gc[36 + i]);
-            bb[8 + i] = __dmul_rn(__dsub_rn(bb[8 + i], SB[i * TM_SLD + lane]), gc[36 + i]);
+            // columns past the round's tiles: the product warp leaves their S unwritten (stale or
+            // uninitialised shared memory), so they are forced to t = 0 (h stays 0, no gain)
+            const double sa = __dmul_rn(__dsub_rn(bb[i], SA[i * TM_SLD + lane]), gc[36 + i]);
+            const double sb = __dmul_rn(__dsub_rn(bb[8 + i], SB[i * TM_SLD + lane]), gc[36 + i]);
+            bb[i] = vA ? sa : 0.0;
+            bb[8 + i] = vB ? sb : 0.0;
             x[i] = tm_d(xa[2 * i], xa[2 * i + 1]);
             x[8 + i] = tm_d(xb[2 * i], xb[2 * i + 1]);
           }
@@ -384,6 +421,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
           tm_wait_st();
           tc::fence_before();
           if (b + 1 < NB) bar_arrive_n<64>(idH);
+          pf.mark(2);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (vA && 8 * b + i < r) hpA[i * ld] = x[i];
@@ -398,6 +436,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
           cpB += ld8;
           hpA += ld8;
           hpB += ld8;
+          pf.mark(3);
         }
         nf |= hmax >= 0x7FF00000;
       }
@@ -405,9 +444,19 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
     // ---- grid-wide end of sweep `sw` (the row warps' last TMEM stores are ordered before the
     // next sweep's fragment loads by the fences around grid_decision's block barriers) ----
     tc::fence_before();
+    pf.mark(6);
     const int cont = grid_decision(a, gain, nf, sw, first_total, red);
     tc::fence_after();
-    if (!cont) break;
+    pf.mark(4);
+    if (!cont) {
+#ifdef ENMF_SWEEP_PROF
+      if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && lane == 0)
+        printf("sweep_tm prof cta %d warp %d sweeps %d cycles/sweep: %lld %lld %lld %lld | decision %lld | stage %lld | "
+               "end %lld\n", blockIdx.x, warp, sw + 1, pf.t[0] / (sw + 1), pf.t[1] / (sw + 1), pf.t[2] / (sw + 1),
+               pf.t[3] / (sw + 1), pf.t[4] / (sw + 1), pf.t[5] / (sw + 1), pf.t[6] / (sw + 1));
+#endif
+      break;
+    }
     gain = 0.0;
     nf = 0;
     src = a.H;

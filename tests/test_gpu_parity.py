@@ -625,3 +625,19 @@ def test_tmem_sweep_parity(ctx, port, shape):
     assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
     assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
     assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+
+
+@pytest.mark.parametrize("nt", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_tmem_sweep_tiles_per_subpartition(ctx, port, nt):
+    """hals_solve (nnls.hpp:154-176) at r = 128 with N = 148·4·8·nt columns: on a 148-SM B200 every
+    SM sub-partition of sweep_tm holds exactly nt 8-column tiles (one product-loop variant each)."""
+    r, n = 128, 148 * 4 * 8 * nt
+    rng = np.random.default_rng(nt)
+    w = rng.random((300, r))
+    g = port.gram(w)
+    c = port.cross_wx(w, rng.random((300, n)))
+    h0 = rng.random((r, n))
+    hd, sd = ctx.hals_solve(g, c, h0, 6, 0.01)
+    hr, sr = port.hals_solve(g, c, h0, 6, 0.01)
+    assert sd == sr
+    assert np.max(np.abs(hd - hr)) <= 1e-9 * np.max(np.abs(hr))
