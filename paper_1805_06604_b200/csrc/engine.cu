@@ -137,7 +137,7 @@ struct enmf_gpu_ctx {
   struct DistHost* dist = nullptr;
   // standalone kernel API
   int kernel_precision = ENMF_PRECISION_FP64;
-  DBuf<double> ka, kb, kc, kd, ke;
+  DBuf<double> ka, kb, kc, kd, ke, kf;
   DBuf<double> ls_part, ls_val;   // optimal_beta_linesearch scratch (never captured in a graph)
   DBuf<HalsCtl> kctl;
 };
@@ -1065,6 +1065,7 @@ void enqueue_inner(enmf_gpu_ctx* c, cudaStream_t s, const Plan& pl, int side, in
     a.part = c->gain_part.p + side * (c->gain_part.n / 2);
     a.part_nf = c->part_nf.p + side * (c->part_nf.n / 2);
     a.terms = c->terms.p; a.st = st; a.side = side;
+    a.H2 = c->scratch.p;                 // r·max(m, n): unused while the iteration graphs run
     a.cond = (unsigned long long)cond; a.use_cond = mode == INNER_CAPTURE ? 1 : 0;
     a.dv = D ? D->dview : nullptr;
     hals::reset_ctl<<<1, 1, 0, s>>>(a.ctl, st);

@@ -48,6 +48,7 @@ struct Args {
   int use_cond;
   const dist::View* dv;     // multi-GPU: all-reduce the sweep gain across ranks (nullable)
   const double* Gf;         // sweep_ws: Gram in A-fragment order (ws_prep)
+  double* H2;               // sweep_tm: r×N scratch (row stride ld) for odd sweeps (speculative stall decision)
 };
 
 ENMF_DEV void set_cond(const Args& a, unsigned v) {

@@ -234,6 +234,35 @@ ENMF_DEV void tm_producer_round_nt(int nt, uint32_t tq, double* Ss, const double
   }
 }
 
+// Speculative stall decision (single GPU): the decision on sweep `s` (nnls.hpp:172-173), taken by
+// ONE warp of every CTA while the CTA already runs sweep s+1.  Waits until every CTA has published
+// its sweep-s gain partial, then forms the total in a fixed order (lane l sums CTAs l, l+32, ...,
+// then a fixed xor tree), so every CTA reaches the identical decision; CTA 0 also does the
+// solve's bookkeeping (sweep count, first/last gain, sticky non-finite flag, NaN guard).
+ENMF_DEV int tm_decide(const Args& a, int s, double& first_total) {
+  const int lane = threadIdx.x & 31;
+  const unsigned target = (unsigned)(s + 1) * gridDim.x;
+  unsigned e;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
+  } while (e < target);
+  const double* part = a.part + (s & 1) * gridDim.x;
+  const int* part_nf = a.part_nf + (s & 1) * gridDim.x;
+  double v = 0.0;
+  int f = 0;
+  for (int b = lane; b < (int)gridDim.x; b += 32) {
+    v = __dadd_rn(v, __ldcg(part + b));
+    f |= __ldcg(part_nf + b);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  f = __any_sync(0xffffffffu, f) ? 1 : 0;
+  if (s == 0) first_total = v;
+  const bool stop = (s + 1 >= a.max_sweeps) || (v <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
+  if (blockIdx.x == 0 && lane == 0) finish_sweep(a, v, f);
+  return stop ? 1 : 0;
+}
+
 // Copies rows [0, RMAX) of `ncols` columns starting at `col` (lane = column) from global into the
 // group at TMEM address tg (zeros outside r × N and past ncols).
 template <int RMAX>
@@ -310,8 +339,23 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   const double2* gfs = reinterpret_cast<const double2*>(Gfs) + lane;
   SwProf pf;
   pf.start();
+  // Speculative end of sweep (single GPU): sweep s writes its rows to Hb[s & 1] (a.H / a.H2) and
+  // publishes its gain partial without waiting; the decision on sweep s is formed during sweep s+1
+  // by warp 4 (idle until its first hand-off) and read at the end of sweep s+1.  A "stop" on
+  // sweep s discards sweep s+1 — its rows went to the other buffer — and the result is Hb[s & 1].
+  // Sharded solves keep the synchronous grid_decision (its cross-GPU exchange).
+  const bool spec = a.dv == nullptr && a.H2 != nullptr;
+  __shared__ double s_wg[2][4];
+  __shared__ int s_wnf[2][4];
+  __shared__ int s_dec[2];
+  int result_sweep = -1;
 
   for (int sw = 0;; ++sw) {
+    double* const hout = (spec && (sw & 1)) ? a.H2 : a.H;
+    if (spec && sw > 0 && warp == 4) {
+      const int d = tm_decide(a, sw - 1, first_total);
+      if (lane == 0) s_dec[(sw - 1) & 1] = d;
+    }
     for (int i = 0; i < rounds; ++i) {
       const long ta = tq0 + (long)i * cnt / rounds;
       const int nt = (int)(tq0 + (long)(i + 1) * cnt / rounds - ta);
@@ -338,8 +382,8 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         const bool vB = lane < ntB * 8 && colB + lane < a.N;
         const double* cpA = a.C + (vA ? colA + lane : 0);
         const double* cpB = a.C + (vB ? colB + lane : 0);
-        double* hpA = a.H + (vA ? colA + lane : 0);
-        double* hpB = a.H + (vB ? colB + lane : 0);
+        double* hpA = hout + (vA ? colA + lane : 0);
+        double* hpB = hout + (vB ? colB + lane : 0);
         const double* SA = Ss;
         const double* SB = Ss + 8 * TM_SLD;
         double cn[16];
@@ -441,6 +485,46 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         nf |= hmax >= 0x7FF00000;
       }
     }
+    if (spec) {
+      // ---- speculative end of sweep `sw` ----
+      if (!producer) {
+        double g = __dadd_rn(gain, gain);   // gains are accumulated halved
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) g = __dadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
+        const int f = __any_sync(0xffffffffu, nf) ? 1 : 0;
+        if (lane == 0) {
+          s_wg[sw & 1][pair] = g;
+          s_wnf[sw & 1][pair] = f;
+        }
+      }
+      tc::fence_before();                    // the row warps' last TMEM stores before the next sweep
+      pf.mark(6);
+      __syncthreads();
+      tc::fence_after();
+      const int last = sw + 1 >= a.max_sweeps;
+      if (warp == 4 && lane == 0) {          // this CTA's sweep-sw partial (fixed order over the warps)
+        const double g = __dadd_rn(__dadd_rn(s_wg[sw & 1][0], s_wg[sw & 1][1]),
+                                   __dadd_rn(s_wg[sw & 1][2], s_wg[sw & 1][3]));
+        const int f = s_wnf[sw & 1][0] | s_wnf[sw & 1][1] | s_wnf[sw & 1][2] | s_wnf[sw & 1][3];
+        a.part[(sw & 1) * gridDim.x + blockIdx.x] = g;
+        a.part_nf[(sw & 1) * gridDim.x + blockIdx.x] = f;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&a.ctl->arrive) : "memory");
+      }
+      pf.mark(4);
+      if (sw > 0 && s_dec[(sw - 1) & 1]) {   // sweep sw-1 was the last: sweep sw is discarded
+        result_sweep = sw - 1;
+        break;
+      }
+      if (last) {                            // max_sweeps reached: no speculation past the cap
+        if (blockIdx.x == 0 && warp == 4) tm_decide(a, sw, first_total);   // bookkeeping only
+        result_sweep = sw;
+        break;
+      }
+      gain = 0.0;
+      nf = 0;
+      src = hout;
+      continue;
+    }
     // ---- grid-wide end of sweep `sw` (the row warps' last TMEM stores are ordered before the
     // next sweep's fragment loads by the fences around grid_decision's block barriers) ----
     tc::fence_before();
@@ -449,17 +533,26 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
     tc::fence_after();
     pf.mark(4);
     if (!cont) {
-#ifdef ENMF_SWEEP_PROF
-      if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && lane == 0)
-        printf("sweep_tm prof cta %d warp %d sweeps %d cycles/sweep: %lld %lld %lld %lld | decision %lld | stage %lld | "
-               "end %lld\n", blockIdx.x, warp, sw + 1, pf.t[0] / (sw + 1), pf.t[1] / (sw + 1), pf.t[2] / (sw + 1),
-               pf.t[3] / (sw + 1), pf.t[4] / (sw + 1), pf.t[5] / (sw + 1), pf.t[6] / (sw + 1));
-#endif
+      result_sweep = sw;
       break;
     }
     gain = 0.0;
     nf = 0;
     src = a.H;
+  }
+#ifdef ENMF_SWEEP_PROF
+  if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && lane == 0)
+    printf("sweep_tm prof cta %d warp %d sweeps %d cycles/sweep: %lld %lld %lld %lld | decision %lld | stage %lld | "
+           "end %lld\n", blockIdx.x, warp, result_sweep + 1, pf.t[0] / (result_sweep + 1), pf.t[1] / (result_sweep + 1),
+           pf.t[2] / (result_sweep + 1), pf.t[3] / (result_sweep + 1), pf.t[4] / (result_sweep + 1),
+           pf.t[5] / (result_sweep + 1), pf.t[6] / (result_sweep + 1));
+#endif
+  if (spec && (result_sweep & 1)) {
+    // the result is in the scratch buffer: copy this pair's columns into a.H (rows < r)
+    const long c0 = tq0 * 8, c1 = min((tq0 + cnt) * 8, (long)a.N);
+    const int t = (threadIdx.x & 31) + (producer ? 0 : 32);
+    for (long col = c0 + t; col < c1; col += 64)
+      for (int k = 0; k < r; ++k) a.H[(long)k * a.ld + col] = a.H2[(long)k * a.ld + col];
   }
   tc::fence_before();
   __syncthreads();
