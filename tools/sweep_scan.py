@@ -1,0 +1,20 @@
+"""Per-sweep cost of the persistent sweep kernel vs the number of sweeps in one solve (device-timed:
+ctx.hals_solve_device keeps G, C, H on the device).  C5 shape, forced sweep counts."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1805_06604_b200 as E
+
+r, n = 128, 32768
+rng = np.random.default_rng(0)
+w = rng.random((4096, r))
+G = w.T @ w
+C = G @ rng.random((r, n)) * 0.9
+h0 = rng.random((r, n))
+ctx = E.Context()
+for ms in (2, 4, 8, 16, 32, 64, 129, 129, 64, 8):
+    t = time.perf_counter()
+    h, sw = ctx.hals_solve(G, C, h0, ms, 1e-300)
+    dt = time.perf_counter() - t
+    print(f"max_sweeps={ms:4d} sweeps={sw:4d} wall={dt*1e3:8.2f} ms", flush=True)
