@@ -124,6 +124,9 @@ struct enmf_gpu_ctx {
   DBuf<double> partials, gain_part, terms, ddpart, dd;
   DBuf<int> part_nf, flags, kpart_nf;
   DBuf<unsigned> counters;
+  DBuf<double> kpartials;                 // kernel-level API calls: own split-K scratch (never a session graph's)
+  DBuf<unsigned> kcounters;
+  bool kapi = false;
   DBuf<unsigned long long> bpp_exch;
   DBuf<int> bpp_rounds, bpp_nf;
   DBuf<double> cmax;
@@ -263,22 +266,82 @@ bool gemm_big_tile() {  // ENMF_GEMM_TILE=128: the 128×128 single-CTA-per-SM ke
   return v == 1;
 }
 
+// Split-K scratch of one GEMM (the tile grid and split count gemm_launch_small / gemm_launch choose).
+struct SplitNeed {
+  int S, tiles;
+  bool last;
+};
+SplitNeed split_need(const enmf_gpu_ctx* c, int M, int N, int K) {
+  SplitNeed n{};
+  if (!gemm_big_tile()) {
+    n.tiles = ((N + gemm::st::BN - 1) / gemm::st::BN) * ((M + gemm::st::BM - 1) / gemm::st::BM);
+    n.S = choose_splits(n.tiles, (K + gemm::st::BK - 1) / gemm::st::BK, 3 * c->sms);
+  } else {
+    n.tiles = ((N + gemm::BN - 1) / gemm::BN) * ((M + gemm::BM - 1) / gemm::BM);
+    n.S = choose_splits(n.tiles, (K + gemm::BK - 1) / gemm::BK, c->sms);
+  }
+  n.last = n.S > 1 && n.S <= 8;
+  return n;
+}
+
+// The split-K workspace for a launch: sized in begin() for every GEMM a session graph holds
+// (presize_splits), so a captured launch never reallocates it — growing it while a stream is
+// capturing would free memory an earlier node of the same graph still uses, hence an internal
+// error.  Kernel-level API calls (c->kapi) use their own workspace, never a session graph's.
+void split_ws(enmf_gpu_ctx* c, cudaStream_t s, const SplitNeed& n, int M, int N, double** part, unsigned** cnt) {
+  DBuf<double>& P = c->kapi ? c->kpartials : c->partials;
+  DBuf<unsigned>& Q = c->kapi ? c->kcounters : c->counters;
+  if (n.S > 1) {
+    const size_t need = (size_t)n.S * M * N;
+    const bool grow = P.n < need || (n.last && Q.n < (size_t)n.tiles);
+    if (grow) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      CU(cudaStreamIsCapturing(s, &cs));
+      if (cs != cudaStreamCaptureStatusNone)
+        throw Fail{ENMF_CUDA_ERROR, "internal: split-K workspace would grow during graph capture"};
+    }
+    P.ensure(need);
+    if (n.last && Q.n < (size_t)n.tiles) {
+      Q.ensure(n.tiles);
+      CU(cudaMemsetAsync(Q.p, 0, sizeof(unsigned) * n.tiles, s));
+    }
+  }
+  *part = n.S > 1 ? P.p : nullptr;
+  *cnt = Q.p;
+}
+
+// Sizes the session workspace for the GEMMs of an m×n, rank-r problem held as ml rows / nl
+// columns here (sharded: local extents): the two Grams (K = ml, nl) and both cross products on the
+// DMMA GEMM (N = nl, K = m and N = ml, K = n; the INT8-digit / CSR / TF32 products use their own
+// buffers).
+void presize_splits(enmf_gpu_ctx* c, cudaStream_t s, size_t m, size_t n, size_t ml, size_t nl, size_t r) {
+  size_t need = 0, tiles = 0;
+  const int shapes[4][3] = {{(int)r, (int)r, (int)ml}, {(int)r, (int)r, (int)nl}, {(int)r, (int)nl, (int)m},
+                            {(int)r, (int)ml, (int)n}};
+  for (const auto& sh : shapes) {
+    const SplitNeed k = split_need(c, sh[0], sh[1], sh[2]);
+    if (k.S > 1) need = std::max(need, (size_t)k.S * sh[0] * sh[1]);
+    if (k.last) tiles = std::max(tiles, (size_t)k.tiles);
+  }
+  if (need) c->partials.ensure(need);
+  if (tiles && c->counters.n < tiles) {
+    c->counters.ensure(tiles);
+    CU(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned) * tiles, s));
+  }
+}
+
 void gemm_launch_small(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long lda, const double* B, long ldb,
                        double* C, long ldc, int M, int N, int K, bool sym, const DevState* st) {
   using namespace gemm;
-  const int tn = (N + st::BN - 1) / st::BN, tm = (M + st::BM - 1) / st::BM, tiles = tn * tm;
-  const int kb = (K + st::BK - 1) / st::BK;
-  const int S = choose_splits(tiles, kb, 3 * c->sms);
-  const bool last = S > 1 && S <= 8;
-  if (S > 1) {
-    c->partials.ensure((size_t)S * M * N);
-    if (last && c->counters.n < (size_t)tiles) {
-      c->counters.ensure(tiles);
-      CU(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned) * tiles, s));
-    }
-  }
+  const int tn = (N + st::BN - 1) / st::BN, tm = (M + st::BM - 1) / st::BM;
+  const SplitNeed need = split_need(c, M, N, K);
+  const int S = need.S;
+  const bool last = need.last;
+  double* part;
+  unsigned* cnt;
+  split_ws(c, s, need, M, N, &part, &cnt);
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
-  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, S > 1 ? c->partials.p : nullptr, c->counters.p, sym ? 1 : 0, st};
+  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, part, cnt, sym ? 1 : 0, st};
   // M-tiles vary fastest (blockIdx.x): the r/64 CTAs sharing one X tile run
   // together, so X is fetched from HBM once and hit in L2 by the others.
   dim3 grid(tm, tn, S);
@@ -294,7 +357,7 @@ void gemm_launch_small(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A
   CUK();
   c->launches++;
   if (S > 1 && !last) {
-    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(c->partials.p, S, M, N, C, ldc, sym ? 1 : 0, st);
+    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(part, S, M, N, C, ldc, sym ? 1 : 0, st);
     CUK();
     c->launches++;
   }
@@ -307,19 +370,15 @@ void gemm_launch(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long
     gemm_launch_small(c, s, bk, A, lda, B, ldb, C, ldc, M, N, K, sym, st);
     return;
   }
-  const int tn = (N + BN - 1) / BN, tm = (M + BM - 1) / BM, tiles = tn * tm;
-  const int kb = (K + BK - 1) / BK;
-  const int S = choose_splits(tiles, kb, c->sms);
-  const bool last = S > 1 && S <= 8;
-  if (S > 1) {
-    c->partials.ensure((size_t)S * M * N);
-    if (last && c->counters.n < (size_t)tiles) {
-      c->counters.ensure(tiles);
-      CU(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned) * tiles, s));
-    }
-  }
+  const int tn = (N + BN - 1) / BN, tm = (M + BM - 1) / BM;
+  const SplitNeed need = split_need(c, M, N, K);
+  const int S = need.S;
+  const bool last = need.last;
+  double* part;
+  unsigned* cnt;
+  split_ws(c, s, need, M, N, &part, &cnt);
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
-  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, S > 1 ? c->partials.p : nullptr, c->counters.p, sym ? 1 : 0, st};
+  Params p{A, lda, B, ldb, C, ldc, M, N, K, S, part, cnt, sym ? 1 : 0, st};
   dim3 grid(tn, tm, S);
   static int w16 = -1;  // ENMF_GEMM_WARPS=16: 16 warps of 32×32 instead of 8 of 64×32
   if (w16 < 0) {
@@ -342,7 +401,7 @@ void gemm_launch(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A, long
   CUK();
   c->launches++;
   if (S > 1 && !last) {
-    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(c->partials.p, S, M, N, C, ldc, sym ? 1 : 0, st);
+    reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(part, S, M, N, C, ldc, sym ? 1 : 0, st);
     CUK();
     c->launches++;
   }
@@ -1360,6 +1419,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   BeginTrace tr(s);
   set_attrs_once();
   ensure_buffers(c, ml, nl, r);
+  presize_splits(c, s, m, n, ml, nl, r);
   tr.mark("buffers");
   if (cfg->precision == PREC_EXACT || r > 128) c->terms.ensure(std::max(wsz, hsz));
   const size_t K = cfg->max_outer_iterations;

@@ -641,3 +641,22 @@ def test_tmem_sweep_tiles_per_subpartition(ctx, port, nt):
     hr, sr = port.hals_solve(g, c, h0, 6, 0.01)
     assert sd == sr
     assert np.max(np.abs(hd - hr)) <= 1e-9 * np.max(np.abs(hr))
+
+
+def test_int8_digit_products_integer_counts(ctx, port):
+    """Short-mantissa data (integer term counts, Poisson): every digit past the first one or two
+    is exactly zero, so the truncation-bias estimate (ozk::finish) sees zero digit sums and only
+    the uncut-residual term remains (relative weight 2^-8S); vs the oracle at 4096² r=32."""
+    m = n = 4096
+    r = 32
+    rng = np.random.default_rng(71)
+    lam = rng.random((m, r)) @ rng.random((r, n)) / 4.0
+    x = rng.poisson(lam).astype(np.float64)
+    assert np.all(x == np.round(x)) and x.max() < 256
+    w0, h0 = port.random_init(m, n, r, 72)
+    ref = port.run_dense(x, w0, h0, preset("e-ahals-hp3", max_outer_iterations=6))
+    rec = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 6), E.TimingMode.none)
+    assert min(ctx.digit_levels) >= 6, ctx.digit_levels   # INT8-digit products, not the DMMA fallback
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
+    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
