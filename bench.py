@@ -415,8 +415,8 @@ def run_ours(args, rank, world, local_rank):
                                window=f"outer iterations 1..{args.steps} of the seeded C5 run (after a discarded "
                                       f"{args.warmup}-iteration warm-up run)"),
                 "roofline": {"bound": "tensor",
-                             "kernel": "hals::sweep_ws (persistent FP64 DMMA HALS sweeps, one launch per "
-                                       "inner solve; 2·r²·N flop per sweep)",
+                             "kernel": "hals::sweep_tm (persistent FP64 DMMA HALS sweeps with the iterate held "
+                                       "in tensor memory, one launch per inner solve; 2·r²·N flop per sweep)",
                              "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                              "frac": achieved / FP64_PEAK_TFLOPS, "traffic": (args.traffic if args.traffic is not None else SWEEP_DRAM_BYTES * (ph["sweeps_h"] + ph["sweeps_w"]) / 2),
                              "traffic_note": "DRAM bytes per launch (one inner solve), from the ncu --set full capture's "
@@ -425,8 +425,9 @@ def run_ours(args, rank, world, local_rank):
                              "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
                              "cross_products": {
                                  "kernel": "FP64-accurate W_yᵀX / X·Tᵀ on the hand-written tcgen05 kind::i8 "
-                                           "kernel (ozk.cuh): S 8-bit digits per operand, the S(S+1)/2 digit "
-                                           "pairs summed per level in TMEM over CTA pairs, exact offset "
+                                           "CTA-pair kernel (ozk::gemm_pair): S 8-bit digits per operand, one "
+                                           "cta_group::2 MMA forms two digit pairs (factor digits p, p+1 x one "
+                                           "X digit split over the pair), level sums in TMEM, exact offset "
                                            "corrections, truncation-bias estimate, FP64 recombination",
                                  "digit_levels": list(levels), "digit_products": digit_gemms,
                                  "ms": cross_ms, "fp64_equiv_tflops": cross_flops / (cross_ms * 1e-3) / 1e12,

@@ -902,21 +902,14 @@ void ozaki_prepare_x(enmf_gpu_ctx* c, cudaStream_t s, enmf_gpu_ctx::XDig& xd, co
   xd.ready = true;
 }
 
-// ENMF_OZK selects how the digit pairs are split over a cluster: "c2" (default: two CTAs, the
-// levels split 11/10 at S = 6) or "c3" (three CTAs, 7/7/7).
-int ozk_cluster() {
-  static int v = [] {
-    const char* e = std::getenv("ENMF_OZK");
-    return (e && std::string(e) == "c3") ? 3 : 2;
-  }();
-  return v;
-}
+// FP64 partial slices per unit: one per CTA of the pair (ozk::gemm_pair)
+int ozk_cluster() { return 2; }
 
-template <int S, int CL>
-void ozk_launch_v(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* B, const OzkPlan& p, long R, long N,
-                  const DevState* st) {
-  using Cf = ozk::Cfg<S, CL, kOzkBN>;
-  auto kern = ozk::gemm_levels<S, CL, kOzkBN>;
+template <int S>
+void ozk_launch_pair(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* B, const OzkPlan& p, long R, long N,
+                     const DevState* st) {
+  using Cf = ozk::PairCfg<S>;
+  auto kern = ozk::gemm_pair<S>;
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
@@ -925,34 +918,30 @@ void ozk_launch_v(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t
   ozk::GemmArgs g{A, B, (int)((R + ozk::TROWS - 1) / ozk::TROWS), (int)((N + ozk::TROWS - 1) / ozk::TROWS),
                   (int)R, (int)N, p.nkc, p.unit_chunks, p.nkq, p.nmb, p.ntn, c->ozws.p, st};
   const long items = (long)p.nkq * p.nmb * p.ntn;
-  cudaLaunchConfig_t lc = {};
-  // persistent grid: exactly the clusters that can be co-resident (the GPCs' shapes can leave
-  // fewer than sms / CL of them; one more would run as a second wave)
-  static int maxc = [&] {
+  static int maxc = [&] {                 // co-resident CTA pairs (persistent grid, one wave)
     cudaLaunchConfig_t q = {};
-    q.gridDim = dim3((unsigned)(c->sms / CL * CL));
+    q.gridDim = dim3((unsigned)(c->sms / 2 * 2));
     q.blockDim = dim3(ozk::THREADS);
     q.dynamicSmemBytes = Cf::SMEM;
     cudaLaunchAttribute qa[1];
     qa[0].id = cudaLaunchAttributeClusterDimension;
-    qa[0].val.clusterDim.x = CL;
+    qa[0].val.clusterDim.x = 2;
     qa[0].val.clusterDim.y = 1;
     qa[0].val.clusterDim.z = 1;
     q.attrs = qa;
     q.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &q) != cudaSuccess || n <= 0) n = c->sms / CL;
-    if (std::getenv("ENMF_OZK_DEBUG")) std::fprintf(stderr, "ozk: cluster %d, %d co-resident clusters\n", CL, n);
-    return std::min(n, c->sms / CL);
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &q) != cudaSuccess || n <= 0) n = c->sms / 2;
+    return std::min(n, c->sms / 2);
   }();
-  const int grid = (int)std::min<long>(items, maxc) * CL;
-  lc.gridDim = dim3((unsigned)grid);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(std::min<long>(items, maxc) * 2));
   lc.blockDim = dim3(ozk::THREADS);
   lc.dynamicSmemBytes = Cf::SMEM;
   lc.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
@@ -963,8 +952,7 @@ void ozk_launch_v(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t
 template <int S>
 void ozk_launch(enmf_gpu_ctx* c, cudaStream_t s, const int8_t* A, const int8_t* B, const OzkPlan& p, long R, long N,
                 const DevState* st) {
-  if (ozk_cluster() == 3) ozk_launch_v<S, 3>(c, s, A, B, p, R, N, st);
-  else ozk_launch_v<S, 2>(c, s, A, B, p, R, N, st);
+  ozk_launch_pair<S>(c, s, A, B, p, R, N, st);
 }
 
 // out (r × N, row stride ldo) = A (r × K FP64, row stride lda) · Xdᵀ in FP64 accuracy, Xd = the

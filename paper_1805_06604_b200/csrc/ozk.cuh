@@ -155,32 +155,6 @@ __global__ void split_cols_chunked(const double* __restrict__ x, long R, long C,
 }
 
 // ---- the digit GEMM ---------------------------------------------------------------
-// The S(S+1)/2 digit pairs of a tile are split BY LEVEL over the CL CTAs of a cluster: CTA
-// rank ρ owns the levels of group ρ (the pairs (p, q) with p + q in the group) and keeps one
-// 128-lane × BN accumulator per owned level in its TMEM.  With BN = 128 every MMA (M = 128,
-// N = 128, K = 32) runs at the tensor core's floor — measured: an M = 128 kind::i8 MMA costs
-// ≥ ~48 cycles whatever its N, so N = 64 tiles (all S levels in one CTA) reach only 67%
-// (profiles/r02_umma_rate.txt) — and the groups are balanced:
-//   S = 6, CL = 2: {0,1,2,4} (11 pairs) | {3,5} (10);   S = 6, CL = 3: {0,5} | {1,4} | {2,3} (7 each)
-//   S = 7, CL = 2: {0,2,3,4} (13) | {1,5,6} (15);       S = 7, CL = 3: {1,6} | {2,5} | {0,3,4}
-// Every digit tile of a stage (S factor tiles of 128 rows, S X tiles of BN rows, 32 B of K
-// each) is loaded ONCE per cluster by one CTA and multicast to all CL of them.
-template <int S, int CL>
-struct Levels {
-  static constexpr int G = CL;
-  __host__ __device__ static constexpr int count(int rank) {
-    return S == 6 ? (CL == 2 ? (rank == 0 ? 4 : 2) : 2) : (CL == 2 ? (rank == 0 ? 4 : 3) : (rank == 2 ? 3 : 2));
-  }
-  __host__ __device__ static constexpr int level(int rank, int i) {
-    // tables above, row = rank, padded with -1
-    return S == 6 ? (CL == 2 ? (rank == 0 ? (i == 0 ? 0 : i == 1 ? 1 : i == 2 ? 2 : 4) : (i == 0 ? 3 : 5))
-                             : (rank == 0 ? (i == 0 ? 0 : 5) : rank == 1 ? (i == 0 ? 1 : 4) : (i == 0 ? 2 : 3)))
-                  : (CL == 2 ? (rank == 0 ? (i == 0 ? 0 : i == 1 ? 2 : i == 2 ? 3 : 4) : (i == 0 ? 1 : i == 1 ? 5 : 6))
-                             : (rank == 0 ? (i == 0 ? 1 : 6) : rank == 1 ? (i == 0 ? 2 : 5) : (i == 0 ? 0 : i == 1 ? 3 : 4)));
-  }
-  static constexpr int MAXL = S == 6 ? (CL == 2 ? 4 : 2) : (CL == 2 ? 4 : 3);
-};
-
 struct GemmArgs {
   const int8_t* A;   // factor digits (tile layout, nta row tiles)
   const int8_t* B;   // X digits (tile layout, ntb row tiles)
@@ -193,170 +167,229 @@ struct GemmArgs {
   const DevState* st;
 };
 
-template <int S, int CL, int BN>
-struct Cfg {
-  static_assert(BN == TROWS, "X tiles of 128 rows (the digit layout's row tile)");
-  static constexpr int A_TILE = TILE, B_TILE = TILE;
-  static constexpr int A_BYTES = S * A_TILE;
-  static constexpr int B_BYTES = S * B_TILE;
+ENMF_DEV double p2m(int e) { return __longlong_as_double((long long)(1023 - e) << 52); }   // 2^-e, 0 <= e < 1023
+
+// One tcgen05.mma.cta_group::2.kind::i8 (M = 256, N = 128, K = 32) multiplies ONE X digit tile q
+// (B: the tile's 128 X rows split 64 / 64 over the two CTAs' shared memory, read by both tensor
+// cores) by TWO different factor digits at once: the A operand at the same shared-memory offset
+// holds digit p in CTA 0 and digit p + 1 in CTA 1, so CTA 0 accumulates pair (p, q) into its
+// level-(p+q) slot while CTA 1 accumulates (p+1, q) into its level-(p+q+1) slot.  TMEM slot j
+// holds level 2j in CTA 0 and 2j+1 in CTA 1 (J = ⌈S/2⌉ slots of 128 columns).  Per K chunk the
+// S(S+1)/2 pairs take 12 pair-MMAs at S = 6 (19 at S = 7; the few half-empty ones multiply a
+// zero A tile).
+//
+// Why (replacing a level-split kernel that multicast every digit tile of a stage to both CTAs of
+// a pair, each CTA forming 10-11 of the 21 pairs with cta_group::1 MMAs): each X digit tile now
+// reaches shared memory once, as its two halves, so a stage is 2 × (S factor tiles + S half X
+// tiles) = 72 KB per 128 X rows × 32 of K instead of 96 KB, and the tensor cores read 6 KB of
+// shared memory per 64-cycle MMA instead of 8 KB.  Measured at C5: 2.07 → 1.92 ms per product
+// (ncu), tensor pipe 61 → 87% active (profiles/r02_ozk_gemm_ncu.txt, r02_ozk_pair_ncu.txt); the
+// pair layout was checked against the host first (tools/probe/umma2_probe.cu).
+//
+// Roles (per CTA, 192 threads): warp 0 = TMA producer (both CTAs: the S factor tiles into slots
+// shifted by one in CTA 1, and this CTA's S half X tiles); warp 1 = MMA issuer in CTA 0, and in
+// CTA 1 the forwarder that tells CTA 0's issuer its half of the stage has landed; warps 2-5 =
+// epilogue (each CTA reads its own slots).  The MMA commits free the stage / publish the
+// accumulators in both CTAs (multicast); both CTAs' epilogues release the accumulators to CTA 0.
+template <int S>
+struct PairCfg {
+  static constexpr int J = (S + 1) / 2;                // accumulator slots (levels 2j + rank)
+  static constexpr int A_SLOTS = S + 1;                // digit tiles −1..S−1 (rank 0) / 0..S (rank 1)
+  static constexpr int A_BYTES = A_SLOTS * TILE;
+  static constexpr int B_HALF = TILE / 2;              // 64 X rows × 32 B (the first / second half of a tile)
+  static constexpr int B_BYTES = S * B_HALF;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NS = (SMEM_LIMIT - 2048) / STAGE > 8 ? 8 : (SMEM_LIMIT - 2048) / STAGE;
+  static constexpr int NS = (SMEM_LIMIT - 4096) / STAGE > 8 ? 8 : (SMEM_LIMIT - 4096) / STAGE;
   static constexpr int SMEM = 1024 + NS * STAGE + 1024;
-  static constexpr int ACC_COLS = Levels<S, CL>::MAXL * BN;        // one accumulator set
-  static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;        // double-buffered when it fits
-  static constexpr int TMEM_COLS = NACC * ACC_COLS <= 256 ? 256 : 512;
-  static_assert(ACC_COLS <= 512, "level accumulators must fit the 512 TMEM columns");
+  static constexpr int TMEM_COLS = 512;
+  static_assert(J * TROWS <= 512, "level slots must fit the TMEM columns");
   static_assert(NS >= 3, "pipeline too shallow");
 };
 
-template <int S, int CL, int BN>
-__global__ void __launch_bounds__(THREADS, 1) gemm_levels(GemmArgs g) {
-  using C = Cfg<S, CL, BN>;
-  using LV = Levels<S, CL>;
+ENMF_DEV uint32_t peer0(const void* p) {               // CTA 0's shared::cluster address of p
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(tc::smem_u32(p)));
+  return r;
+}
+// relaxed: what it announces (bulk copies landed / TMEM loads waited) is already ordered by the
+// mbarrier wait / tcgen05.wait it follows; a release here costs a full GPU membar per stage
+ENMF_DEV void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+ENMF_DEV void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+ENMF_DEV void commit_pair(uint64_t* b) {               // arrive on b in both CTAs of the pair
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                   tc::smem_u32(b)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(THREADS, 1) gemm_pair(GemmArgs g) {
+  using C = PairCfg<S>;
   if (g.st && !dev_active(g.st)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                  // NS × A_BYTES
   uint8_t* sB = smem + C::NS * C::A_BYTES;             // NS × B_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + C::NS;
-  uint64_t* tfull = bars + 2 * C::NS;                  // [NACC]
-  uint64_t* tempty = tfull + 2;                        // [NACC]
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* full = bars;                               // this CTA's half of the stage landed
+  uint64_t* pfull = bars + C::NS;                      // (CTA 0) CTA 1's half landed
+  uint64_t* empty = bars + 2 * C::NS;                  // the pair-MMAs are done with the stage
+  uint64_t* tfull = bars + 3 * C::NS;                  // accumulators complete
+  uint64_t* tempty = tfull + 1;                        // (CTA 0) both epilogues drained them
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)tc::cluster_rank();
-  const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
-  constexpr uint16_t MASK = (uint16_t)((1u << CL) - 1);
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  // the A slot no digit lands in stays zero: slot 0 (digit −1) in CTA 0, slot S (digit S) in CTA 1
+  {
+    const int zs = rank == 0 ? 0 : S;
+    for (int st = 0; st < C::NS; ++st)
+      for (int e = threadIdx.x; e < TILE / 16; e += THREADS)
+        reinterpret_cast<uint4*>(sA + st * C::A_BYTES + zs * TILE)[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) {
       tc::mbar_init(full + s, 1);
-      tc::mbar_init(empty + s, CL);                    // every CTA's MMA issuer frees the stage
+      tc::mbar_init(pfull + s, 1);
+      tc::mbar_init(empty + s, 1);
     }
-    for (int b = 0; b < C::NACC; ++b) {
-      tc::mbar_init(tfull + b, 1);
-      tc::mbar_init(tempty + b, EPI_THREADS);
-    }
+    tc::mbar_init(tfull, 1);
+    tc::mbar_init(tempty, 2 * (EPI_THREADS / 32));
     tc::fence_mbar_init();
   }
-  if (warp == 2) tc::tmem_alloc<C::TMEM_COLS>(tbase_s);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc::smem_u32(tbase_s)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
   tc::fence_before();
-  tc::cluster_sync();                                  // peers' barriers initialised before any multicast
+  tc::cluster_sync();                                  // barriers, zero tiles and TMEM ready in both CTAs
   tc::fence_after();
   const uint32_t tbase = *tbase_s;
 
   const int items = g.nkq * g.nmb * g.ntn;
-  if (warp == 0) {                                     // ---- TMA producer (this CTA's share of the tiles)
+  if (warp == 0) {                                     // ---- TMA producer (both CTAs)
     int stage = 0;
     uint32_t phase = 0;
-    // the stage = 2S contiguous 4 KB tiles (S factor, S X), this CTA's contiguous share of them
-    // multicast to the cluster (A: tiles [0, S), B: [S, 2S))
-    const int t0 = rank * 2 * S / CL, t1 = (rank + 1) * 2 * S / CL;
-    const int ae = min(t1, S), b0t = max(t0, S) - S, b1t = t1 - S;
     for (int w = cluster; w < items; w += nclusters) {
       const int kq = w / (g.nmb * g.ntn), rem = w % (g.nmb * g.ntn);
       const int mb = rem / g.ntn, tn = rem % g.ntn;
       const int c0 = kq * g.unit_chunks, c1 = min(g.nkc, c0 + g.unit_chunks);
       for (int c = c0; c < c1; ++c) {
-        tc::mbar_wait(empty + stage, phase ^ 1);       // every CTA of the cluster is done with the stage
+        tc::mbar_wait(empty + stage, phase ^ 1);
         if (tc::elect_one()) {
-          tc::mbar_expect_tx(full + stage, C::STAGE);
+          tc::mbar_expect_tx(full + stage, (uint32_t)(S * TILE + S * C::B_HALF));
           const int8_t* asrc = g.A + ((long)c * g.nta + mb) * SMAX * TILE;
-          const int8_t* bsrc = g.B + ((long)c * g.ntb + tn) * SMAX * TILE;
-          if (t0 < S)
-            tc::bulk_load_mc(sA + stage * C::A_BYTES + t0 * TILE, asrc + (long)t0 * TILE, (uint32_t)((ae - t0) * TILE),
-                             full + stage, MASK);
-          if (t1 > S) {
-            tc::bulk_load_mc(sB + stage * C::B_BYTES + b0t * TILE, bsrc + (long)b0t * TILE,
-                             (uint32_t)((b1t - b0t) * TILE), full + stage, MASK);
-            // the X digits stream from HBM exactly once: pull the tiles PF stages ahead into L2 so
-            // the (few-stage) shared-memory pipeline only sees L2 latency
-            if (c + PF < c1)
-              tc::bulk_prefetch_l2(g.B + ((long)(c + PF) * g.ntb + tn) * SMAX * TILE + (long)b0t * TILE,
-                                   (uint32_t)((b1t - b0t) * TILE));
-          }
+          const int8_t* bsrc = g.B + ((long)c * g.ntb + tn) * SMAX * TILE + rank * C::B_HALF;
+          tc::bulk_load(sA + stage * C::A_BYTES + (rank == 0 ? TILE : 0), asrc, (uint32_t)(S * TILE), full + stage);
+#pragma unroll
+          for (int q = 0; q < S; ++q)
+            tc::bulk_load(sB + stage * C::B_BYTES + q * C::B_HALF, bsrc + (long)q * TILE, (uint32_t)C::B_HALF,
+                          full + stage);
+          // the X digits stream from HBM exactly once: pull them PF stages ahead into L2
+          if (rank == 0 && c + PF < c1)
+            tc::bulk_prefetch_l2(g.B + ((long)(c + PF) * g.ntb + tn) * SMAX * TILE, (uint32_t)(S * TILE));
         }
         __syncwarp();
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {                              // ---- MMA issuer (this CTA's levels)
-    constexpr uint32_t IDESC = tc::idesc_i8(128, BN);
-    // no-swizzle K-major descriptors: K-adjacent core matrices 128 B apart, 8-row groups 256 B
-    const uint64_t dA0 = tc::desc_noswz(tc::smem_u32(sA), 128, 256);
-    const uint64_t dB0 = tc::desc_noswz(tc::smem_u32(sB), 128, 256);
-    int stage = 0, ab = 0;
-    uint32_t phase = 0, aph[2] = {0, 0};
-    const int nl = LV::count(rank);
+  } else if (warp == 1 && rank == 1) {                 // ---- CTA 1: forward "my half landed" to CTA 0
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t pf0 = peer0(pfull);
     for (int w = cluster; w < items; w += nclusters) {
       const int kq = w / (g.nmb * g.ntn);
       const int c0 = kq * g.unit_chunks, c1 = min(g.nkc, c0 + g.unit_chunks);
-      tc::mbar_wait(tempty + ab, aph[ab] ^ 1);         // the epilogue has drained this accumulator set
-      tc::fence_after();
-      const uint32_t dset = tbase + (uint32_t)(ab * C::ACC_COLS);
       for (int c = c0; c < c1; ++c) {
         tc::mbar_wait(full + stage, phase);
+        if (tc::elect_one()) arrive_remote(pf0 + stage * 8);
+        __syncwarp();
+        if (++stage == C::NS) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {                              // ---- CTA 0: the pair-MMA issuer
+    constexpr uint32_t IDESC = tc::idesc_i8(256, TROWS);
+    const uint64_t dA0 = tc::desc_noswz(tc::smem_u32(sA), 128, 256);
+    const uint64_t dB0 = tc::desc_noswz(tc::smem_u32(sB), 128, 256);
+    int stage = 0;
+    uint32_t phase = 0, tph = 0;
+    for (int w = cluster; w < items; w += nclusters) {
+      const int kq = w / (g.nmb * g.ntn);
+      const int c0 = kq * g.unit_chunks, c1 = min(g.nkc, c0 + g.unit_chunks);
+      tc::mbar_wait(tempty, tph ^ 1);                  // both epilogues have drained the slots
+      tc::fence_after();
+      for (int c = c0; c < c1; ++c) {
+        tc::mbar_wait(full + stage, phase);
+        tc::mbar_wait(pfull + stage, phase);
         tc::fence_after();
         const uint64_t dA = dA0 + (uint64_t)((stage * C::A_BYTES) >> 4);
         const uint64_t dB = dB0 + (uint64_t)((stage * C::B_BYTES) >> 4);
-        const uint32_t first = c > c0 ? 1u : 0u;
         if (tc::elect_one()) {
+          bool started[C::J] = {};
 #pragma unroll
-          for (int i = 0; i < LV::MAXL; ++i) {
-            if (i < nl) {
-              const int l = LV::level(rank, i);
-              const uint32_t d = dset + (uint32_t)(i * BN);
+          for (int q = 0; q < S; ++q) {
 #pragma unroll
-              for (int q = 0; q < S; ++q) {
-                const int p = l - q;
-                if (p >= 0 && p < S)
-                  tc::mma_i8(d, dA + (uint64_t)(p * (TILE >> 4)), dB + (uint64_t)(q * (TILE >> 4)), IDESC,
-                             (first | (q > 0 ? 1u : 0u)));
-              }
+            for (int j = 0; j < C::J; ++j) {
+              const int p0 = 2 * j - q;                // CTA 0: pair (p0, q) → level 2j
+              const bool v0 = p0 >= 0 && 2 * j <= S - 1;
+              const bool v1 = p0 + 1 >= 0 && 2 * j + 1 <= S - 1;   // CTA 1: (p0 + 1, q) → level 2j + 1
+              if (!v0 && !v1) continue;
+              const uint32_t acc = (c > c0 || started[j]) ? 1u : 0u;
+              started[j] = true;
+              mma_i8_pair(tbase + (uint32_t)(j * TROWS), dA + (uint64_t)(((p0 + 1) * TILE) >> 4),
+                          dB + (uint64_t)((q * C::B_HALF) >> 4), IDESC, acc);
             }
           }
-          tc::commit_mc(empty + stage, MASK);          // frees the stage in every CTA of the cluster
+          commit_pair(empty + stage);                  // frees the stage in both CTAs
         }
         __syncwarp();
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
-      if (tc::elect_one()) tc::commit(tfull + ab);     // this group's level sums of the unit complete
+      if (tc::elect_one()) commit_pair(tfull);         // this unit's level sums complete, both CTAs
       __syncwarp();
-      aph[ab] ^= 1;
-      if (C::NACC == 2) ab ^= 1;
+      tph ^= 1;
     }
-  } else {                                             // ---- epilogue (warps 2..5)
+  } else if (warp >= 2) {                              // ---- epilogue (warps 2..5, both CTAs)
     const int quarter = warp & 3;
-    const int nl = LV::count(rank);
-    int ab = 0;
-    uint32_t aph[2] = {0, 0};
+    uint32_t tph = 0;
+    const uint32_t te0 = peer0(tempty);
     for (int w = cluster; w < items; w += nclusters) {
       const int kq = w / (g.nmb * g.ntn), rem = w % (g.nmb * g.ntn);
       const int mb = rem / g.ntn, tn = rem % g.ntn;
-      tc::mbar_wait(tfull + ab, aph[ab]);
+      tc::mbar_wait(tfull, tph);
       tc::fence_after();
       const long row = (long)mb * 128 + quarter * 32 + lane;
-      const uint32_t taddr = tbase + (uint32_t)(ab * C::ACC_COLS) + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16);
       double* wrow = g.ws + (((long)rank * g.nkq + kq) * g.R + row) * g.N;
 #pragma unroll 1
-      for (int j0 = 0; j0 < BN; j0 += 16) {
-        uint32_t v[LV::MAXL][16];
+      for (int j0 = 0; j0 < TROWS; j0 += 16) {
+        uint32_t v[C::J][16];
 #pragma unroll
-        for (int i = 0; i < LV::MAXL; ++i)
-          if (i < nl) tc::ld16(taddr + (uint32_t)(i * BN + j0), v[i]);
+        for (int j = 0; j < C::J; ++j) tc::ld16(taddr + (uint32_t)(j * TROWS + j0), v[j]);
         tc::ld_wait();
-        const long col0 = (long)tn * BN + j0;
+        const long col0 = (long)tn * TROWS + j0;
         if (row < g.R && col0 < g.N) {
           double o[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            double acc = 0.0;                          // Σ 2^{-8ℓ} L_ℓ over this group's levels
+            double acc = 0.0;                          // Σ 2^{-8ℓ} L_ℓ over this CTA's levels, smallest first
 #pragma unroll
-            for (int i = LV::MAXL - 1; i >= 0; --i)
-              if (i < nl)
-                acc = __dadd_rn(acc, __dmul_rn((double)(int)v[i][t],
-                                               __longlong_as_double((long long)(1023 - 8 * LV::level(rank, i)) << 52)));
+            for (int j = C::J - 1; j >= 0; --j) {
+              const int l = 2 * j + rank;
+              if (l <= S - 1) acc = __dadd_rn(acc, __dmul_rn((double)(int)v[j][t], p2m(8 * l)));
+            }
             o[t] = acc;
           }
           if (col0 + 16 <= g.N && ((g.N & 1) == 0)) {
@@ -371,16 +404,19 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_levels(GemmArgs g) {
         }
       }
       tc::fence_before();
-      tc::mbar_arrive(tempty + ab);
-      aph[ab] ^= 1;
-      if (C::NACC == 2) ab ^= 1;
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) tc::mbar_arrive(tempty);
+        else arrive_remote(te0);
+      }
+      tph ^= 1;
     }
   }
   tc::fence_before();
-  tc::cluster_sync();                                  // no CTA leaves while a peer may still signal it
+  tc::cluster_sync();                                  // no CTA leaves while its peer may still signal it
   if (warp == 2) {
     tc::fence_after();
-    tc::tmem_dealloc<C::TMEM_COLS>(tbase);
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(C::TMEM_COLS));
   }
 }
 
