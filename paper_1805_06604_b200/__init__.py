@@ -8,7 +8,7 @@ from .enmf import (  # noqa: F401
     BetaSchedule, CacheStale, Context, DEFAULT_ALGORITHMS, DegenerateColumn, DeviceError, FactorPair,
     InnerSolver, InvalidArgument, IterationRecord, NoConvergence, NonFiniteIterate, Precision, RunRecord,
     SolverConfig, TimingMode, active_set_solve, algorithm_config, cross_wx, cross_xht, default_context,
-    fast_error, frob_norm_sq, gram, hals_solve, IoError, optimal_beta_linesearch, ZeroDirection, ParseError, run, run_batch, run_csr, UnsupportedFormat,
+    fast_error, frob_norm_sq, gram, hals_solve, IoError, optimal_beta_linesearch, ZeroDirection, ParseError, run, run_batch, run_batch_packed, batch_eligible, run_csr, UnsupportedFormat,
     update_beta,
 )
 from . import data, suite  # noqa: F401  (enmf/data.hpp formats + generators; enmf/bench.hpp suites)

@@ -69,6 +69,7 @@ EXPORTS = [
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
     "enmf_gpu_dist_finalize", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
     "enmf_gpu_optimal_beta_linesearch", "enmf_gpu_optimal_beta_linesearch_csr",
+    "enmf_gpu_batch_eligible", "enmf_gpu_run_batch_dense",
     # data formats and generators (csrc/io.cpp)
     "enmf_io_read_matrix_market", "enmf_io_read_dense_csv", "enmf_io_matrix_shape",
     "enmf_io_matrix_offsets", "enmf_io_matrix_col_indices", "enmf_io_matrix_values",
@@ -113,6 +114,9 @@ def load() -> C.CDLL:
     L.enmf_gpu_run_dense.argtypes = [vp, dp, sz, sz, dp, dp] + run_tail
     L.enmf_gpu_run_csr.argtypes = [vp, dp, dp, dp, sz, sz, sz, dp, dp] + run_tail
     L.enmf_gpu_load_dense.argtypes = [vp, dp, sz, sz, C.c_int]
+    L.enmf_gpu_batch_eligible.argtypes = [sz, sz, sz, C.POINTER(CConfig)]
+    L.enmf_gpu_run_batch_dense.argtypes = [vp, sz, dp, sz, sz, dp, dp, sz, C.POINTER(CConfig), C.POINTER(CIter), sz,
+                                           ip, ip, dp, dp, dp]
     L.enmf_gpu_load_csr.argtypes = [vp, dp, dp, dp, sz, sz, sz]
     L.enmf_gpu_solve.argtypes = [vp, dp, dp, sz, C.c_int, C.POINTER(CConfig), C.POINTER(CIter), sz,
                                  C.POINTER(sz), dp, dp, C.POINTER(C.c_double)]

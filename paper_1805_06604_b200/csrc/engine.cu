@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "batch.cuh"
 #include "bpp.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
@@ -212,6 +213,10 @@ void set_attrs_once() {
   big((const void*)hals::sweep_ws<64, true>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128, true>, hals::ws_smem_bytes<128>());
   big((const void*)hals::sweep_tm<128>, hals::tm_smem_bytes<128>());
+  big((const void*)batch::run<8>, batch::smem_bytes());
+  big((const void*)batch::run<16>, batch::smem_bytes());
+  big((const void*)batch::run<24>, batch::smem_bytes());
+  big((const void*)batch::run<32>, batch::smem_bytes());
   big((const void*)hals::sweep_fast<16, 1>, hals::smem_bytes<16, 1>());
   big((const void*)hals::sweep_fast<32, 1>, hals::smem_bytes<32, 1>());
   big((const void*)hals::sweep_fast<32, 2>, hals::smem_bytes<32, 2>());
@@ -1772,3 +1777,4 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }   // io.cpp'
 #include "dist_api.inc"
 #include "cabi.inc"
 #include "kernels_api.inc"
+#include "batch_api.inc"

@@ -498,16 +498,79 @@ def run(x, w0, h0, cfg: SolverConfig, timing: TimingMode = TimingMode.wall) -> R
     return default_context().run(x, w0, h0, cfg, timing)
 
 
+def batch_eligible(m: int, n: int, r: int, cfg: SolverConfig, timing: TimingMode = TimingMode.none) -> bool:
+    """Whether runs of this shape and config fit the packed one-CTA-per-run kernel (batch.cuh):
+    FP64 HALS presets, r <= 32, max(m, n)·(r rounded up to 8) <= 9216, no wall budget, no timing records."""
+    if timing != TimingMode.none:
+        return False
+    c = cfg.to_c(timing)
+    return L.load().enmf_gpu_batch_eligible(m, n, r, C.byref(c)) == L.ENMF_OK
+
+
+def run_batch_packed(problems, cfg: SolverConfig, device: int = -1) -> List[RunRecord]:
+    """Many independent runs of one shape in ONE launch (csrc/batch.cuh): one CTA per run
+    executes every step() of enmf::run (engine.hpp:447-521) for its problem.  The FP64 product
+    arithmetic of the engine (parity bars, not bit equality); raises the first failing run's
+    error as `run` would."""
+    problems = [(_f64(x, "x"), _f64(w0, "w0"), _f64(h0, "h0")) for x, w0, h0 in problems]
+    if not problems:
+        return []
+    m, n = problems[0][0].shape
+    r = problems[0][1].shape[1]
+    for x, w0, h0 in problems:
+        if x.shape != (m, n) or w0.shape != (m, r) or h0.shape != (r, n):
+            raise InvalidArgument("run_batch_packed: every problem must have the same shapes")
+    B = len(problems)
+    xs = np.ascontiguousarray(np.stack([p[0] for p in problems]))
+    ws = np.ascontiguousarray(np.stack([p[1] for p in problems]))
+    hs = np.ascontiguousarray(np.stack([p[2] for p in problems]))
+    c = cfg.to_c(TimingMode.none)
+    cap = int(cfg.max_outer_iterations) + 1
+    iters = (L.CIter * (cap * B))()
+    nit = np.zeros(B, dtype=np.int32)
+    st = np.zeros(B, dtype=np.int32)
+    wo = np.empty((B, m, r))
+    ho = np.empty((B, r, n))
+    nx = np.empty(B)
+    ctx = default_context() if device < 0 else Context(device)
+    ip = C.POINTER(C.c_int32)
+    _check(L.load().enmf_gpu_run_batch_dense(ctx._h, B, _p(xs), m, n, _p(ws), _p(hs), r, C.byref(c), iters, cap,
+                                             nit.ctypes.data_as(ip), st.ctypes.data_as(ip), _p(wo), _p(ho),
+                                             _p(nx)))
+    for b in range(B):
+        if st[b] != L.ENMF_OK:
+            raise _ERRORS.get(int(st[b]), RuntimeError)(f"run_batch_packed: run {b} failed (status {int(st[b])})")
+    arr = C.cast(iters, C.POINTER(L.CIter))
+    out = []
+    for b in range(B):
+        recs = _records(arr[b * cap:(b + 1) * cap], min(int(nit[b]), cap))
+        out.append(RunRecord(recs, FactorPair(wo[b], ho[b]), float(nx[b])))
+    return out
+
+
 def run_batch(problems, cfg: SolverConfig, timing: TimingMode = TimingMode.none, streams: int = 8,
-              device: int = -1) -> List[RunRecord]:
+              device: int = -1, backend: str = "auto") -> List[RunRecord]:
     """Many independent dense runs in flight together — the paper protocol's dataset × init
     grid that the reference runs on a host thread pool (run_suite, bench.hpp:233-294).
 
-    `problems` is a sequence of (x, w0, h0).  Up to `streams` contexts, each with its own
-    CUDA stream and iteration graph, take a problem each; all K iterations of every context
-    are enqueued before any result is read, so the GPU overlaps the small launch-bound runs.
-    Every run is computed exactly as `run` would compute it on its own."""
+    backend "packed" (the default for eligible batches: same shapes, FP64 HALS presets,
+    r <= 32, small problems — batch_eligible): one launch, one CTA per run (run_batch_packed).
+    backend "streams": up to `streams` contexts, each with its own CUDA stream and iteration
+    graph, take a problem each; all K iterations of every context are enqueued before any
+    result is read.  Every run is then computed exactly as `run` computes it on its own (this
+    is the path for fp64_exact, BPP and large problems)."""
     problems = list(problems)
+    if backend not in ("auto", "packed", "streams"):
+        raise InvalidArgument("run_batch: backend must be auto, packed or streams")
+    if backend != "streams" and problems:
+        x0, w00 = problems[0][0], problems[0][1]
+        same = all(np.shape(p[0]) == np.shape(x0) and np.shape(p[1]) == np.shape(w00) for p in problems)
+        ok = same and np.ndim(x0) == 2 and batch_eligible(np.shape(x0)[0], np.shape(x0)[1], np.shape(w00)[1], cfg,
+                                                          timing)
+        if ok:
+            return run_batch_packed(problems, cfg, device)
+        if backend == "packed":
+            raise InvalidArgument("run_batch: this batch does not fit the packed kernel (batch_eligible)")
     pool = [Context(device) for _ in range(max(1, min(streams, len(problems))))]
     out: List[RunRecord] = []
     try:

@@ -53,7 +53,7 @@ def test_concurrent_streams_bitwise(ctx):
     cfg = _cfg("e-ahals-hp3", 6)
     alone = [ctx.run(x, w, h, cfg, E.TimingMode.none) for x, w, h in probs]
     for rep in range(2):
-        batch = E.run_batch(probs, cfg, streams=4)
+        batch = E.run_batch(probs, cfg, streams=4, backend="streams")
         for a, b in zip(alone, batch):
             _same(a, b)
 

@@ -510,7 +510,7 @@ def test_run_batch_matches_single_runs(ctx, golden):
     rng = np.random.default_rng(3)
     probs = [(inp["x"], rng.random((200, 20)), rng.random((20, 200))) for _ in range(6)]
     cfg = _cfg("e-ahals-hp3", 60)
-    batch = E.run_batch(probs, cfg, streams=4)
+    batch = E.run_batch(probs, cfg, streams=4, backend="streams")
     for (x, w0, h0), rb in zip(probs, batch):
         rs = ctx.run(x, w0, h0, cfg, E.TimingMode.none)
         assert np.array_equal(rb.column("error"), rs.column("error"))
