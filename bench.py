@@ -52,9 +52,11 @@ METRIC = "E-A-HALS outer iters/sec + % roofline, 32768² r=128, 1/2/4/8 B200"
 UNIT = "outer_iters/s"
 FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.txt)
 FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry)"
-# DRAM bytes per HALS sweep inside sweep_ws: ncu --set full of one 24-sweep launch,
-# dram__bytes_read.sum + dram__bytes_write.sum = 72.60 + 9.72 MB (profiles/r01_sweep_ncu.txt)
-SWEEP_DRAM_BYTES = (72.602368e6 + 9.718272e6) / 24
+# DRAM bytes per HALS sweep inside sweep_tm: ncu --set full of one 16-sweep launch at C5 size,
+# dram__bytes_read.sum + dram__bytes_write.sum = 79.12 + 403.19 MB (profiles/r02_sweep_tm_ncu.txt):
+# mostly the rows written back each sweep (H ping-pongs between two buffers for the speculative
+# stall decision), C and H reads stay L2-resident
+SWEEP_DRAM_BYTES = (79.117568e6 + 403.19104e6) / 16
 # tcgen05 kind::i8 floor: 8192 MAC/cycle/SM (M=128 N≥128 MMAs at 100% in profiles/r02_umma_rate.txt)
 INT8_PEAK_TOPS = 2 * 8192 * 148 * 1.965e9 / 1e12
 INT8_PEAK_SRC = ("tcgen05 kind::i8 MMA floor measured on this pool's B200 (M=128, N>=128: 8192 MAC/cycle/SM, "
@@ -420,8 +422,8 @@ def run_ours(args, rank, world, local_rank):
                              "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                              "frac": achieved / FP64_PEAK_TFLOPS, "traffic": (args.traffic if args.traffic is not None else SWEEP_DRAM_BYTES * (ph["sweeps_h"] + ph["sweeps_w"]) / 2),
                              "traffic_note": "DRAM bytes per launch (one inner solve), from the ncu --set full capture's "
-                                             "bytes per sweep (profiles/r01_sweep_ncu.txt); H and C stay L2-resident, "
-                                             "so it is far below the 2·r·N·8 B per sweep the iterate and C occupy",
+                                             "bytes per sweep (profiles/r02_sweep_tm_ncu.txt, 30 MB: the rows written "
+                                             "back each sweep); the iterate lives in tensor memory and C is read from L2",
                              "peak_source": FP64_PEAK_SRC, "launch_ms": sweep_ms / 2,
                              "cross_products": {
                                  "kernel": "FP64-accurate W_yᵀX / X·Tᵀ on the hand-written tcgen05 kind::i8 "

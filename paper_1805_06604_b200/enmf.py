@@ -507,11 +507,11 @@ def batch_eligible(m: int, n: int, r: int, cfg: SolverConfig, timing: TimingMode
     return L.load().enmf_gpu_batch_eligible(m, n, r, C.byref(c)) == L.ENMF_OK
 
 
-def run_batch_packed(problems, cfg: SolverConfig, device: int = -1) -> List[RunRecord]:
+def run_batch_packed(problems, cfg: SolverConfig, device: int = -1, raise_errors: bool = True) -> List[RunRecord]:
     """Many independent runs of one shape in ONE launch (csrc/batch.cuh): one CTA per run
     executes every step() of enmf::run (engine.hpp:447-521) for its problem.  The FP64 product
-    arithmetic of the engine (parity bars, not bit equality); raises the first failing run's
-    error as `run` would."""
+    arithmetic of the engine (parity bars, not bit equality).  raise_errors: raise the first
+    failing run's error as `run` would; otherwise that run's slot holds the exception."""
     problems = [(_f64(x, "x"), _f64(w0, "w0"), _f64(h0, "h0")) for x, w0, h0 in problems]
     if not problems:
         return []
@@ -537,12 +537,15 @@ def run_batch_packed(problems, cfg: SolverConfig, device: int = -1) -> List[RunR
     _check(L.load().enmf_gpu_run_batch_dense(ctx._h, B, _p(xs), m, n, _p(ws), _p(hs), r, C.byref(c), iters, cap,
                                              nit.ctypes.data_as(ip), st.ctypes.data_as(ip), _p(wo), _p(ho),
                                              _p(nx)))
-    for b in range(B):
-        if st[b] != L.ENMF_OK:
-            raise _ERRORS.get(int(st[b]), RuntimeError)(f"run_batch_packed: run {b} failed (status {int(st[b])})")
     arr = C.cast(iters, C.POINTER(L.CIter))
     out = []
     for b in range(B):
+        if st[b] != L.ENMF_OK:
+            err = _ERRORS.get(int(st[b]), RuntimeError)(f"run_batch_packed: run {b} failed (status {int(st[b])})")
+            if raise_errors:
+                raise err
+            out.append(err)
+            continue
         recs = _records(arr[b * cap:(b + 1) * cap], min(int(nit[b]), cap))
         out.append(RunRecord(recs, FactorPair(wo[b], ho[b]), float(nx[b])))
     return out

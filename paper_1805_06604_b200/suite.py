@@ -33,7 +33,7 @@ from typing import List, Optional, Sequence, Union
 import numpy as np
 
 from . import data as io
-from .enmf import (Context, FactorPair, InvalidArgument, Precision, RunRecord, SolverConfig, TimingMode,
+from .enmf import (batch_eligible, run_batch_packed, Context, FactorPair, InvalidArgument, Precision, RunRecord, SolverConfig, TimingMode,
                    UnsupportedFormat, algorithm_config)
 
 __all__ = [
@@ -210,9 +210,14 @@ def _load(ctx: Context, x: DataMatrix) -> None:
         ctx.load(x)
 
 
-def run_suite(spec: SuiteSpec) -> SuiteResults:
+def run_suite(spec: SuiteSpec, backend: str = "auto") -> SuiteResults:
     """enmf::run_suite (bench.hpp:233-294) on the GPU.  Load-time errors (a missing or
-    malformed file) are raised; per-run failures are captured in RunResult."""
+    malformed file) are raised; per-run failures are captured in RunResult.
+
+    backend "auto": the (dataset, algorithm) groups that fit the packed kernel (dense data, FP64
+    HALS presets, small shapes, no wall clock — enmf.batch_eligible) run all their inits in ONE
+    launch (run_batch_packed); everything else — and every run with backend "streams" — runs
+    on per-run device contexts, computed exactly as `run` computes it."""
     spec.validate()
     data = [load_dataset(d) for d in spec.datasets]
     wall = spec.wall_timing or math.isfinite(spec.budget.max_seconds)
@@ -228,13 +233,42 @@ def run_suite(spec: SuiteSpec) -> SuiteResults:
                                            io.mix_seed(spec.base_seed, d, i))
         return inits[(d, i)]
 
-    width = max(1, min(total, spec.threads if spec.threads > 0 else 16))
+    done = set()
+    if backend == "auto" and tm == TimingMode.none:
+        for d in range(nd):
+            if isinstance(data[d], io.SparseMatrix):
+                continue
+            x = np.asarray(data[d], dtype=np.float64)
+            for a in range(na):
+                cfg = replace(spec.algorithms[a].config, max_outer_iterations=spec.budget.max_iterations,
+                              max_seconds=spec.budget.max_seconds, precision=spec.precision)
+                try:
+                    cfg.validate()
+                except Exception:  # noqa: BLE001 — reported per run by the general path
+                    continue
+                if not batch_eligible(x.shape[0], x.shape[1], spec.datasets[d].r, cfg):
+                    continue
+                ts = [(d * ni + i) * na + a for i in range(ni)]
+                res = run_batch_packed([(x, *init_pair(d, i)) for i in range(ni)], cfg, spec.device,
+                                       raise_errors=False)
+                for i, (t, rec) in enumerate(zip(ts, res)):
+                    rr = out.runs[t]
+                    rr.dataset_index, rr.init_index, rr.algorithm_index = d, i, a
+                    if isinstance(rec, Exception):
+                        rr.failed, rr.failure = True, str(rec)
+                    else:
+                        rr.record = rec
+                    done.add(t)
+    todo = [t for t in range(total) if t not in done]
+    if not todo:
+        return out
+    width = max(1, min(len(todo), spec.threads if spec.threads > 0 else 16))
     pool = [Context(spec.device) for _ in range(width)]
     loaded: List[Optional[int]] = [None] * width
     try:
-        for start in range(0, total, width):
+        for start in range(0, len(todo), width):
             live = []
-            for k, t in enumerate(range(start, min(total, start + width))):
+            for k, t in enumerate(todo[start:start + width]):
                 a, i, d = t % na, (t // na) % ni, t // (na * ni)
                 rr = out.runs[t]
                 rr.dataset_index, rr.init_index, rr.algorithm_index = d, i, a
