@@ -146,7 +146,7 @@ int enmf_gpu_run_csr(enmf_gpu_ctx* ctx, const uint64_t* offsets, const uint64_t*
  * bench.hpp:233-294): `count` independent dense runs of one shape and config, one CTA per
  * run, one launch for the whole batch.  x: count × m × n, w0: count × m × r, h0: count × r × n
  * (row-major, packed); outputs per run: iters_cap records (iters + b·iters_cap), n_iters[b],
- * status[b] (ENMF_* of that run), w_out, h_out, norm_x.  FP64 HALS presets only (r <= 32,
+ * status[b] (ENMF_* of that run), w_out, h_out, norm_x.  FP64 product mode, HALS or BPP (r <= 32,
  * max(m, n)·⌈r⌉₈ <= 9216, no wall budget): enmf_gpu_batch_eligible says whether a config fits. */
 int enmf_gpu_batch_eligible(size_t m, size_t n, size_t r, const enmf_gpu_config* cfg);
 int enmf_gpu_run_batch_dense(enmf_gpu_ctx* ctx, size_t count, const double* x, size_t m, size_t n,

@@ -1,4 +1,4 @@
-// batch.cuh — packed many-small-runs backend: one CTA runs a WHOLE E-A-HALS / A-HALS run
+// batch.cuh — packed many-small-runs backend: one CTA runs a WHOLE E-A-HALS / A-HALS / E-ANLS run
 // (enmf::run, engine.hpp:447-521, every step() of it, engine.hpp:309-440) for one small dense
 // problem, and one launch runs a batch of them (the paper protocol's dataset × init × algorithm
 // grid, bench.hpp:233-294, which the reference spreads over host threads).
@@ -19,13 +19,17 @@
 //   error                     fast_error in double-double (||X||², ⟨W_n, X Tᵀ⟩, ⟨W_nᵀW_n, T Tᵀ⟩)
 //   decide                    NaN guard, restart / accept, update_beta, IterationRecord
 //
+//   (E-ANLS) H / W update     active_set_solve by the engine's lane-parallel BPP column solver
+//                             (bpp::solve_fast_col), six warps, a column per warp at a time
+//
 // Arithmetic is the engine's FP64 product mode (FMA, parallel reduction orders): parity with
 // the reference is the north_star bar (identical restarts, errors within 1e-9, factors within
-// 1e-6; tests/test_gpu_batch.py), not bit equality — the bitwise fp64_exact mode and BPP inner
-// solvers run on the per-run engine (run_batch streams).  Limits: r ≤ 32, max(m, n)·⌈r⌉₈ ≤
+// 1e-6; tests/test_gpu_batch.py), not bit equality — the bitwise fp64_exact mode runs on the
+// per-run engine (run_batch streams).  Limits: r ≤ 32, max(m, n)·⌈r⌉₈ ≤
 // SMEM_FACTOR doubles (the staged factor), no wall-clock budget.
 #pragma once
 
+#include "bpp.cuh"
 #include "common.cuh"
 
 namespace batch {
@@ -291,6 +295,89 @@ ENMF_DEV int hals(const double* G, const double* Gz, const double* dinv, const d
   return sweep;
 }
 
+// E-ANLS inner solve (active_set_solve, nnls.hpp:259-406) on r × N columns: G (R × R, shared),
+// C and the warm start H0 (r × N, global) → Hn.  bpp::solve_fast_col — the per-run engine's
+// lane-parallel FP64 solver — on BPP_WARPS warps, one column per warp at a time, its shared
+// memory carved out of WS (the staged-factor region, free after the cross product).  Returns
+// the solve rounds (max over the columns); *status = NoConvergence past 3·r·N exchanges
+// (nnls.hpp:384-387), NonFiniteIterate on a non-finite solution (engine.hpp:334-337).
+constexpr int BPP_WARPS = 6;
+constexpr int BPP_LDL = 33;
+__host__ __device__ constexpr int bpp_ws_doubles() {
+  return 32 * BPP_LDL + BPP_WARPS * (32 * BPP_LDL + 64) + (BPP_WARPS * 32 + 528 + 1) / 2;
+}
+static_assert(bpp_ws_doubles() <= SMEM_FACTOR, "BPP workspace must fit the staged-factor region");
+
+template <int R>
+ENMF_DEV int bpp_solve(const double* G, const double* C, const double* H0, double* Hn, int r, int N, double* WS,
+                       double* red, int* status) {
+  __shared__ unsigned long long sh_exch;
+  __shared__ int sh_rounds, sh_nf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();                                   // WS (the staged factor) no longer read
+  const int gld = r | 1;
+  double* Gs = WS;
+  int* fidx0 = reinterpret_cast<int*>(WS + 32 * BPP_LDL + BPP_WARPS * (32 * BPP_LDL + 64));
+  int* tri = fidx0 + BPP_WARPS * 32;
+  for (int e = threadIdx.x; e < r * r; e += NT) Gs[(e / r) * gld + e % r] = G[(e / r) * R + e % r];
+  bpp::fill_tri(tri, NW);
+  double mx = 0.0;                                   // max |C| (feas_tol, nnls.hpp:271)
+  for (long e = threadIdx.x; e < (long)r * N; e += NT) {
+    const double v = fabs(C[e]);
+    mx = mx < v ? v : mx;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0) red[warp] = mx;
+  if (threadIdx.x == 0) {
+    sh_exch = 0;
+    sh_rounds = 0;
+    sh_nf = 0;
+  }
+  __syncthreads();
+  double cmax = red[0];
+  for (int i = 1; i < NW; ++i) cmax = fmax(cmax, red[i]);
+  double maxd = 0.0;
+  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * gld + i]) ? Gs[i * gld + i] : maxd;
+  __syncthreads();
+  if (warp < BPP_WARPS) {
+    bpp::FastCol w;
+    w.Gs = Gs;
+    w.gld = gld;
+    w.tri = tri;
+    w.L = WS + 32 * BPP_LDL + warp * (32 * BPP_LDL + 64);
+    w.xs = w.L + 32 * BPP_LDL;
+    w.invd = w.xs + 32;
+    w.fidx = fidx0 + warp * 32;
+    w.r = r;
+    w.pivot_floor = 1e-12 * maxd;
+    w.feas_tol = 1e-12 * (1.0 + cmax);
+    w.limit = 3ULL * (unsigned long long)r * (unsigned long long)N;
+    unsigned long long ex = 0;
+    int rounds = 0, nf = 0;
+    for (int col = warp; col < N; col += BPP_WARPS) {
+      unsigned long long e;
+      int f;
+      const int sv = bpp::solve_fast_col(w, C, H0, Hn, N, col, &e, &f);
+      ex += e;
+      rounds = max(rounds, sv);
+      nf |= f;
+    }
+    if (lane == 0) {
+      atomicAdd(&sh_exch, ex);
+      atomicMax(&sh_rounds, rounds);
+      atomicOr(&sh_nf, nf);
+    }
+  }
+  __syncthreads();
+  const unsigned long long ex = sh_exch;
+  const int rounds = sh_rounds, nf = sh_nf;
+  __syncthreads();
+  if (ex > 3ULL * (unsigned long long)r * (unsigned long long)N) *status = ENMF_NO_CONVERGENCE;
+  else if (nf) *status = ENMF_NON_FINITE;
+  return rounds;
+}
+
 // out = next + beta (next − prev) [+ clamp]
 ENMF_DEV void extrap(const double* next, const double* prev, double beta, long count, bool clamp, double* out) {
   for (long i = threadIdx.x; i < count; i += NT) {
@@ -420,9 +507,17 @@ __global__ void __launch_bounds__(NT, 2) run(Args a) {
       if (gram_reinit<R>(WyT, SF, r, m, GA, cfg.reinit_seed, 2 * k, &mod, sh_bad, &sh_nb)) { status = ENMF_NO_CONVERGENCE; break; }
       if (threadIdx.x == 0 && mod) rec.reinit_events |= 1;
       cross_wx<R>(SF, X, m, n, r, CH);
-      hals_prep<R>(GA, r, GZ, DI);                       // (ends with a block barrier: CH complete)
-      rec.inner_h_count = hals<R>(GA, GZ, DI, CH, Hy, Hn, r, n, a.ms_h, cfg.inner_stall_fraction, red, &nf);
-      if (__syncthreads_or(nf)) { status = ENMF_NON_FINITE; break; }
+      if (cfg.inner_h == ENMF_INNER_EXACT) {
+        int st = ENMF_OK;
+        __syncthreads();                                 // CH complete
+        rec.inner_h_count = bpp_solve<R>(GA, CH, Hy, Hn, r, n, SF, red, &st);
+        if (st != ENMF_OK) { status = st; break; }
+      } else {
+        hals_prep<R>(GA, r, GZ, DI);                     // (ends with a block barrier: CH complete)
+        rec.inner_h_count = hals<R>(GA, GZ, DI, CH, Hy, Hn, r, n, a.ms_h, cfg.inner_stall_fraction, red, &nf);
+        if (__syncthreads_or(nf)) { status = ENMF_NON_FINITE; break; }
+      }
+      __syncthreads();
       // ---- early H extrapolation (:340-347)
       if (cfg.hp >= 2) {
         if (ext) extrap(Hn, H, b, rn, cfg.hp == 3, Hy);
@@ -437,10 +532,18 @@ __global__ void __launch_bounds__(NT, 2) run(Args a) {
       if (gram_reinit<R>(T, SF, r, n, GB, cfg.reinit_seed, 2 * k + 1, &mod, sh_bad, &sh_nb)) { status = ENMF_NO_CONVERGENCE; break; }
       if (threadIdx.x == 0 && mod) rec.reinit_events |= 2;
       cross_txt<R>(SF, X, m, n, r, P);
-      hals_prep<R>(GB, r, GZ, DI);
-      nf = 0;
-      rec.inner_w_count = hals<R>(GB, GZ, DI, P, WyT, WnT, r, m, a.ms_w, cfg.inner_stall_fraction, red, &nf);
-      if (__syncthreads_or(nf)) { status = ENMF_NON_FINITE; break; }
+      if (cfg.inner_w == ENMF_INNER_EXACT) {
+        int st = ENMF_OK;
+        __syncthreads();                                 // P complete
+        rec.inner_w_count = bpp_solve<R>(GB, P, WyT, WnT, r, m, SF, red, &st);
+        if (st != ENMF_OK) { status = st; break; }
+      } else {
+        hals_prep<R>(GB, r, GZ, DI);
+        nf = 0;
+        rec.inner_w_count = hals<R>(GB, GZ, DI, P, WyT, WnT, r, m, a.ms_w, cfg.inner_stall_fraction, red, &nf);
+        if (__syncthreads_or(nf)) { status = ENMF_NON_FINITE; break; }
+      }
+      __syncthreads();
       // ---- W extrapolation, late H extrapolation (:386-397)
       if (ext) extrap(WnT, WT, b, rm, false, WyT);
       else copy(WnT, rm, WyT);

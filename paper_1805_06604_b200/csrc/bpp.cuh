@@ -288,32 +288,34 @@ constexpr int fast_smem_bytes() {
   return 32 * 33 * 8 + WPB * (32 * 33 * 8 + 2 * 32 * 8 + 32 * 4) + 528 * 4;
 }
 
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
-  if (a.st && !dev_active(a.st)) return;
+// One column of the lane-parallel solver (FP64 product mode, r <= 32): warp-collective.
+// Gs: the Gram in shared memory (row stride gld); tri: the lower-triangle index table; L (32 ×
+// LDL), xs, invd (32 each), fidx (32 ints): this warp's shared-memory workspace.  C, H0 (read)
+// and H (written) are r × N with row stride ld.  Returns the solve count; *exch / *nf get the
+// column's exchanges and non-finite flag.
+struct FastCol {
+  const double* Gs;
+  int gld;
+  const int* tri;
+  double* L;
+  double* xs;
+  double* invd;
+  int* fidx;
+  int r;
+  double pivot_floor, feas_tol;
+  unsigned long long limit;
+};
+ENMF_DEV int solve_fast_col(const FastCol& w, const double* C, const double* H0, double* H, long ld, long col,
+                            unsigned long long* exch_out, int* nf_out) {
   constexpr int LDL = 33;
-  extern __shared__ __align__(16) double sm[];
-  const int r = a.r;
-  double* Gs = sm;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* L = sm + 32 * LDL + warp * (32 * LDL + 64);
-  double* xs = L + 32 * LDL;
-  double* invd = xs + 32;
-  int* fidx = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + warp * 32;
-  int* tri = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + WPB * 32;
-
-  const int gld = r | 1;
-  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
-  for (int u = warp; u < 32; u += WPB)           // tri[u(u+1)/2 + v] = (u, v), v <= u
-    for (int v = lane; v <= u; v += 32) tri[u * (u + 1) / 2 + v] = (u << 8) | v;
-  __syncthreads();
-
-  double maxd = 0.0;
-  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * gld + i]) ? Gs[i * gld + i] : maxd;
-  const double pivot_floor = __dmul_rn(1e-12, maxd);
-  const double feas_tol = __dmul_rn(1e-12, __dadd_rn(1.0, *a.cmax));
-  const unsigned long long limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
-
+  const int lane = threadIdx.x & 31;
+  const int r = w.r, gld = w.gld;
+  const double* Gs = w.Gs;
+  const int* tri = w.tri;
+  double* L = w.L;
+  double* xs = w.xs;
+  double* invd = w.invd;
+  int* fidx = w.fidx;
   // lane-parallel triangular solves with the factor in L: b (lane q's entry) -> A⁻¹ b
   auto chol_solve = [&](double b, int f) -> double {
     for (int i = 0; i < f; ++i) {                 // forward: L y = b
@@ -328,117 +330,153 @@ __global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
     }
     return b;
   };
-
-  for (int col = blockIdx.x * WPB + warp; col < a.N; col += gridDim.x * WPB) {
-    unsigned long long P = 0, B = 0;
-    if (lane < r && a.H0[(long)lane * a.ld + col] > 0.0) P = 1ULL << lane;
-    P = warp_or64(P);
-    int best_inf = 0x7fffffff, backup = 3, solves = 0;
-    unsigned long long exch = 0;
-    int f = 0, fq = 0;
-    double x = 0.0;                               // lane q: x_F[q]
-    for (;;) {
-      ++solves;
-      // passive index list (ascending) from the mask
-      const unsigned pm = (unsigned)P;
-      if (lane < r && ((pm >> lane) & 1u)) fidx[__popc(pm & ((1u << lane) - 1u))] = lane;
-      f = __popc(pm);
-      __syncwarp();
-      // factor G[F,F] right-looking, dropping and banning variables whose pivot collapses
-      for (;;) {
-        if (f == 0) break;
-        fq = lane < f ? fidx[lane] : 0;
-        if (lane < f)
-          for (int k = 0; k <= lane; ++k) L[lane * LDL + k] = Gs[fq * gld + fidx[k]];
-        __syncwarp();
-        int bad = f;
-        for (int j = 0; j < f; ++j) {
-          const double d = L[j * LDL + j];
-          if (!(d > pivot_floor)) { bad = j; break; }
-          const double ljj = sqrt(d), inv = 1.0 / ljj;
-          double lqj = 0.0;
-          if (lane > j && lane < f) {
-            lqj = L[lane * LDL + j] * inv;
-            L[lane * LDL + j] = lqj;
-          }
-          if (lane == j) {
-            L[j * LDL + j] = ljj;
-            invd[j] = inv;
-          }
-          __syncwarp();
-          // trailing update L[i][k] -= L[i][j]·L[k][j] (j < k <= i < f), the triangle's entries
-          // dealt round-robin over the lanes (balanced, instead of one row per lane)
-          const int nt = f - j - 1;
-          for (int e = lane; e < nt * (nt + 1) / 2; e += 32) {
-            const int uv = tri[e], i = j + 1 + (uv >> 8), k = j + 1 + (uv & 255);
-            L[i * LDL + k] = fma(-L[i * LDL + j], L[k * LDL + j], L[i * LDL + k]);
-          }
-          (void)lqj;
-          __syncwarp();
-        }
-        if (bad == f) break;
-        if (lane == 0) {
-          const int var = fidx[bad];
-          P &= ~(1ULL << var);
-          B |= 1ULL << var;
-          for (int q = bad; q + 1 < f; ++q) fidx[q] = fidx[q + 1];
-        }
-        P = __shfl_sync(0xffffffffu, P, 0);
-        B = __shfl_sync(0xffffffffu, B, 0);
-        --f;
-        __syncwarp();
-      }
-      fq = lane < f ? fidx[lane] : 0;
-      // x_F = chol_solve(C[F,col]) + one refinement step
-      x = 0.0;
-      if (f > 0) {
-        const double df = lane < f ? a.C[(long)fq * a.ld + col] : 0.0;
-        x = chol_solve(df, f);
-        xs[lane] = x;
-        __syncwarp();
-        double rs = df;
-        if (lane < f)
-          for (int b2 = 0; b2 < f; ++b2) rs = fma(-Gs[fq * gld + fidx[b2]], xs[b2], rs);
-        rs = chol_solve(rs, f);
-        x += rs;
-        __syncwarp();
-        xs[lane] = x;
-        __syncwarp();
-      }
-      // infeasible set
-      unsigned long long I = 0;
-      if (lane < f && x < -feas_tol) I = 1ULL << fq;
-      if (lane < r && !(((P | B) >> lane) & 1ULL)) {
-        double y = -a.C[(long)lane * a.ld + col];
-        for (int q = 0; q < f; ++q) y = fma(Gs[lane * gld + fidx[q]], xs[q], y);
-        if (y < -feas_tol) I |= 1ULL << lane;
-      }
-      I = warp_or64(I);
-      if (I == 0) break;
-      if (++exch > limit) break;
-      const int count = __popcll(I);
-      if (count < best_inf) {
-        best_inf = count;
-        backup = 3;
-        P ^= I;
-      } else if (backup > 0) {
-        --backup;
-        P ^= I;
-      } else {
-        P ^= 1ULL << (63 - __clzll(I));
-      }
-      __syncwarp();
-    }
-    // write the column: max(x, 0) on F, zero elsewhere
-    int nf = 0;
-    if (lane < r) a.H[(long)lane * a.ld + col] = 0.0;
+  unsigned long long P = 0, B = 0;
+  if (lane < r && H0[(long)lane * ld + col] > 0.0) P = 1ULL << lane;
+  P = warp_or64(P);
+  int best_inf = 0x7fffffff, backup = 3, solves = 0;
+  unsigned long long exch = 0;
+  int f = 0, fq = 0;
+  double x = 0.0;                               // lane q: x_F[q]
+  for (;;) {
+    ++solves;
+    // passive index list (ascending) from the mask
+    const unsigned pm = (unsigned)P;
+    if (lane < r && ((pm >> lane) & 1u)) fidx[__popc(pm & ((1u << lane) - 1u))] = lane;
+    f = __popc(pm);
     __syncwarp();
-    if (lane < f) {
-      const double v = x > 0.0 ? x : 0.0;
-      a.H[(long)fq * a.ld + col] = v;
-      nf = !isfinite(v);
+    // factor G[F,F] right-looking, dropping and banning variables whose pivot collapses
+    for (;;) {
+      if (f == 0) break;
+      fq = lane < f ? fidx[lane] : 0;
+      if (lane < f)
+        for (int k = 0; k <= lane; ++k) L[lane * LDL + k] = Gs[fq * gld + fidx[k]];
+      __syncwarp();
+      int bad = f;
+      for (int j = 0; j < f; ++j) {
+        const double d = L[j * LDL + j];
+        if (!(d > w.pivot_floor)) { bad = j; break; }
+        const double ljj = sqrt(d), inv = 1.0 / ljj;
+        if (lane > j && lane < f) L[lane * LDL + j] = L[lane * LDL + j] * inv;
+        if (lane == j) {
+          L[j * LDL + j] = ljj;
+          invd[j] = inv;
+        }
+        __syncwarp();
+        // trailing update L[i][k] -= L[i][j]·L[k][j] (j < k <= i < f), the triangle's entries
+        // dealt round-robin over the lanes (balanced, instead of one row per lane)
+        const int nt = f - j - 1;
+        for (int e = lane; e < nt * (nt + 1) / 2; e += 32) {
+          const int uv = tri[e], i = j + 1 + (uv >> 8), k = j + 1 + (uv & 255);
+          L[i * LDL + k] = fma(-L[i * LDL + j], L[k * LDL + j], L[i * LDL + k]);
+        }
+        __syncwarp();
+      }
+      if (bad == f) break;
+      if (lane == 0) {
+        const int var = fidx[bad];
+        P &= ~(1ULL << var);
+        B |= 1ULL << var;
+        for (int q = bad; q + 1 < f; ++q) fidx[q] = fidx[q + 1];
+      }
+      P = __shfl_sync(0xffffffffu, P, 0);
+      B = __shfl_sync(0xffffffffu, B, 0);
+      --f;
+      __syncwarp();
     }
-    nf = __any_sync(0xffffffffu, nf);
+    fq = lane < f ? fidx[lane] : 0;
+    // x_F = chol_solve(C[F,col]) + one refinement step
+    x = 0.0;
+    if (f > 0) {
+      const double df = lane < f ? C[(long)fq * ld + col] : 0.0;
+      x = chol_solve(df, f);
+      xs[lane] = x;
+      __syncwarp();
+      double rs = df;
+      if (lane < f)
+        for (int b2 = 0; b2 < f; ++b2) rs = fma(-Gs[fq * gld + fidx[b2]], xs[b2], rs);
+      rs = chol_solve(rs, f);
+      x += rs;
+      __syncwarp();
+      xs[lane] = x;
+      __syncwarp();
+    }
+    // infeasible set
+    unsigned long long I = 0;
+    if (lane < f && x < -w.feas_tol) I = 1ULL << fq;
+    if (lane < r && !(((P | B) >> lane) & 1ULL)) {
+      double y = -C[(long)lane * ld + col];
+      for (int q = 0; q < f; ++q) y = fma(Gs[lane * gld + fidx[q]], xs[q], y);
+      if (y < -w.feas_tol) I |= 1ULL << lane;
+    }
+    I = warp_or64(I);
+    if (I == 0) break;
+    if (++exch > w.limit) break;
+    const int count = __popcll(I);
+    if (count < best_inf) {
+      best_inf = count;
+      backup = 3;
+      P ^= I;
+    } else if (backup > 0) {
+      --backup;
+      P ^= I;
+    } else {
+      P ^= 1ULL << (63 - __clzll(I));
+    }
+    __syncwarp();
+  }
+  // write the column: max(x, 0) on F, zero elsewhere
+  int nf = 0;
+  if (lane < r) H[(long)lane * ld + col] = 0.0;
+  __syncwarp();
+  if (lane < f) {
+    const double v = x > 0.0 ? x : 0.0;
+    H[(long)fq * ld + col] = v;
+    nf = !isfinite(v);
+  }
+  *nf_out = __any_sync(0xffffffffu, nf);
+  *exch_out = exch;
+  __syncwarp();
+  return solves;
+}
+
+// the index table of solve_fast_col's balanced trailing update: tri[u(u+1)/2 + v] = (u, v), v <= u < 32
+ENMF_DEV void fill_tri(int* tri, int nwarps) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int u = warp; u < 32; u += nwarps)
+    for (int v = lane; v <= u; v += 32) tri[u * (u + 1) / 2 + v] = (u << 8) | v;
+}
+
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) solve_fast(Args a) {
+  if (a.st && !dev_active(a.st)) return;
+  constexpr int LDL = 33;
+  extern __shared__ __align__(16) double sm[];
+  const int r = a.r;
+  double* Gs = sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  FastCol w;
+  w.L = sm + 32 * LDL + warp * (32 * LDL + 64);
+  w.xs = w.L + 32 * LDL;
+  w.invd = w.xs + 32;
+  w.fidx = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + warp * 32;
+  int* tri = reinterpret_cast<int*>(sm + 32 * LDL + WPB * (32 * LDL + 64)) + WPB * 32;
+  const int gld = r | 1;
+  for (int e = threadIdx.x; e < r * r; e += WPB * 32) Gs[(e / r) * gld + e % r] = a.G[e];
+  fill_tri(tri, WPB);
+  __syncthreads();
+  double maxd = 0.0;
+  for (int i = 0; i < r; ++i) maxd = (maxd < Gs[i * gld + i]) ? Gs[i * gld + i] : maxd;
+  w.Gs = Gs;
+  w.gld = gld;
+  w.tri = tri;
+  w.r = r;
+  w.pivot_floor = __dmul_rn(1e-12, maxd);
+  w.feas_tol = __dmul_rn(1e-12, __dadd_rn(1.0, *a.cmax));
+  w.limit = 3ULL * (unsigned long long)r * (unsigned long long)a.N;
+  for (int col = blockIdx.x * WPB + warp; col < a.N; col += gridDim.x * WPB) {
+    unsigned long long exch;
+    int nf;
+    const int solves = solve_fast_col(w, a.C, a.H0, a.H, a.ld, col, &exch, &nf);
     if (lane == 0) {
       if (exch) atomicAdd(a.exchanges, exch);
       atomicMax(a.rounds, solves);

@@ -24,8 +24,8 @@
 #include <string>
 #include <vector>
 
-#include "batch.cuh"
 #include "bpp.cuh"
+#include "batch.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
 #include "hals.cuh"

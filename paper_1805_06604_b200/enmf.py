@@ -500,7 +500,8 @@ def run(x, w0, h0, cfg: SolverConfig, timing: TimingMode = TimingMode.wall) -> R
 
 def batch_eligible(m: int, n: int, r: int, cfg: SolverConfig, timing: TimingMode = TimingMode.none) -> bool:
     """Whether runs of this shape and config fit the packed one-CTA-per-run kernel (batch.cuh):
-    FP64 HALS presets, r <= 32, max(m, n)·(r rounded up to 8) <= 9216, no wall budget, no timing records."""
+    FP64 (HALS or BPP inner solvers), r <= 32, max(m, n)·(r rounded up to 8) <= 9216, no wall budget, no timing
+    records."""
     if timing != TimingMode.none:
         return False
     c = cfg.to_c(timing)
@@ -556,12 +557,12 @@ def run_batch(problems, cfg: SolverConfig, timing: TimingMode = TimingMode.none,
     """Many independent dense runs in flight together — the paper protocol's dataset × init
     grid that the reference runs on a host thread pool (run_suite, bench.hpp:233-294).
 
-    backend "packed" (the default for eligible batches: same shapes, FP64 HALS presets,
-    r <= 32, small problems — batch_eligible): one launch, one CTA per run (run_batch_packed).
+    backend "packed" (the default for eligible batches: same shapes, FP64, r <= 32, small
+    problems — batch_eligible): one launch, one CTA per run (run_batch_packed).
     backend "streams": up to `streams` contexts, each with its own CUDA stream and iteration
     graph, take a problem each; all K iterations of every context are enqueued before any
     result is read.  Every run is then computed exactly as `run` computes it on its own (this
-    is the path for fp64_exact, BPP and large problems)."""
+    is the path for fp64_exact and large problems)."""
     problems = list(problems)
     if backend not in ("auto", "packed", "streams"):
         raise InvalidArgument("run_batch: backend must be auto, packed or streams")

@@ -215,7 +215,7 @@ def run_suite(spec: SuiteSpec, backend: str = "auto") -> SuiteResults:
     malformed file) are raised; per-run failures are captured in RunResult.
 
     backend "auto": the (dataset, algorithm) groups that fit the packed kernel (dense data, FP64
-    HALS presets, small shapes, no wall clock — enmf.batch_eligible) run all their inits in ONE
+    presets (HALS or BPP), small shapes, no wall clock — enmf.batch_eligible) run all their inits in ONE
     launch (run_batch_packed); everything else — and every run with backend "streams" — runs
     on per-run device contexts, computed exactly as `run` computes it."""
     spec.validate()

@@ -13,15 +13,19 @@ from test_gpu_parity import _cfg, _cfg_from_meta, assert_parity
 pytestmark = pytest.mark.gpu
 
 
-def _check_run(rec, ref):
-    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3])
-    assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
-    assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
+def _check_run(rec, ref, kappa=False):
+    assert_parity(rec, ref[0]["error"], ref[0]["restarted"], ref[1], ref[2], ref[3], kappa=kappa)
+    if not kappa:   # below the noise floor (noise-free E-ANLS) BPP's rounds follow rounding noise
+        assert np.array_equal(rec.column("inner_h_count"), ref[0]["inner_h"])
+        assert np.array_equal(rec.column("inner_w_count"), ref[0]["inner_w"])
 
 
-@pytest.mark.parametrize("alg", ["e-ahals-hp3", "e-ahals-hp1", "ahals"])
+@pytest.mark.parametrize("alg", ["e-ahals-hp3", "e-ahals-hp1", "ahals", "e-anls-hp1", "e-anls-hp3", "anls"])
 def test_c1_batch_vs_oracle(port, golden, alg):
-    """Config 1 (200 × 200, r = 20, 200 outer iterations) for 24 initialisations in one launch."""
+    """Config 1 (200 × 200, r = 20, 200 outer iterations) for 24 initialisations in one launch,
+    every preset of the protocol (E-ANLS: BPP inner solves; on this noise-free data its error
+    reaches ~5e-7·||X||, so the per-iteration bar includes the trace identity's own
+    cancellation bound, as in test_gpu_parity.test_c1_fp64_parity_vs_reference)."""
     x = golden.load("c1_inputs")["x"]
     probs = []
     for s in range(24):
@@ -31,7 +35,7 @@ def test_c1_batch_vs_oracle(port, golden, alg):
     out = E.run_batch(probs, cfg, backend="packed")
     for (xx, w0, h0), rec in zip(probs[::5], out[::5]):          # every 5th run vs the oracle
         ref = port.run_dense(xx, w0, h0, preset(alg, max_outer_iterations=200))
-        _check_run(rec, ref)
+        _check_run(rec, ref, kappa="anls" in alg)
 
 
 @pytest.mark.parametrize("variant", [dict(hp=2), dict(hp=1, literal_hp1_order=True),
@@ -50,8 +54,9 @@ def test_config_variants_vs_oracle(port, golden, variant):
     _check_run(rec, ref)
 
 
+@pytest.mark.parametrize("alg", ["e-ahals-hp3", "e-anls-hp1"])
 @pytest.mark.parametrize("shape", [(150, 260, 13), (280, 40, 32), (37, 301, 1), (64, 280, 32), (90, 113, 7)])
-def test_shapes_vs_oracle(port, shape):
+def test_shapes_vs_oracle(port, shape, alg):
     """Ragged shapes: n > 256 columns per CTA (thread loops), r = 1 and the r = 32 maximum."""
     m, n, r = shape
     rng = np.random.default_rng(m + n + r)
@@ -60,9 +65,9 @@ def test_shapes_vs_oracle(port, shape):
     # r = 1 converges within ~5 iterations; past that the errors tie to the last bit and the
     # restart decisions are rounding noise in any summation order
     it = 4 if r == 1 else 40
-    out = E.run_batch_packed(probs, _cfg("e-ahals-hp3", it))
+    out = E.run_batch_packed(probs, _cfg(alg, it))
     for (xx, w0, h0), rec in zip(probs, out):
-        _check_run(rec, port.run_dense(xx, w0, h0, preset("e-ahals-hp3", max_outer_iterations=it)))
+        _check_run(rec, port.run_dense(xx, w0, h0, preset(alg, max_outer_iterations=it)))
 
 
 def test_dead_column_reinit(golden):
@@ -94,12 +99,15 @@ def test_eligibility_and_errors(golden):
     rng = np.random.default_rng(1)
     assert E.batch_eligible(200, 200, 20, _cfg("e-ahals-hp3", 10))
     assert not E.batch_eligible(200, 200, 33, _cfg("e-ahals-hp3", 10))                 # r > 32
-    assert not E.batch_eligible(200, 200, 20, _cfg("e-anls-hp1", 10))                  # BPP
+    assert E.batch_eligible(200, 200, 20, _cfg("e-anls-hp1", 10))                      # BPP, r <= 32
     assert not E.batch_eligible(200, 200, 20, _cfg("e-ahals-hp3", 10, E.Precision.fp64_exact))
     with pytest.raises(E.InvalidArgument):
         E.run_batch([(x, rng.random((200, 33)), rng.random((33, 200)))], _cfg("e-ahals-hp3", 5), backend="packed")
     with pytest.raises(E.InvalidArgument):                                               # negative init
         E.run_batch_packed([(x, -rng.random((200, 20)), rng.random((20, 200)))], _cfg("e-ahals-hp3", 5))
-    # auto picks the streams backend for BPP and stays exact there
-    out = E.run_batch([(x, rng.random((200, 20)), rng.random((20, 200)))], _cfg("e-anls-hp1", 3))
-    assert len(out[0].column("error")) == 4
+    # auto picks the streams backend for fp64_exact and stays bitwise there
+    p = (x, rng.random((200, 20)), rng.random((20, 200)))
+    cfg = _cfg("e-anls-hp1", 3, E.Precision.fp64_exact)
+    out = E.run_batch([p], cfg)
+    one = E.Context().run(*p, cfg, E.TimingMode.none)
+    assert np.array_equal(out[0].column("error"), one.column("error"))

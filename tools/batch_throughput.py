@@ -42,6 +42,14 @@ for rep in range(3):
     best = min(best, time.perf_counter() - t)
 print(f"packed: {B} runs x 200 iterations in {best:.3f} s = {B / best:.0f} runs/s "
       f"(final rel. error of run 0: {out[0].final_relative_error():.6e})")
+for alg in ("e-anls-hp1", "ahals"):
+    ca = E.algorithm_config(alg)
+    ca.max_outer_iterations = 200
+    E.run_batch_packed(probs[:16], ca)
+    t = time.perf_counter()
+    E.run_batch_packed(probs, ca)
+    dt = time.perf_counter() - t
+    print(f"packed {alg}: {B} runs in {dt:.3f} s = {B / dt:.0f} runs/s (through Python)")
 nb = min(B, 64)
 t = time.perf_counter()
 E.run_batch(probs[:nb], cfg, backend="streams", streams=16)
