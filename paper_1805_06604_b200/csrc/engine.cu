@@ -1420,14 +1420,19 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
 
   // validate + upload factors (engine.hpp:451-459)
   if (!dev_factors) {
-    for (size_t i = 0; i < wsz; ++i)
-      if (!std::isfinite(w0[i]) || !(w0[i] >= 0.0))
-        throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
-    for (size_t i = 0; i < hsz; ++i)
-      if (!std::isfinite(h0[i]) || !(h0[i] >= 0.0))
-        throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
+    // upload first, then the same finite / nonnegative check on the device (one pass over the
+    // 2·r·(m+n) values instead of a host loop)
     CU(cudaMemcpyAsync(c->scratch.p, w0, wsz * 8, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(c->H.p, h0, hsz * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), s));
+    misc::check_factor<<<grid_for(wsz), 256, 0, s>>>(c->scratch.p, wsz, c->flags.p, 1);
+    misc::check_factor<<<grid_for(hsz), 256, 0, s>>>(c->H.p, hsz, c->flags.p, 1);
+    CUK();
+    c->launches += 2;
+    int bad = 0;
+    CU(cudaMemcpyAsync(&bad, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (bad) throw Fail{ENMF_INVALID_ARGUMENT, "run: initial factors must be finite and nonnegative"};
   } else {
     CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), s));
     misc::check_factor<<<grid_for(wsz), 256, 0, s>>>(w0, wsz, c->flags.p, 1);

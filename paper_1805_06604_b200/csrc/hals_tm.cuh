@@ -158,9 +158,12 @@ ENMF_DEV void tm_store_s(double* Ss, int gi, int gt, const double (&c)[8][2]) {
 // S_{b+1} over every block but b (whose columns come in as the "tail" once the row warp has solved
 // block b; S_{b+1}'s accumulators stay in registers across the hand-off).  Gram fragments stream
 // from shared memory (gfs, ws_prep order) next to the TMEM fragment loads, one k-step pair ahead.
+// abort (speculative decision, nullable): nonzero once the previous sweep was decided to be the
+// last — this sweep's rows are discarded, so the round stops at the next block pair; the
+// decision is handed to the row warp in *ab_out with the S_b hand-off.  Returns 1 if aborted.
 template <int KS, int NB, int NT>
-ENMF_DEV void tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS, int idH,
-                                SwProf& pf) {
+ENMF_DEV int tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS, int idH,
+                               const volatile int* abort, volatile int* ab_out, SwProf& pf) {
   constexpr uint32_t GC = 8 * KS;   // TMEM columns per group (2 words × RMAX rows)
   const uint32_t la[4] = {tq, tq + (16u << 16), tq + GC, tq + GC + (16u << 16)};
   uint32_t f[2][4][8];
@@ -174,6 +177,14 @@ ENMF_DEV void tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int
       bar_sync_n<64>(idH);                       // rows of block b-1 are final in TMEM
       tc::fence_after();
       pf.mark(2);
+    }
+    if (abort) {
+      const int ab = *abort;
+      if ((threadIdx.x & 31) == 0) *ab_out = ab;
+      if (ab) {
+        bar_arrive_n<64>(idS);                   // the row warp reads the abort and stops too
+        return 1;
+      }
     }
     double c0[8][2], c1[8][2];
 #pragma unroll
@@ -217,20 +228,21 @@ ENMF_DEV void tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int
     bar_arrive_n<64>(idS);                       // S_{b+1} ready
     pf.mark(3);
   }
+  return 0;
 }
 
 template <int KS, int NB>
-ENMF_DEV void tm_producer_round_nt(int nt, uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS,
-                                   int idH, SwProf& pf) {
+ENMF_DEV int tm_producer_round_nt(int nt, uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS,
+                                  int idH, const volatile int* abort, volatile int* ab_out, SwProf& pf) {
   switch (nt) {
-    case 8: tm_producer_round<KS, NB, 8>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 7: tm_producer_round<KS, NB, 7>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 6: tm_producer_round<KS, NB, 6>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 5: tm_producer_round<KS, NB, 5>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 4: tm_producer_round<KS, NB, 4>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 3: tm_producer_round<KS, NB, 3>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    case 2: tm_producer_round<KS, NB, 2>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
-    default: tm_producer_round<KS, NB, 1>(tq, Ss, gfs, gi, gt, idS, idH, pf); break;
+    case 8: return tm_producer_round<KS, NB, 8>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 7: return tm_producer_round<KS, NB, 7>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 6: return tm_producer_round<KS, NB, 6>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 5: return tm_producer_round<KS, NB, 5>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 4: return tm_producer_round<KS, NB, 4>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 3: return tm_producer_round<KS, NB, 3>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    case 2: return tm_producer_round<KS, NB, 2>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
+    default: return tm_producer_round<KS, NB, 1>(tq, Ss, gfs, gi, gt, idS, idH, abort, ab_out, pf);
   }
 }
 
@@ -348,15 +360,22 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   __shared__ double s_wg[2][4];
   __shared__ int s_wnf[2][4];
   __shared__ int s_dec[2];
+  __shared__ int s_abort;                   // the previous sweep was the last (speculative path)
+  __shared__ int s_ab[4];                   // per pair: the product warp's abort decision at a pair start
+  if (threadIdx.x == 0) s_abort = 0;
   int result_sweep = -1;
 
   for (int sw = 0;; ++sw) {
     double* const hout = (spec && (sw & 1)) ? a.H2 : a.H;
     if (spec && sw > 0 && warp == 4) {
       const int d = tm_decide(a, sw - 1, first_total);
-      if (lane == 0) s_dec[(sw - 1) & 1] = d;
+      if (lane == 0) {
+        s_dec[(sw - 1) & 1] = d;
+        if (d) *(volatile int*)&s_abort = 1;  // stop on sw-1: the rest of sweep sw is discarded
+      }
     }
-    for (int i = 0; i < rounds; ++i) {
+    int aborted = 0;
+    for (int i = 0; i < rounds && !aborted; ++i) {
       const long ta = tq0 + (long)i * cnt / rounds;
       const int nt = (int)(tq0 + (long)(i + 1) * cnt / rounds - ta);
       const int ntA = nt < 4 ? nt : 4, ntB = nt - ntA;   // tiles 0-3: group A, 4-7: group B
@@ -374,7 +393,8 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         pf.mark(5);
       }
       if (producer) {
-        tm_producer_round_nt<KS, NB>(nt, tq, Ss, gfs, gi, gt, idS, idH, pf);
+        aborted = tm_producer_round_nt<KS, NB>(nt, tq, Ss, gfs, gi, gt, idS, idH, spec ? &s_abort : nullptr,
+                                               &s_ab[pair], pf);
       } else {
         // two columns per lane: cA in group A, cB in group B (predicated, no branches)
         const long ld = a.ld, ld8 = 8 * ld;
@@ -425,6 +445,10 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
           pf.mark(0);
           bar_sync_n<64>(idS);
           pf.mark(1);
+          if (spec && !(b & 1) && *(volatile int*)&s_ab[pair]) {   // sweep discarded (see tm_producer_round)
+            aborted = 1;
+            break;
+          }
           double x[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
