@@ -220,14 +220,23 @@ class RunRecord:
         return np.array([getattr(r, name) for r in self.iterations])
 
 
+_ITER_DTYPE = np.dtype([("iteration", "<u8"), ("elapsed_seconds", "<f8"), ("error", "<f8"),
+                        ("relative_error", "<f8"), ("beta", "<f8"), ("restarted", "<i4"),
+                        ("inner_h_count", "<i4"), ("inner_w_count", "<i4"), ("reinit_events", "<i4")])
+
+
+def _records_np(rows: np.ndarray) -> List[IterationRecord]:
+    """IterationRecords from a structured array of enmf_gpu_iter (one tolist() instead of a
+    ctypes field access per value)."""
+    return [IterationRecord(it, el, e, re, b, rs != 0, ih, iw, ev)
+            for it, el, e, re, b, rs, ih, iw, ev in rows.tolist()]
+
+
 def _records(arr, count) -> List[IterationRecord]:
-    out = []
-    for i in range(count):
-        it = arr[i]
-        out.append(IterationRecord(int(it.iteration), it.elapsed_seconds, it.error, it.relative_error,
-                                   it.beta, bool(it.restarted), it.inner_h_count, it.inner_w_count,
-                                   it.reinit_events))
-    return out
+    """IterationRecords from the first `count` entries of a ctypes array of enmf_gpu_iter."""
+    if count == 0:
+        return []
+    return _records_np(np.frombuffer(arr, dtype=_ITER_DTYPE, count=count))
 
 
 def _f64(a, name):
@@ -538,7 +547,7 @@ def run_batch_packed(problems, cfg: SolverConfig, device: int = -1, raise_errors
     _check(L.load().enmf_gpu_run_batch_dense(ctx._h, B, _p(xs), m, n, _p(ws), _p(hs), r, C.byref(c), iters, cap,
                                              nit.ctypes.data_as(ip), st.ctypes.data_as(ip), _p(wo), _p(ho),
                                              _p(nx)))
-    arr = C.cast(iters, C.POINTER(L.CIter))
+    allrec = np.frombuffer(iters, dtype=_ITER_DTYPE, count=cap * B).reshape(B, cap)
     out = []
     for b in range(B):
         if st[b] != L.ENMF_OK:
@@ -547,7 +556,7 @@ def run_batch_packed(problems, cfg: SolverConfig, device: int = -1, raise_errors
                 raise err
             out.append(err)
             continue
-        recs = _records(arr[b * cap:(b + 1) * cap], min(int(nit[b]), cap))
+        recs = _records_np(allrec[b, :min(int(nit[b]), cap)])
         out.append(RunRecord(recs, FactorPair(wo[b], ho[b]), float(nx[b])))
     return out
 
