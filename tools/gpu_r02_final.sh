@@ -9,7 +9,9 @@ timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 fi
 timeout 900 python bench.py --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-for w in c2 c3 c4; do timeout 600 python bench.py --workload $w --warmup 5 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
+timeout 600 python bench.py --workload c2 --steps 500 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 600 python bench.py --workload c3 --steps 100 --warmup 5 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 600 python bench.py --workload c4 --steps 300 --warmup 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 if [ "${REF:-1}" = "1" ]; then
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 fi
