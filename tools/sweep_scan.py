@@ -1,5 +1,6 @@
-"""Per-sweep cost of the persistent sweep kernel vs the number of sweeps in one solve (device-timed:
-ctx.hals_solve_device keeps G, C, H on the device).  C5 shape, forced sweep counts."""
+"""Per-sweep cost of the persistent sweep kernel vs the number of sweeps in one solve: run under ncu
+(tools/gpu_sweep_scan.sh), whose launch durations are the device times.  C5 shape, forced sweep
+counts (stall fraction 1e-300)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
