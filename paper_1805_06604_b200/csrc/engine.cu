@@ -517,7 +517,6 @@ void launch_sweep_tm(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   CU(cudaLaunchKernelEx(&lc, hals::sweep_tm<R_>, a, ntiles));
 }
 
-bool hals_use_fma() { return hals_variant() == 1; }
 
 // The persistent sweep kernel runs a whole inner solve in one launch.
 bool hals_persistent(int prec, int r) {
