@@ -111,3 +111,22 @@ def test_eligibility_and_errors(golden):
     out = E.run_batch([p], cfg)
     one = E.Context().run(*p, cfg, E.TimingMode.none)
     assert np.array_equal(out[0].column("error"), one.column("error"))
+
+
+def test_failing_run_is_reported_per_run(golden, port):
+    """A run whose H update overflows (a column of X at 1e307: W_yᵀX is +inf) fails with
+    NonFiniteIterate (engine.hpp:334-337, "H update produced a non-finite value", as the reference
+    does for this input) in its own slot; the other runs of the launch finish."""
+    x = golden.load("c1_inputs")["x"]
+    bad = x.copy()
+    bad[:, 0] = 1e307
+    w0, h0 = port.random_init(200, 200, 20, 3)
+    cfg = _cfg("e-ahals-hp3", 10)
+    out = E.run_batch_packed([(x, w0, h0), (bad, w0, h0), (x, w0, h0)], cfg, raise_errors=False)
+    assert isinstance(out[1], E.NonFiniteIterate)
+    assert not isinstance(out[0], Exception) and not isinstance(out[2], Exception)
+    assert np.array_equal(out[0].column("error"), out[2].column("error"))
+    with pytest.raises(E.NonFiniteIterate):
+        E.run_batch_packed([(bad, w0, h0)], cfg)
+    with pytest.raises(E.NonFiniteIterate):                       # the single-run engine agrees
+        E.Context().run(bad, w0, h0, cfg, E.TimingMode.none)
