@@ -314,7 +314,9 @@ def test_c5_full_size_properties(ctx):
 # ---------------------------------------------------- multi-GPU engine, world 1
 @pytest.mark.parametrize("alg,shape", [("e-ahals-hp3", (1030, 400, 40)), ("e-ahals-hp1", (300, 257, 17)),
                                        ("e-anls-hp1", (400, 300, 12)),
-                                       ("e-ahals-hp3", (4096, 4100, 64))])   # INT8-digit products
+                                       ("e-ahals-hp3", (4096, 4100, 64)),    # INT8-digit products
+                                       ("e-ahals-hp3", (700, 900, 100)),     # sweep_tm, synchronous
+                                       ("e-ahals-hp3", (2048, 2048, 128))])  # decision (gain exchange)
 def test_sharded_engine_world1_matches_single(ctx, port, alg, shape):
     """The sharded engine (peer-memory all-gathers, mailbox all-reduces, per-sweep
     gain exchange, csrc/dist.cuh) driven with one rank must reproduce the
