@@ -206,6 +206,10 @@ void set_attrs_once() {
   big((const void*)gemm::gemm_f64_dmma_s<true, 2, true>, gemm::st::SMEM_BYTES);
   big((const void*)gemm::gemm_f64_dmma_s<true, 1, false>, gemm::st::SMEM_BYTES);
   big((const void*)gemm::gemm_f64_dmma_s<true, 1, true>, gemm::st::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_t<false, false>, gemm::tm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_t<false, true>, gemm::tm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_t<true, false>, gemm::tm::SMEM_BYTES);
+  big((const void*)gemm::gemm_f64_dmma_t<true, true>, gemm::tm::SMEM_BYTES);
   big((const void*)hals::sweep_ws<32>, hals::ws_smem_bytes<32>());
   big((const void*)hals::sweep_ws<64>, hals::ws_smem_bytes<64>());
   big((const void*)hals::sweep_ws<128>, hals::ws_smem_bytes<128>());
@@ -267,6 +271,48 @@ bool gemm_big_tile() {  // ENMF_GEMM_TILE=128: the 128×128 single-CTA-per-SM ke
   if (v < 0) {
     const char* e = std::getenv("ENMF_GEMM_TILE");
     v = (e && std::string(e) == "128") ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// ---- TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 2-D FP64 operand (outer rows of `inner` contiguous doubles, row stride ld) in boxes of
+// box_inner × box_outer, SWIZZLE_128B (box_inner = 16 doubles = one 128-byte row), zeros past the edges
+CUtensorMap f64_tmap(const double* base, long inner, long outer, long ld, int box_inner, int box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dim[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t stride[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dim, stride, box,
+                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Fail{ENMF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+// ENMF_GEMM_LOAD=cpasync: the FP64 DMMA GEMM loads its tiles with cp.async (gemm_f64_dmma_s)
+// instead of TMA (gemm_f64_dmma_t) — A/B timing.
+bool gemm_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ENMF_GEMM_LOAD");
+    v = (e && std::string(e) == "cpasync") ? 0 : 1;
   }
   return v == 1;
 }
@@ -350,6 +396,22 @@ void gemm_launch_small(enmf_gpu_ctx* c, cudaStream_t s, bool bk, const double* A
   // M-tiles vary fastest (blockIdx.x): the r/64 CTAs sharing one X tile run
   // together, so X is fetched from HBM once and hit in L2 by the others.
   dim3 grid(tm, tn, S);
+  if (vec2 && gemm_tma()) {   // TMA-fed (16-byte aligned bases and row strides)
+    const CUtensorMap ta = f64_tmap(A, K, M, lda, 16, 64);
+    const CUtensorMap tb = bk ? f64_tmap(B, K, N, ldb, 16, 64) : f64_tmap(B, N, K, ldb, 16, 16);
+#define GEMM_GO_T(BKM, L) gemm_f64_dmma_t<BKM, L><<<grid, st::NTH, gemm::tm::SMEM_BYTES, s>>>(p, ta, tb)
+    if (bk) { if (last) GEMM_GO_T(true, true); else GEMM_GO_T(true, false); }
+    else { if (last) GEMM_GO_T(false, true); else GEMM_GO_T(false, false); }
+#undef GEMM_GO_T
+    CUK();
+    c->launches++;
+    if (S > 1 && !last) {
+      reduce_splits<<<grid_for((long)M * N), 256, 0, s>>>(part, S, M, N, C, ldc, sym ? 1 : 0, st);
+      CUK();
+      c->launches++;
+    }
+    return;
+  }
 #define GEMM_GO(BKM, V, L) gemm_f64_dmma_s<BKM, V, L><<<grid, st::NTH, st::SMEM_BYTES, s>>>(p)
   if (bk) {
     if (vec2) { if (last) GEMM_GO(true, 2, true); else GEMM_GO(true, 2, false); }

@@ -19,6 +19,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace gemm {
 
@@ -272,6 +273,64 @@ ENMF_DEV void st_load_nmajor(double* s, const double* g, long ld, int k0, int K,
   }
 }
 
+// Epilogue of the 64×64 DMMA kernels: the warp's 32×32 accumulators to C (or to this split's
+// partial slice), and with REDUCE_LAST the last split CTA of a tile sums the slices in order.
+template <bool REDUCE_LAST>
+ENMF_DEV void st_epilogue(const Params& p, const double (&acc)[4][4][2], int m0, int n0, int wm, int wn, int g, int t) {
+  constexpr int BM = st::BM, BN = st::BN, NTH = st::NTH;
+  const int tid = threadIdx.x;
+  const bool split = p.splits > 1;
+  double* out = split ? p.partials + (long)blockIdx.z * p.M * p.N : p.C;
+  const long ldo = split ? p.N : p.ldc;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = m0 + wm * 32 + mi * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int col = n0 + wn * 32 + ni * 8 + 2 * t;
+      if (!split && p.sym) {
+        for (int e = 0; e < 2; ++e) {
+          const int c = col + e;
+          if (c < p.N && row <= c) {
+            out[(long)row * ldo + c] = acc[mi][ni][e];
+            out[(long)c * ldo + row] = acc[mi][ni][e];
+          }
+        }
+      } else if (col + 1 < p.N && ((ldo & 1) == 0)) {
+        *reinterpret_cast<double2*>(out + (long)row * ldo + col) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (col < p.N) out[(long)row * ldo + col] = acc[mi][ni][0];
+        if (col + 1 < p.N) out[(long)row * ldo + col + 1] = acc[mi][ni][1];
+      }
+    }
+  }
+  if (!split || !REDUCE_LAST) return;
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* ctr = p.counters + blockIdx.y * gridDim.x + blockIdx.x;
+    const unsigned prev = atomicAdd(ctr, 1u);
+    s_last = (prev == (unsigned)p.splits - 1) ? 1u : 0u;
+    if (s_last) *ctr = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+  const long MN = (long)p.M * p.N;
+  for (int e = tid; e < rows * cols; e += NTH) {
+    const int i = m0 + e / cols, j = n0 + e % cols;
+    if (p.sym && i > j) continue;
+    const double* src = p.partials + (long)i * p.N + j;
+    double v = __ldcg(src);
+    for (int s = 1; s < p.splits; ++s) v = __dadd_rn(v, __ldcg(src + s * MN));
+    p.C[(long)i * p.ldc + j] = v;
+    if (p.sym) p.C[(long)j * p.ldc + i] = v;
+  }
+}
+
 template <bool B_KMAJOR, int VEC, bool REDUCE_LAST>
 __global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_s(Params p) {
   constexpr int BM = st::BM, BN = st::BN, BK = st::BK, STAGES = st::STAGES, NTH = st::NTH;
@@ -369,56 +428,7 @@ __global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_s(Params p) {
   }
   cp_wait<0>();
 
-  const bool split = p.splits > 1;
-  double* out = split ? p.partials + (long)blockIdx.z * p.M * p.N : p.C;
-  const long ldo = split ? p.N : p.ldc;
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int row = m0 + wm * 32 + mi * 8 + g;
-    if (row >= p.M) continue;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int col = n0 + wn * 32 + ni * 8 + 2 * t;
-      if (!split && p.sym) {
-        for (int e = 0; e < 2; ++e) {
-          const int c = col + e;
-          if (c < p.N && row <= c) {
-            out[(long)row * ldo + c] = acc[mi][ni][e];
-            out[(long)c * ldo + row] = acc[mi][ni][e];
-          }
-        }
-      } else if (col + 1 < p.N && ((ldo & 1) == 0)) {
-        *reinterpret_cast<double2*>(out + (long)row * ldo + col) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-      } else {
-        if (col < p.N) out[(long)row * ldo + col] = acc[mi][ni][0];
-        if (col + 1 < p.N) out[(long)row * ldo + col + 1] = acc[mi][ni][1];
-      }
-    }
-  }
-  if (!split || !REDUCE_LAST) return;
-  __shared__ unsigned s_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    unsigned* ctr = p.counters + blockIdx.y * gridDim.x + blockIdx.x;
-    const unsigned prev = atomicAdd(ctr, 1u);
-    s_last = (prev == (unsigned)p.splits - 1) ? 1u : 0u;
-    if (s_last) *ctr = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
-  const long MN = (long)p.M * p.N;
-  for (int e = tid; e < rows * cols; e += NTH) {
-    const int i = m0 + e / cols, j = n0 + e % cols;
-    if (p.sym && i > j) continue;
-    const double* src = p.partials + (long)i * p.N + j;
-    double v = __ldcg(src);
-    for (int s = 1; s < p.splits; ++s) v = __dadd_rn(v, __ldcg(src + s * MN));
-    p.C[(long)i * p.ldc + j] = v;
-    if (p.sym) p.C[(long)j * p.ldc + i] = v;
-  }
+  st_epilogue<REDUCE_LAST>(p, acc, m0, n0, wm, wn, g, t);
 }
 
 // Separate split-K reduction (fixed order), used when one output tile has
@@ -482,6 +492,112 @@ __global__ void cross_xht_exact(const double* __restrict__ X, const double* __re
   double s = 0.0;
   for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(xi[j], tk[j]));
   P[idx] = s;
+}
+
+// ---- the same kernel fed by TMA -----------------------------------------------------------
+// Operand tiles arrive by cp.async.bulk.tensor (one elected thread, mbarrier completion) in the
+// hardware's SWIZZLE_128B layout: a K-major tile is 64 rows × 16 doubles (one 128-byte row per
+// tile row, its 16-byte chunks XOR-permuted by row % 8), an N-major B tile four 16 × 16 boxes.
+// The 8-byte fragment loads follow the same permutation, so they stay conflict-free (K-major:
+// the 8 rows of a fragment touch 8 distinct chunk positions).  Out-of-range elements are filled
+// with zeros by the TMA unit — partial tiles need no separate load path.  Four stages, the
+// slots released by each warp's arrive on an "empty" mbarrier; split-K and the epilogue as in
+// gemm_f64_dmma_s.
+namespace tm {
+constexpr int A_BYTES = st::BM * st::BK * 8, B_BYTES = st::BN * st::BK * 8;
+constexpr int SMEM_BYTES = 1024 + st::STAGES * (A_BYTES + B_BYTES) + 2 * st::STAGES * 8;
+// element (row, k) of a K-major tile: row·16 + ((k/2) ^ (row % 8))·2 + k % 2
+ENMF_DEV int kidx(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
+}  // namespace tm
+
+template <bool B_KMAJOR, bool REDUCE_LAST>
+__global__ void __launch_bounds__(st::NTH, 3) gemm_f64_dmma_t(Params p, const __grid_constant__ CUtensorMap ta,
+                                                                const __grid_constant__ CUtensorMap tb) {
+  constexpr int BM = st::BM, BN = st::BN, BK = st::BK, STAGES = st::STAGES;
+  if (p.st && !dev_active(p.st)) return;
+  extern __shared__ uint8_t smem_raw_t[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_t) + 1023) & ~uintptr_t(1023));
+  double* As = reinterpret_cast<double*>(sm);
+  double* Bs = reinterpret_cast<double*>(sm + STAGES * tm::A_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * (tm::A_BYTES + tm::B_BYTES));
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int KB = (p.K + BK - 1) / BK;
+  const int per = (KB + p.splits - 1) / p.splits;
+  const int kb0 = blockIdx.z * per;
+  const int nk = max(0, min(KB, kb0 + per) - kb0);
+  if (tid == 0) {
+    tc::prefetch_tmap(&ta);
+    tc::prefetch_tmap(&tb);
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      tc::mbar_init(full + s2, 1);
+      tc::mbar_init(empty + s2, st::NTH / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kb, int s2) {
+    const int k0 = (kb0 + kb) * BK;
+    tc::mbar_expect_tx(full + s2, (uint32_t)(tm::A_BYTES + tm::B_BYTES));
+    tc::tma_load_2d(As + s2 * BM * BK, &ta, full + s2, k0, m0);
+    if (B_KMAJOR) {
+      tc::tma_load_2d(Bs + s2 * BN * BK, &tb, full + s2, k0, n0);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tc::tma_load_2d(Bs + s2 * BN * BK + q * 256, &tb, full + s2, n0 + 16 * q, k0);
+    }
+  };
+  if (tid == 0)
+    for (int s2 = 0; s2 < STAGES - 1 && s2 < nk; ++s2) issue(s2, s2);
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kb = 0; kb < nk; ++kb) {
+    const int s2 = kb % STAGES;
+    if (tid == 0 && kb + STAGES - 1 < nk) {     // refill the slot consumed at kb - 1
+      const int sn = (kb + STAGES - 1) % STAGES;
+      if (kb >= 1) tc::mbar_wait(empty + sn, (uint32_t)(((kb - 1) / STAGES) & 1));
+      issue(kb + STAGES - 1, sn);
+    }
+    tc::mbar_wait(full + s2, (uint32_t)((kb / STAGES) & 1));
+    const double* as = As + s2 * BM * BK;
+    const double* bs = Bs + s2 * BN * BK;
+    double a[2][4], b[2][4];
+    auto load_frag = [&](int kk, int buf) {
+      const int k = 4 * kk + t;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = as[tm::kidx(wm * 32 + mi * 8 + g, k)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        if (B_KMAJOR) {
+          b[buf][ni] = bs[tm::kidx(wn * 32 + ni * 8 + g, k)];
+        } else {               // box q = n / 16, row k, column c = n % 16 (16 doubles per row)
+          const int c = (ni & 1) * 8 + g;
+          b[buf][ni] = bs[(wn * 2 + (ni >> 1)) * 256 + k * 16 + ((((c >> 1) ^ (k & 7)) << 1) | (c & 1))];
+        }
+      }
+    };
+    load_frag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int cur = kk & 1;
+      if (kk + 1 < BK / 4) load_frag(kk + 1, cur ^ 1);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[cur][mi], b[cur][ni]);
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(empty + s2);  // this warp is done with the slot
+  }
+  st_epilogue<REDUCE_LAST>(p, acc, m0, n0, wm, wn, g, t);
 }
 
 }  // namespace gemm
