@@ -1160,7 +1160,8 @@ void ws_prepare(enmf_gpu_ctx* c, cudaStream_t s, hals::Args& a, int prec, int sl
   if (hals_variant() != 50 && hals_variant() != 54 && hals_variant() != 55) return;
   if (a.r <= 32) hals::ws_prep<32><<<8, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
   else if (a.r <= 64) hals::ws_prep<64><<<16, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
-  else hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+  else if (hals_variant() == 50 || hals_variant() == 55) hals::ws_prep<128><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);
+  else hals::ws_prep<128, true, true><<<64, 256, 0, s>>>(a.G, a.r, gf, a.st, a.ctl);   // sweep_tm: rows / G_kk
   CUK();
   c->launches++;
   a.Gf = gf;

@@ -250,7 +250,9 @@ ENMF_DEV double pos_part_ws(double t) {
 // on/below the diagonal inside diagonal blocks, and — for odd b — in the columns of block
 // b-1, whose fragments go to Gf[RMAX² + ...] instead (the "tail" of the paired product).
 // SPLIT = false (sweep_t2): no tail split, every block's fragments in the main array.
-template <int RMAX, bool SPLIT = true>
+// SCALE (sweep_tm): row k divided by G_kk, so the block products come out as S/G_kk and the row
+// pass forms t = C/G_kk - S/G_kk with one fma.
+template <int RMAX, bool SPLIT = true, bool SCALE = false>
 __global__ void ws_prep(const double* G, int r, double* Gf, const DevState* st, const HalsCtl* ctl) {
   if ((st && !dev_active(st)) || !ctl->cont) return;
   constexpr int KS = RMAX / 4;
@@ -259,7 +261,10 @@ __global__ void ws_prep(const double* G, int r, double* Gf, const DevState* st, 
     const int s = 2 * s2 + e, gi = lane >> 2, gt = lane & 3;
     const int row = 8 * b + gi, col = 4 * s + gt;
     double v = 0.0;
-    if (row < r && col < r && !((s >> 1) == b && col - 8 * b <= gi)) v = G[(long)row * r + col];
+    if (row < r && col < r && !((s >> 1) == b && col - 8 * b <= gi)) {
+      v = G[(long)row * r + col];
+      if (SCALE) v = __dmul_rn(v, __ddiv_rn(1.0, G[(long)row * r + row]));
+    }
     const bool tail = SPLIT && (b & 1) && s2 == b - 1;
     Gf[i] = tail ? 0.0 : v;
     if (tail) Gf[RMAX * RMAX + (b >> 1) * 64 + lane * 2 + e] = v;

@@ -27,7 +27,7 @@
 //     and the row-pass constants: 48 KB instead of 141 KB.
 //
 // Everything else — Gram fragments pre-arranged by ws_prep, the "tail" of the joint
-// two-block product, the multiply-free row chain t = (C − S)/G_kk, the halved gain form,
+// two-block product, the multiply-free row chain on t = (C − S)/G_kk, the halved gain form,
 // the fixed-order grid-wide stall decision (grid_decision) — is sweep_ws's.
 #pragma once
 
@@ -158,12 +158,19 @@ ENMF_DEV void tm_store_s(double* Ss, int gi, int gt, const double (&c)[8][2]) {
 // S_{b+1} over every block but b (whose columns come in as the "tail" once the row warp has solved
 // block b; S_{b+1}'s accumulators stay in registers across the hand-off).  Gram fragments stream
 // from shared memory (gfs, ws_prep order) next to the TMEM fragment loads, one k-step pair ahead.
+// One block of look-ahead: the pass over H starts as soon as S_{b-1} is handed over and takes the
+// row blocks in the order b, b+1, ..., b-2 (mod NB) WHILE the row warp solves block b-1 — slowly,
+// its scalar FP64 gets one issue slot per ~2 DMMAs next to this stream (profiles/r02_share_probe.txt:
+// ~4.7 K cycles per block instead of ~1 K), but hidden under ~8 K cycles of products — and ends with
+// block b-1's k-steps once its rows are in.  Block b is then solved with the FP64 pipe to itself
+// (nothing to overlap it with: both of the pair's products need its rows).
 // abort (speculative decision, nullable): nonzero once the previous sweep was decided to be the
 // last — this sweep's rows are discarded, so the round stops at the next block pair; the
 // decision is handed to the row warp in *ab_out with the S_b hand-off.  Returns 1 if aborted.
 template <int KS, int NB, int NT>
 ENMF_DEV int tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int gi, int gt, int idS, int idH,
                                const volatile int* abort, volatile int* ab_out, SwProf& pf) {
+  static_assert(NB == KS / 2 && (NB & (NB - 1)) == 0, "row blocks = k-step pairs, a power of two");
   constexpr uint32_t GC = 8 * KS;   // TMEM columns per group (2 words × RMAX rows)
   const uint32_t la[4] = {tq, tq + (16u << 16), tq + GC, tq + GC + (16u << 16)};
   uint32_t f[2][4][8];
@@ -173,15 +180,11 @@ ENMF_DEV int tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int 
     for (int i = 0; i < 8; ++i) f[0][q][i] = f[1][q][i] = 0u;
 #pragma unroll 1
   for (int b = 0; b < NB; b += 2) {
-    if (b > 0) {
-      bar_sync_n<64>(idH);                       // rows of block b-1 are final in TMEM
-      tc::fence_after();
-      pf.mark(2);
-    }
     if (abort) {
       const int ab = *abort;
       if ((threadIdx.x & 31) == 0) *ab_out = ab;
       if (ab) {
+        if (b > 0) bar_sync_n<64>(idH);          // the row warp has taken S_{b-1} (one arrival per hand-off)
         bar_arrive_n<64>(idS);                   // the row warp reads the abort and stops too
         return 1;
       }
@@ -189,22 +192,34 @@ ENMF_DEV int tm_producer_round(uint32_t tq, double* Ss, const double2* gfs, int 
     double c0[8][2], c1[8][2];
 #pragma unroll
     for (int t = 0; t < 8; ++t) c0[t][0] = c0[t][1] = c1[t][0] = c1[t][1] = 0.0;
-    const double2* g0 = gfs + (b * KS / 2) * 32;         // block b's fragments, k-step pair j at j·32
-    const double2* g1 = gfs + ((b + 1) * KS / 2) * 32;   // block b+1's (without block b's columns)
-    tm_issue<NT>(la, 0, f[0]);
-    double2 a0 = g0[0], a1 = g1[0];
+    const double2* g0 = gfs + (b * NB) * 32;         // block b's fragments, k-step pair j at j·32
+    const double2* g1 = gfs + ((b + 1) * NB) * 32;   // block b+1's (without block b's columns)
+    // look-ahead: row blocks b, b+1, ..., b-2 (mod NB) while the row warp still solves block b-1,
+    // whose k-steps come last
+    tm_issue<NT>(la, b, f[0]);
+    double2 a0 = g0[b * 32], a1 = g1[b * 32];
     tm_wait_ld32(f[0]);
 #pragma unroll
-    for (int j = 0; j < KS / 2; ++j) {
-      const int cur = j & 1;
+    for (int jj = 0; jj < NB; ++jj) {
+      const int cur = jj & 1;
+      const int jn = (b + jj + 1) & (NB - 1);
       double2 n0, n1;
-      if (j + 1 < KS / 2) {                      // next k-step pair in flight while these DMMAs issue
-        tm_issue<NT>(la, j + 1, f[cur ^ 1]);
-        n0 = g0[(j + 1) * 32];
-        n1 = g1[(j + 1) * 32];
+      if (jj + 1 < NB) {
+        n0 = g0[jn * 32];
+        n1 = g1[jn * 32];
       }
+      if (jj + 2 < NB) tm_issue<NT>(la, jn, f[cur ^ 1]);   // next k-step pair in flight while these DMMAs issue
       tm_mma_j<NT>(c0, c1, a0, a1, f[cur]);
-      if (j + 1 < KS / 2) {
+      if (jj + 2 == NB) {                        // block b-1: its rows must be final in TMEM
+        if (b > 0) {
+          pf.mark(0);
+          bar_sync_n<64>(idH);
+          tc::fence_after();
+          pf.mark(2);
+        }
+        tm_issue<NT>(la, jn, f[cur ^ 1]);
+      }
+      if (jj + 1 < NB) {
         tm_wait_ld32(f[cur ^ 1]);
         a0 = n0;
         a1 = n1;
@@ -416,6 +431,15 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         tm_ld_rows(tq, xa);
         tm_ld_rows(tq + GC, xb);
         int hmax = 0;
+        // S slots of lanes past the round's tiles are never written by the product warp: zero them
+        // once, so those lanes run t = 0 - 0 (h stays 0, no gain) without a select per row
+        if (!(lane < ntA * 8))
+#pragma unroll
+          for (int i = 0; i < 8; ++i) Ss[i * TM_SLD + lane] = 0.0;
+        if (!(lane < ntB * 8))
+#pragma unroll
+          for (int i = 0; i < 8; ++i) Ss[8 * TM_SLD + i * TM_SLD + lane] = 0.0;
+        __syncwarp();
 #pragma unroll 1
         for (int b = 0; b < NB; ++b) {
           double bb[16];
@@ -452,12 +476,11 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
           double x[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            // columns past the round's tiles: the product warp leaves their S unwritten (stale or
-            // uninitialised shared memory), so they are forced to t = 0 (h stays 0, no gain)
-            const double sa = __dmul_rn(__dsub_rn(bb[i], SA[i * TM_SLD + lane]), gc[36 + i]);
-            const double sb = __dmul_rn(__dsub_rn(bb[8 + i], SB[i * TM_SLD + lane]), gc[36 + i]);
-            bb[i] = vA ? sa : 0.0;
-            bb[8 + i] = vB ? sb : 0.0;
+            // t = C/G_kk - S/G_kk (the Gram fragments are pre-divided by G_kk, ws_prep SCALE)
+            const double sa = fma(bb[i], gc[36 + i], -SA[i * TM_SLD + lane]);
+            const double sb = fma(bb[8 + i], gc[36 + i], -SB[i * TM_SLD + lane]);
+            bb[i] = sa;
+            bb[8 + i] = sb;
             x[i] = tm_d(xa[2 * i], xa[2 * i + 1]);
             x[8 + i] = tm_d(xb[2 * i], xb[2 * i + 1]);
           }
@@ -470,10 +493,11 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
               bb[l] = fma(-gc[l * (l - 1) / 2 + i], h0, bb[l]);
               bb[8 + l] = fma(-gc[l * (l - 1) / 2 + i], h1, bb[8 + l]);
             }
-            const double u0 = __dsub_rn(x[i], h0), v0 = __dadd_rn(x[i], h0);
-            const double u1 = __dsub_rn(x[8 + i], h1), v1 = __dadd_rn(x[8 + i], h1);
-            gain = fma(__dmul_rn(u0, gc[28 + i]), fma(-2.0, bb[i], v0), gain);
-            gain = fma(__dmul_rn(u1, gc[28 + i]), fma(-2.0, bb[8 + i], v1), gain);
+            // G_kk((x-t)² - (h-t)²) = (x-h)·(G_kk/2)·(x+h-2t)·2, accumulated halved (an integer-pipe
+            // max(-t, 0) in place of x+h costs more issue slots than the DADD it saves: measured)
+            const double u0 = __dsub_rn(x[i], h0), u1 = __dsub_rn(x[8 + i], h1);
+            gain = fma(__dmul_rn(u0, gc[28 + i]), fma(-2.0, bb[i], __dadd_rn(x[i], h0)), gain);
+            gain = fma(__dmul_rn(u1, gc[28 + i]), fma(-2.0, bb[8 + i], __dadd_rn(x[8 + i], h1)), gain);
             x[i] = h0;
             x[8 + i] = h1;
           }
