@@ -363,26 +363,34 @@ def run_ours(args, rank, world, local_rank):
         xn = [x.numpy() for x in xh]
         wn, hn = wh.numpy(), hh.numpy()
         wout, hout = torch.empty_like(wh).pin_memory(), torch.empty_like(hh).pin_memory()
-        torch.cuda.synchronize()
+        # three whole calls on one context (the first also allocates the device buffers); the
+        # median is reported, every call listed: a single call is at the mercy of one slow
+        # cudaMalloc or page-in on a fresh box
+        walls = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if world == 1:
+                rec2 = ctx2.run(xn[0], wn, hn, cfg2, E.TimingMode.none)
+                fre = rec2.final_relative_error()
+            else:
+                ctx2.load_sharded(xn[0], xn[1])
+                ctx2.begin(wn, hn, cfg2)
+                ctx2.step(args.steps)
+                rr = ctx2.sync()
+                ctx2.end(wout.data_ptr(), hout.data_ptr())
+                fre = rr[-1].relative_error
+            t1 = time.perf_counter()
+            w1 = t1 - t0
+            if world > 1:
+                t = torch.tensor([w1], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                w1 = float(t.item())
+            walls.append(w1)
+        wall = statistics.median(walls)
         if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        if world == 1:
-            rec2 = ctx2.run(xn[0], wn, hn, cfg2, E.TimingMode.none)
-            fre = rec2.final_relative_error()
-        else:
-            ctx2.load_sharded(xn[0], xn[1])
-            ctx2.begin(wn, hn, cfg2)
-            ctx2.step(args.steps)
-            rr = ctx2.sync()
-            ctx2.end(wout.data_ptr(), hout.data_ptr())
-            fre = rr[-1].relative_error
-        t1 = time.perf_counter()
-        wall = t1 - t0
-        if world > 1:
-            t = torch.tensor([wall], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
             ctx2.finalize()
         ctx2.close()
         xb = sum(x.numel() for x in xh) * 8
@@ -390,10 +398,10 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(xb + (wh.numel() + hh.numel()) * 8),
                "d2h_bytes_per_step": int((wh.numel() + hh.numel()) * 8 + (args.steps + 1) * 56),
                "step": (f"one enmf_gpu_run_dense call: X/W0/H0 host->device, {args.steps} outer iterations, "
-                        f"W/H/records device->host" if world == 1 else
+                        f"W/H/records device->host (median of 3 calls)" if world == 1 else
                         f"per rank: X column+row blocks and factor shards host->device, {args.steps} outer "
                         f"iterations, factor shards/records device->host"),
-               "seconds": wall, "final_relative_error": fre}
+               "seconds": wall, "calls_s": walls, "final_relative_error": fre}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -88,6 +88,13 @@ struct enmf_gpu_ctx {
   DBuf<double> x_own;
   const double* x = nullptr;
   size_t m = 0, n = 0;
+  // host X in flight (x_upload_async .. x_join .. x_verdict): the copy runs on its own stream so
+  // that begin()'s allocations and factor upload overlap it; 0 = none, 1 = copy enqueued, not yet
+  // joined by the engine stream, 2 = joined, finite check enqueued, verdict not read
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t x_copied = nullptr, x_checked = nullptr;
+  int* x_bad = nullptr;                    // pinned host flag
+  int x_state = 0;
   // CSR data matrix (enmf_gpu_load_csr): CSR for X·Tᵀ, CSC copy for W_yᵀX
   bool sparse = false;
   size_t nnz = 0;
@@ -1416,6 +1423,59 @@ struct Session {
 
 namespace {
 
+// Host X → device on the copy stream (DenseMatrix data, matrix.hpp:65-66); returns at once for
+// pinned memory.  The engine stream joins it in x_join, right before X is first read.
+void x_upload_async(enmf_gpu_ctx* c, const double* x, size_t m, size_t n) {
+  if (!c->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->x_copied, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->x_checked, cudaEventDisableTiming));
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&c->x_bad), sizeof(int), cudaHostAllocDefault));
+  }
+  if (c->x_state == 2) CU(cudaEventSynchronize(c->x_checked));   // an unread verdict of the previous X: dropped
+  c->x_own.ensure(m * n);
+  // the previous X may still be read by work queued on the engine stream
+  CU(cudaEventRecord(c->x_checked, c->stream));
+  CU(cudaStreamWaitEvent(c->copy_stream, c->x_checked, 0));
+  CU(cudaMemcpyAsync(c->x_own.p, x, m * n * 8, cudaMemcpyHostToDevice, c->copy_stream));
+  CU(cudaEventRecord(c->x_copied, c->copy_stream));
+  c->x = c->x_own.p;
+  c->x_state = 1;
+}
+
+// The engine stream waits for the copy and checks the values (DenseMatrix rejects NaN/Inf,
+// matrix.hpp:43-51) on the device; the verdict lands in pinned memory.
+void x_join(enmf_gpu_ctx* c) {
+  if (c->x_state != 1) return;
+  if (!c->x || c->sparse) {               // another data matrix was loaded since
+    c->x_state = 0;
+    return;
+  }
+  cudaStream_t s = c->stream;
+  CU(cudaStreamWaitEvent(s, c->x_copied, 0));
+  c->flags.ensure(4);
+  CU(cudaMemsetAsync(c->flags.p + 1, 0, sizeof(int), s));
+  misc::check_factor<<<grid_for((long)(c->m * c->n)), 256, 0, s>>>(c->x, (long)(c->m * c->n), c->flags.p + 1, 0);
+  CUK();
+  c->launches++;
+  CU(cudaMemcpyAsync(c->x_bad, c->flags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(c->x_checked, s));
+  c->x_state = 2;
+}
+
+// Reads the verdict once it is in (wait: block for it); a non-finite X fails the call like the
+// reference's DenseMatrix constructor.
+void x_verdict(enmf_gpu_ctx* c, bool wait) {
+  if (c->x_state != 2) return;
+  if (wait) CU(cudaEventSynchronize(c->x_checked));
+  else if (cudaEventQuery(c->x_checked) != cudaSuccess) { (void)cudaGetLastError(); return; }
+  c->x_state = 0;
+  if (*c->x_bad) {
+    c->x = nullptr;
+    throw Fail{ENMF_INVALID_ARGUMENT, "DenseMatrix: values must be finite"};
+  }
+}
+
 void close_session(enmf_gpu_ctx* c) {
   if (!c->sess) return;
   if (c->sess->exec) cudaGraphExecDestroy(c->sess->exec);
@@ -1520,6 +1580,7 @@ void begin_impl(enmf_gpu_ctx* c, const double* w0, const double* h0, size_t r, b
   CU(cudaMemsetAsync(c->bpp_rounds.p, 0, 2 * sizeof(int), s));
   CU(cudaMemsetAsync(c->bpp_nf.p, 0, 2 * sizeof(int), s));
   tr.mark("factors");
+  x_join(c);                             // a host X still in flight (enmf_gpu_run_dense): first read below
 
   // run state (engine.hpp:471-481)
   DevState hs;
@@ -1699,6 +1760,7 @@ size_t sync_impl(enmf_gpu_ctx* c, enmf_gpu_iter* iters, size_t cap, size_t* n_it
   DevState out;
   CU(cudaMemcpyAsync(&out, c->st.p, sizeof out, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  x_verdict(c, true);
   const size_t done = (size_t)out.k;
   std::vector<enmf_gpu_iter> recs(done + 1);
   CU(cudaMemcpy(recs.data(), c->recs.p, (done + 1) * sizeof(enmf_gpu_iter), cudaMemcpyDeviceToHost));

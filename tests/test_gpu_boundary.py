@@ -59,3 +59,24 @@ def test_non_finite_iterate_through_step_api(ctx, prec):
         ctx.run(x, w0, h0, c, E.TimingMode.none)
     rec = ctx.run(x * 1e-300, w0, h0, c, E.TimingMode.none)
     assert len(rec.iterations) == 6 and np.all(np.isfinite(rec.factors.w))
+
+
+def test_non_finite_data_matrix_rejected(ctx):
+    """DenseMatrix rejects NaN/Inf (matrix.hpp:43-51): enmf_gpu_load_dense fails at once;
+    enmf_gpu_run_dense — whose upload of X overlaps begin() — fails the call with the same error
+    at its first synchronization, and the context keeps working."""
+    rng = np.random.default_rng(3)
+    x, w0, h0 = rng.random((70, 50)), rng.random((70, 5)), rng.random((5, 50))
+    c = E.algorithm_config("e-ahals-hp3")
+    c.max_outer_iterations = 4
+    good = ctx.run(x, w0, h0, c, E.TimingMode.none)
+    for bad_value in (np.nan, np.inf):
+        xb = x.copy()
+        xb[13, 7] = bad_value
+        with pytest.raises(E.InvalidArgument, match="DenseMatrix: values must be finite"):
+            ctx.load(xb)
+        with pytest.raises(E.InvalidArgument, match="DenseMatrix: values must be finite"):
+            ctx.run(xb, w0, h0, c, E.TimingMode.none)
+    again = ctx.run(x, w0, h0, c, E.TimingMode.none)
+    assert np.array_equal(again.column("error"), good.column("error"))
+    assert np.array_equal(again.factors.w, good.factors.w)
