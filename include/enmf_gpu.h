@@ -210,6 +210,14 @@ int enmf_gpu_dist_init(enmf_gpu_ctx* ctx, const void* ipc_handles);
 int enmf_gpu_load_dense_sharded(enmf_gpu_ctx* ctx, const double* x_cols, const double* x_rows,
                                 int on_device);
 int enmf_gpu_dist_finalize(enmf_gpu_ctx* ctx);
+/* Self-test of the cross-rank exchange primitives (epoch flags, double-buffered mailbox slots,
+ * rank-ordered sums, shard all-gather + barrier) with `world` ranks on THIS GPU: one cooperative
+ * launch, block p = rank p, `epochs` rounds of every exchange the sharded engine uses.  in:
+ * [world][count] contributions; red: [world][epochs][count] all-reduced values; sc:
+ * [world][epochs][3] = (gain sum, flag OR, max); rep_w / rep_t: [world][r*full] each rank's
+ * replicas after the last round.  (No reference analogue: the reference is single-process.) */
+int enmf_gpu_dist_selftest(enmf_gpu_ctx* ctx, int world, int count, int epochs, int r, size_t full,
+                           const double* in, double* red, double* sc, double* rep_w, double* rep_t);
 
 /* ---- public kernels the reference's tests call (host pointers) --------------
  * They run in the context's kernel precision (default ENMF_PRECISION_FP64). */

@@ -120,9 +120,8 @@ ENMF_DEV void allreduce_gain(const View& v, double gain, int nf, double* gsum, i
   *nfor = f;
 }
 
-// Barrier only (after the all-gather stores).
-__global__ void barrier(View v, const DevState* st) {
-  if (st && !dev_active(st)) return;
+// Barrier only (after the all-gather stores): thread 0 of the calling block.
+ENMF_DEV void barrier_body(const View& v) {
   if (threadIdx.x == 0) {
     const unsigned long long e = ++(*v.epoch);
     signal_and_wait(v, e);
@@ -131,13 +130,13 @@ __global__ void barrier(View v, const DevState* st) {
 
 // All-gather of a factor shard: local (r × cnt, row-major, ld cnt) is stored
 // into columns [off, off+cnt) of every rank's replica (r × full, ld full).
-__global__ void scatter_shard(View v, const double* __restrict__ local, int r, long cnt, long off, long full, int which,
-                              const DevState* st) {
-  if (st && !dev_active(st)) return;
+// tid / nthreads: the calling thread's index among the threads that share the copy.
+ENMF_DEV void scatter_body(const View& v, const double* __restrict__ local, int r, long cnt, long off, long full,
+                           int which, long tid, long nthreads) {
   const long total = (long)r * cnt;
   for (int q = 0; q < v.world; ++q) {
     double* dst = which == 0 ? v.full_peer_w[q] : v.full_peer_t[q];
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    for (long e = tid; e < total; e += nthreads) {
       const long k = e / cnt, j = e % cnt;
       dst[k * full + off + j] = local[e];
     }
@@ -152,22 +151,55 @@ __global__ void allreduce_inplace(const View* v, double* buf, int count, const D
 
 __global__ void barrier_k(const View* v, const DevState* st) {
   if (st && !dev_active(st)) return;
-  if (threadIdx.x == 0) {
-    const unsigned long long e = ++(*v->epoch);
-    signal_and_wait(*v, e);
-  }
+  barrier_body(*v);
 }
 
 __global__ void scatter_shard_k(const View* v, const double* __restrict__ local, int r, long cnt, long off, long full,
                                 int which, const DevState* st) {
   if (st && !dev_active(st)) return;
-  const long total = (long)r * cnt;
-  for (int q = 0; q < v->world; ++q) {
-    double* dst = which == 0 ? v->full_peer_w[q] : v->full_peer_t[q];
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
-      const long k = e / cnt, j = e % cnt;
-      dst[k * full + off + j] = local[e];
+  scatter_body(*v, local, r, cnt, off, full, which, blockIdx.x * (long)blockDim.x + threadIdx.x,
+               (long)gridDim.x * blockDim.x);
+}
+
+// Self-test of the exchange primitives with `world` ranks on ONE GPU: block p of a cooperative
+// launch (all blocks co-resident, so the spin-waits always make progress) plays rank p with its
+// own View — own flags, slots, replicas and epoch counter, all in this process's memory — and
+// runs `epochs` rounds of every exchange the engine uses: the block all-reduce (Gram / error
+// partials), the scalar gain and max exchanges of the sweeps and BPP, and the shard all-gather +
+// barrier.  out[p] receives what rank p ended up with, for the host to compare with the
+// rank-ordered sums and across ranks (enmf_gpu_dist_selftest).
+//   in:  [world][count]      per-rank contribution (round e uses in·(e+1))
+//   red: [world][epochs][count] all-reduced values;  sc: [world][epochs][3] gain sum, flag, max
+//   rep: each rank's r × full replica ends up holding round (epochs-1)'s shards of every rank
+__global__ void selftest(const View* views, int count, int epochs, const double* in, double* red, double* sc,
+                         double* stage, int r, long full) {
+  const View& v = views[blockIdx.x];
+  const int p = v.rank, P = v.world;
+  double* mine = stage + (long)p * (count + (long)r * full);     // [count] contribution | [r × cnt] shard
+  double* shard = mine + count;
+  const long base = full / P, extra = full % P;
+  const long cnt = base + (p < extra ? 1 : 0), off = p * base + (p < extra ? p : extra);
+  for (int e = 0; e < epochs; ++e) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) mine[i] = __dmul_rn(in[(long)p * count + i], (double)(e + 1));
+    __syncthreads();
+    allreduce_block(v, mine, count, red + ((long)p * epochs + e) * count);
+    if (threadIdx.x == 0) {
+      double g;
+      int f;
+      allreduce_gain(v, __dmul_rn(in[(long)p * count], (double)(e + 2)), (p == e % P) ? 1 : 0, &g, &f);
+      double* o = sc + ((long)p * epochs + e) * 3;
+      o[0] = g;
+      o[1] = (double)f;
+      o[2] = allmax_scalar(v, __dmul_rn(in[(long)p * count + (count > 1 ? 1 : 0)], (double)(1 + (e + p) % P)));
     }
+    __syncthreads();
+    for (long i = threadIdx.x; i < (long)r * cnt; i += blockDim.x)
+      shard[i] = (double)(1000 * e + 10 * p) + 1e-3 * (double)i;
+    __syncthreads();
+    scatter_body(v, shard, r, cnt, off, full, e & 1, threadIdx.x, blockDim.x);
+    __syncthreads();
+    barrier_body(v);
+    __syncthreads();
   }
 }
 

@@ -58,6 +58,24 @@ def torch_exchange(group=None) -> Callable[[bytes], List[bytes]]:
     return ex
 
 
+def exchange_selftest(ctx: Context, world: int, contributions: np.ndarray, epochs: int, r: int, full: int):
+    """The exchange primitives of csrc/dist.cuh with `world` ranks on ONE GPU (one cooperative launch,
+    block p = rank p; enmf_gpu_dist_selftest).  contributions: (world, count).  Returns (red, sc,
+    rep_w, rep_t): red[p, e] = rank p's all-reduced vector of round e (contributions·(e+1) summed in
+    rank order), sc[p, e] = (gain sum, flag OR, max), rep_*[p] = rank p's r×full replicas."""
+    a = _f64(contributions, "contributions")
+    if a.ndim != 2 or a.shape[0] != world:
+        raise ValueError("exchange_selftest: contributions must be (world, count)")
+    count = a.shape[1]
+    red = np.empty((world, epochs, count))
+    sc = np.empty((world, epochs, 3))
+    rep_w = np.empty((world, r, full))
+    rep_t = np.empty((world, r, full))
+    _check(ctx._lib.enmf_gpu_dist_selftest(ctx._h, world, count, epochs, r, full, _p(a), _p(red), _p(sc),
+                                           _p(rep_w), _p(rep_t)))
+    return red, sc, rep_w, rep_t
+
+
 class ShardedContext(Context):
     """An enmf_gpu_ctx in sharded mode (rank `rank` of `world`)."""
 
