@@ -36,6 +36,7 @@
 #include "ozk.cuh"
 #include "tf32k.cuh"
 #include "sweep_tf32.cuh"
+#include "hals_rl.cuh"
 
 namespace {
 
@@ -544,6 +545,38 @@ void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   CU(cudaLaunchKernelEx(&lc, hals::sweep_tf32<R_>, a, ntiles));
 }
 
+// TF32 variant, 64 < r <= 128: right-looking sweeps with the residual in tensor memory and
+// tcgen05 rank-8 updates (hals_rl.cuh) when every CTA's columns fit its two 128-column tiles;
+// ENMF_TF32_SWEEP=mma keeps the mma.sync left-looking kernel (A/B)
+bool sweep_rl_fits(const enmf_gpu_ctx* c, const hals::Args& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("ENMF_TF32_SWEEP");
+    return e && std::strcmp(e, "mma") == 0;
+  }();
+  return !off && a.r > 64 && a.r <= 128 && (long)a.N <= 256L * c->sms;
+}
+
+void launch_sweep_rl(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
+  const unsigned grid = (unsigned)std::max(1L, std::min<long>(c->sms, ((long)a.N + 127) / 128));
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)hals::sweep_rl<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            hals::rl_smem_bytes()));
+    attr = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = hals::rl_smem_bytes();
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&lc, hals::sweep_rl<128>, a));
+}
+
 template <int R_, bool PERSIST = false>
 void launch_sweep_ws(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   const long ntiles = ((long)a.N + 7) / 8;
@@ -606,6 +639,7 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   if (prec == PREC_TF32 && (v == 54 || v == 55)) {  // TF32 variant: block products on the TF32 tensor cores
     if (r <= 32) launch_sweep_tf32<32>(c, s, a);
     else if (r <= 64) launch_sweep_tf32<64>(c, s, a);
+    else if (sweep_rl_fits(c, a)) launch_sweep_rl(c, s, a);
     else launch_sweep_tf32<128>(c, s, a);
   } else if (v == 1) {
 #define SW(S_, T_)                                                                          \

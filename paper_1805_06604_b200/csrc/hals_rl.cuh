@@ -1,0 +1,256 @@
+// hals_rl.cuh — HALS sweeps of the TF32 variant (ENMF_PRECISION_TF32, 64 < r <= 128) on the
+// tcgen05 tensor cores: RIGHT-LOOKING blocked Gauss-Seidel with the residual in tensor memory
+// (nnls.hpp:111-176; the variant's contract is the final relative error within 1e-4 of FP64).
+//
+// The left-looking sweeps (sweep_tm, sweep_tf32) form S_b = G[b rows, :]·H before every 8-row
+// block: M = 8 per product, which only mma.sync shapes fit.  Here the residual
+//     Rᵀ[column][k] = C[k][column] − Σ_j G[k][j]·H[j][column]
+// of the CTA's ≤ 256 columns lives in TMEM for the whole inner solve (two accumulator tiles of
+// 128 lanes × 128 FP32 columns: lane = column of H, TMEM column = row k), and is kept current
+// by RANK-8 UPDATES on the tensor core: once the 8 rows of block b are solved,
+//     Rᵀ += (−ΔH_bᵀ) · G[b rows, :]        one tcgen05.mma.kind::tf32, M = 128, N = 128, K = 8
+// with A = the 128 columns' eight −Δh values, written by the row threads straight into eight
+// TMEM columns (tcgen05.st → TS-form MMA, no shared-memory round trip), and B = block b's Gram
+// rows from shared memory (K-major core-matrix tiles, staged once per solve).  The row pass of a
+// block is one thread per column: r_k from its TMEM lane (tcgen05.ld.32x32b), t = h + r/G_kk,
+// h' = max(t, 0), the in-block chain r_l −= G_lk·Δh_k in FP32, the gain term.  The errors of the
+// TF32 products scale with Δh (they vanish as the solve converges) instead of with H as in the
+// left-looking form; only the first residual R = C − G·H0 is a full TF32 product, formed with H0
+// split into a TF32 head and tail (two MMAs per k-step) against TF32-rounded G.
+//
+// Per CTA: two independent column groups (warps 0-3 ↔ tile 0, warps 4-7 ↔ tile 1), each with its
+// own mbarrier, named barrier and issuing thread, so one group's MMA round trip overlaps the
+// other's row pass.  H itself (the iterate, FP32) sits in shared memory in the A-operand layout
+// (used as the SS-form A of the first product, then as plain storage).  The kernel is resident
+// only: the launcher uses it when every CTA's columns fit its two tiles (N <= 256·grid) and
+// falls back to sweep_tf32 otherwise.  Grid-wide stall decision: grid_decision (hals.cuh).
+#pragma once
+
+#include "hals.cuh"
+#include "sweep_tf32.cuh"
+#include "tc.cuh"
+
+namespace hals {
+
+constexpr int RL_GB = 16 * 4096;        // B tiles of G (TF32): 16 row blocks × (128 n × 8 k × 4 B)
+constexpr int RL_HA = 128 * 128 * 4;    // one tile of Hᵀ in the K-major A layout (128 m × 128 k)
+constexpr int RL_GC = 16 * 48 * 4;      // row-pass constants per block (FP32)
+constexpr int rl_smem_bytes() { return 1024 + RL_GB + 2 * RL_HA + RL_GC + 64; }
+
+// canonical no-swizzle K-major tiles (core matrix = 8 rows × 16 B):
+// A (m = column of H, k = row): core matrices adjacent along K 128 B apart, 8-row groups 4 KB apart
+ENMF_DEV int rl_a_off(int m, int k) { return (m >> 3) * 4096 + (k >> 2) * 128 + (m & 7) * 16 + (k & 3) * 4; }
+// B of block b (n = row index of G, kk = row within the block): K halves 128 B apart, groups 256 B
+ENMF_DEV int rl_b_off(int b, int n, int kk) { return b * 4096 + (n >> 3) * 256 + (kk >> 2) * 128 + (n & 7) * 16 + (kk & 3) * 4; }
+
+ENMF_DEV void rl_ld8(uint32_t ta, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(ta));
+}
+ENMF_DEV void rl_wait_ld8(uint32_t (&v)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+               :
+               : "memory");
+}
+ENMF_DEV void rl_st8(uint32_t ta, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+ENMF_DEV void rl_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+ENMF_DEV void rl_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+ENMF_DEV void rl_bar(int id) { asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory"); }
+
+// D[tmem] += A[tmem: 128 lanes × 8 TF32 columns] · B[smem]ᵀ (TS form)
+ENMF_DEV void rl_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
+  static_assert(RMAX == 128, "two 128 × 128 residual tiles");
+  constexpr int NB = RMAX / 8;
+  if (sweep_skipped(a)) return;
+  extern __shared__ uint8_t rl_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rl_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Gb = sm;                                        // B tiles
+  uint8_t* Ha = sm + RL_GB;                                // [tile] Hᵀ, A layout
+  float* Gc = reinterpret_cast<float*>(sm + RL_GB + 2 * RL_HA);   // [NB][48]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + RL_GB + 2 * RL_HA + RL_GC);   // one per tile group
+  __shared__ double red[256 + 33];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = warp >> 2, quarter = warp & 3;
+  const int mloc = 32 * quarter + lane;                    // this thread's column within its tile
+  const int r = a.r;
+
+  // ---- per-solve staging: Gram B tiles (TF32, round to nearest) and row-pass constants
+  for (int e = threadIdx.x; e < NB * 128 * 8; e += 256) {
+    const int b = e >> 10, n = (e >> 3) & 127, kk = e & 7;
+    const int row = 8 * b + kk;
+    const float v = (row < r && n < r) ? tf32_round((float)a.G[(long)row * r + n]) : 0.f;
+    *reinterpret_cast<float*>(Gb + rl_b_off(b, n, kk)) = v;
+  }
+  for (int e = threadIdx.x; e < NB * 48; e += 256) {
+    const int b = e / 48, j = e % 48;
+    double v = 0.0;
+    if (j < 28) {
+      int l = 1;
+      while (l * (l + 1) / 2 <= j) ++l;
+      const int i = j - l * (l - 1) / 2, k = 8 * b + l, c = 8 * b + i;
+      v = (k < r && c < r) ? a.G[(long)k * r + c] : 0.0;
+    } else if (j < 44) {
+      const int k = 8 * b + ((j - 28) & 7);
+      const double d = k < r ? a.G[(long)k * r + k] : 1.0;
+      v = j < 36 ? 0.5 * d : 1.0 / d;
+    }
+    Gc[e] = (float)v;
+  }
+  if (threadIdx.x == 0) {
+    tc::mbar_init(mbar, 1);
+    tc::mbar_init(mbar + 1, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  rl_proxy_fence();                                        // B tiles: generic-proxy stores → tensor core reads
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+
+  // this CTA's columns [c0, c0 + cnt), cnt <= 256; tile 0 = the first 128, tile 1 = the rest
+  const long c0 = (long)blockIdx.x * a.N / gridDim.x, c1 = (long)(blockIdx.x + 1) * a.N / gridDim.x;
+  const int cnt = (int)(c1 - c0);
+  const int tcols = tile == 0 ? min(cnt, 128) : max(cnt - 128, 0);   // columns of this thread's tile
+  const bool active = tcols > 0;                           // (warp-uniform, group-uniform)
+  const bool valid = mloc < tcols;
+  const long col = c0 + tile * 128 + mloc;
+  const uint32_t tR = tmem_base + (uint32_t)(tile * 128) + ((uint32_t)(32 * quarter) << 16);   // residual tile
+  const uint32_t tS = tmem_base + 256u + (uint32_t)(tile * 8) + ((uint32_t)(32 * quarter) << 16);   // −Δ staging
+  const uint32_t dR = tmem_base + (uint32_t)(tile * 128), dS = tmem_base + 256u + (uint32_t)(tile * 8);
+  uint8_t* Ht = Ha + tile * RL_HA;
+  uint64_t* mb = mbar + tile;
+  uint32_t mph = 0;                                        // mbarrier phase of this group
+  constexpr uint32_t IDESC = tc::idesc_tf32(128, 128);
+  const uint64_t dB0 = tc::desc_noswz(tc::smem_u32(Gb), 128, 256);
+  const uint64_t dA0 = tc::desc_noswz(tc::smem_u32(Ht), 128, 4096);
+  const bool issuer = (threadIdx.x & 127) == 0;
+  const int bar_id = 1 + tile;
+  const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
+  const double* hsrc = src + (valid ? col : 0);
+  const double* csrc = a.C + (valid ? col : 0);
+
+  if (active) {
+    // ---- R = C − G·H0: C into the residual tile, then two SS-form passes over k with A = −head(H0)
+    // and A = −tail(H0) (TF32 head/tail split of the FP32 value)
+#pragma unroll 1
+    for (int k0 = 0; k0 < RMAX; k0 += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = __float_as_uint((valid && k0 + i < r) ? (float)csrc[(long)(k0 + i) * a.ld] : 0.f);
+      rl_st8(tR + k0, v);
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll 1
+      for (int k = 0; k < RMAX; ++k) {
+        const float h = (valid && k < r) ? (float)hsrc[(long)k * a.ld] : 0.f;
+        const float hi = tf32_round(h);
+        *reinterpret_cast<float*>(Ht + rl_a_off(mloc, k)) = pass == 0 ? -hi : -tf32_round(h - hi);
+      }
+      rl_wait_st();
+      rl_proxy_fence();
+      tc::fence_before();
+      rl_bar(bar_id);
+      if (issuer) {
+        tc::fence_after();
+#pragma unroll 1
+        for (int s = 0; s < NB; ++s)
+          tc::mma_tf32(dR, dA0 + (uint64_t)((s * 256) >> 4), dB0 + (uint64_t)((s * 4096) >> 4), IDESC, 1u);
+        tc::commit(mb);
+      }
+      tc::mbar_wait(mb, mph);
+      mph ^= 1;
+      tc::fence_after();
+    }
+    // the iterate itself (FP32, unrounded) replaces the staged operand
+#pragma unroll 1
+    for (int k = 0; k < RMAX; ++k)
+      *reinterpret_cast<float*>(Ht + rl_a_off(mloc, k)) = (valid && k < r) ? (float)hsrc[(long)k * a.ld] : 0.f;
+    __syncwarp();
+  }
+
+  double first_total = 0.0;
+  for (int sw = 0;; ++sw) {
+    float gain = 0.f;
+    int hmax = 0;
+    if (active) {
+#pragma unroll 1
+      for (int b = 0; b < NB; ++b) {
+        float gc[44];
+#pragma unroll
+        for (int j = 0; j < 11; ++j) {
+          const float4 v = reinterpret_cast<const float4*>(Gc + b * 48)[j];
+          gc[4 * j] = v.x; gc[4 * j + 1] = v.y; gc[4 * j + 2] = v.z; gc[4 * j + 3] = v.w;
+        }
+        const float4 h0 = *reinterpret_cast<const float4*>(Ht + rl_a_off(mloc, 8 * b));
+        const float4 h1 = *reinterpret_cast<const float4*>(Ht + rl_a_off(mloc, 8 * b + 4));
+        float x[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        uint32_t rv[8];
+        rl_ld8(tR + 8 * b, rv);
+        rl_wait_ld8(rv);
+        float rr[8], hn[8];
+        uint32_t dv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rr[k] = __uint_as_float(rv[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float t = fmaf(rr[k], gc[36 + k], x[k]);   // h + r/G_kk
+          const float h = pos_part_f(t);
+          const float d = h - x[k];
+          hn[k] = h;
+#pragma unroll
+          for (int l = k + 1; l < 8; ++l) rr[l] = fmaf(-gc[l * (l - 1) / 2 + k], d, rr[l]);
+          dv[k] = __float_as_uint(tf32_round(-d));
+          // G_kk((x−t)² − (h−t)²) = (x−h)(x+h−2t)·G_kk, accumulated halved
+          gain = fmaf(-d * gc[28 + k], fmaf(-2.f, t, x[k] + h), gain);
+          hmax = max(hmax, __float_as_int(h));
+        }
+        rl_st8(tS, dv);
+        *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b)) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+        *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b + 4)) = make_float4(hn[4], hn[5], hn[6], hn[7]);
+        rl_wait_st();
+        tc::fence_before();
+        rl_bar(bar_id);
+        if (issuer) {
+          tc::fence_after();
+          rl_mma_ts(dR, dS, dB0 + (uint64_t)((b * 4096) >> 4), IDESC);
+          tc::commit(mb);
+        }
+        tc::mbar_wait(mb, mph);                            // the residual is current again
+        mph ^= 1;
+        tc::fence_after();
+      }
+    }
+    const int nf = hmax >= 0x7F800000 ? 1 : 0;
+    const int cont = grid_decision(a, (double)gain, nf, sw, first_total, red);
+    if (!cont) break;
+  }
+  // the result: this CTA's columns of H (rows < r)
+  if (active && valid)
+    for (int k = 0; k < r; ++k) a.H[(long)k * a.ld + col] = (double)*reinterpret_cast<const float*>(Ht + rl_a_off(mloc, k));
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace hals

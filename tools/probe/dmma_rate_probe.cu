@@ -9,7 +9,7 @@
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b) : "memory");
 }
 
 template <int ACC, int MODE>
@@ -22,6 +22,7 @@ __global__ void k(long long* out, double* sink, int iters) {
     b[i] = 0.999 - 1e-3 * (threadIdx.x + 2 * i);
   }
   const long long t0 = clock64();
+#pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep)
