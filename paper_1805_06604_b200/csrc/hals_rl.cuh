@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   static_assert(RMAX == 128, "two 128 × 128 residual tiles");
   constexpr int NB = RMAX / 8;
   if (sweep_skipped(a)) return;
-  extern __shared__ uint8_t rl_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rl_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(128) uint8_t rl_raw[];     // (no-swizzle operand tiles: 16-byte alignment suffices)
+  uint8_t* sm = rl_raw;
   uint8_t* Gb = sm;                                        // B tiles
   uint8_t* Ha = sm + RL_GB;                                // [tile] Hᵀ, A layout
   float* Gc = reinterpret_cast<float*>(sm + RL_GB + 2 * RL_HA);   // [NB][48]
@@ -91,11 +91,19 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   const int r = a.r;
 
   // ---- per-solve staging: Gram B tiles (TF32, round to nearest) and row-pass constants
-  for (int e = threadIdx.x; e < NB * 128 * 8; e += 256) {
-    const int b = e >> 10, n = (e >> 3) & 127, kk = e & 7;
-    const int row = 8 * b + kk;
-    const float v = (row < r && n < r) ? tf32_round((float)a.G[(long)row * r + n]) : 0.f;
-    *reinterpret_cast<float*>(Gb + rl_b_off(b, n, kk)) = v;
+#pragma unroll 1
+  for (int e0 = threadIdx.x; e0 < NB * 128 * 8; e0 += 256 * 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {                          // 8 loads in flight
+      const int e = e0 + 256 * u, row = e >> 7, n = e & 127;
+      v[u] = (row < r && n < r) ? (float)a.G[(long)row * r + n] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + 256 * u, row = e >> 7, n = e & 127;
+      *reinterpret_cast<float*>(Gb + rl_b_off(row >> 3, n, row & 7)) = tf32_round(v[u]);
+    }
   }
   for (int e = threadIdx.x; e < NB * 48; e += 256) {
     const int b = e / 48, j = e % 48;
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   if (active) {
     // ---- R = C − G·H0: C into the residual tile, then two SS-form passes over k with A = −head(H0)
     // and A = −tail(H0) (TF32 head/tail split of the FP32 value)
-#pragma unroll 1
+#pragma unroll 2
     for (int k0 = 0; k0 < RMAX; k0 += 8) {
       uint32_t v[8];
 #pragma unroll
@@ -157,13 +165,24 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
       rl_st8(tR + k0, v);
     }
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 3; ++pass) {               // pass 2 leaves the iterate itself (FP32, unrounded)
 #pragma unroll 1
-      for (int k = 0; k < RMAX; ++k) {
-        const float h = (valid && k < r) ? (float)hsrc[(long)k * a.ld] : 0.f;
-        const float hi = tf32_round(h);
-        *reinterpret_cast<float*>(Ht + rl_a_off(mloc, k)) = pass == 0 ? -hi : -tf32_round(h - hi);
+      for (int k0 = 0; k0 < RMAX; k0 += 16) {
+        float h[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) h[i] = (valid && k0 + i < r) ? (float)hsrc[(long)(k0 + i) * a.ld] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          float o[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float hi = tf32_round(h[i + u]);
+            o[u] = pass == 0 ? -hi : pass == 1 ? -tf32_round(h[i + u] - hi) : h[i + u];
+          }
+          *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, k0 + i)) = make_float4(o[0], o[1], o[2], o[3]);
+        }
       }
+      if (pass == 2) break;
       rl_wait_st();
       rl_proxy_fence();
       tc::fence_before();
@@ -179,10 +198,6 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
       mph ^= 1;
       tc::fence_after();
     }
-    // the iterate itself (FP32, unrounded) replaces the staged operand
-#pragma unroll 1
-    for (int k = 0; k < RMAX; ++k)
-      *reinterpret_cast<float*>(Ht + rl_a_off(mloc, k)) = (valid && k < r) ? (float)hsrc[(long)k * a.ld] : 0.f;
     __syncwarp();
   }
 
@@ -193,6 +208,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
     if (active) {
 #pragma unroll 1
       for (int b = 0; b < NB; ++b) {
+        // everything that does not need the residual first: constants and the block's old rows
         float gc[44];
 #pragma unroll
         for (int j = 0; j < 11; ++j) {
@@ -202,6 +218,11 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
         const float4 h0 = *reinterpret_cast<const float4*>(Ht + rl_a_off(mloc, 8 * b));
         const float4 h1 = *reinterpret_cast<const float4*>(Ht + rl_a_off(mloc, 8 * b + 4));
         float x[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        if (sw > 0 || b > 0) {                             // the previous block's update is in
+          tc::mbar_wait(mb, mph);
+          mph ^= 1;
+          tc::fence_after();
+        }
         uint32_t rv[8];
         rl_ld8(tR + 8 * b, rv);
         rl_wait_ld8(rv);
@@ -212,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float t = fmaf(rr[k], gc[36 + k], x[k]);   // h + r/G_kk
-          const float h = pos_part_f(t);
+          const float h = fmaxf(t, 0.f);                   // NaN -> 0, as `t > 0 ? t : 0`
           const float d = h - x[k];
           hn[k] = h;
 #pragma unroll
@@ -233,9 +254,6 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
           rl_mma_ts(dR, dS, dB0 + (uint64_t)((b * 4096) >> 4), IDESC);
           tc::commit(mb);
         }
-        tc::mbar_wait(mb, mph);                            // the residual is current again
-        mph ^= 1;
-        tc::fence_after();
       }
     }
     const int nf = hmax >= 0x7F800000 ? 1 : 0;
@@ -245,6 +263,10 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   // the result: this CTA's columns of H (rows < r)
   if (active && valid)
     for (int k = 0; k < r; ++k) a.H[(long)k * a.ld + col] = (double)*reinterpret_cast<const float*>(Ht + rl_a_off(mloc, k));
+  if (active) {                                            // drain the last MMA before the TMEM is freed
+    tc::mbar_wait(mb, mph);
+    tc::fence_after();
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) {

@@ -14,6 +14,8 @@ G = w.T @ w
 C = G @ rng.random((r, n)) * 0.9
 h0 = rng.random((r, n))
 ctx = E.Context()
+if os.environ.get("SWEEP_PREC") == "tf32":   # the TF32 variant's sweep kernels (hals_rl.cuh / sweep_tf32.cuh)
+    ctx.set_precision(E.Precision.tf32)
 for ms in (2, 4, 8, 16, 32, 64, 129, 129, 64, 8):
     t = time.perf_counter()
     h, sw = ctx.hals_solve(G, C, h0, ms, 1e-300)
