@@ -26,11 +26,12 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"ozk::finish" -s 2 -c 1 -o gpurun_out/prof_finish -f $CMD > gpurun_out/ncu_finish.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tf32k::gemm" -s 2 -c 1 -o gpurun_out/prof_tf32k -f $CMD > gpurun_out/ncu_tf32k.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_f64_dmma_t -s 4 -c 1 -o gpurun_out/prof_gram -f $CMD > gpurun_out/ncu_gram.log 2>&1
+  SWEEP_PREC=tf32 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_rl -s 6 -c 1 -o gpurun_out/prof_rl -f python tools/sweep_scan.py > gpurun_out/ncu_rl.log 2>&1
   BATCH=296 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"batch::run" -s 1 -c 1 -o gpurun_out/prof_batch -f python tools/batch_throughput.py > gpurun_out/ncu_batch.log 2>&1
   echo "ncu done" >> gpurun_out/ncu_batch.log
   # summarise on the box, keep only the sweep capture (gpurun copies back <= 64 MiB)
-  for f in tm pair finish tf32k gram batch; do
+  for f in tm pair finish tf32k gram batch rl; do
     [ -f gpurun_out/prof_$f.ncu-rep ] && python tools/ncu_report.py gpurun_out/prof_$f.ncu-rep "$f" > gpurun_out/summary_$f.txt 2>&1
   done
-  rm -f gpurun_out/prof_pair.ncu-rep gpurun_out/prof_finish.ncu-rep gpurun_out/prof_tf32k.ncu-rep gpurun_out/prof_gram.ncu-rep gpurun_out/prof_batch.ncu-rep
+  rm -f gpurun_out/prof_pair.ncu-rep gpurun_out/prof_finish.ncu-rep gpurun_out/prof_tf32k.ncu-rep gpurun_out/prof_gram.ncu-rep gpurun_out/prof_batch.ncu-rep gpurun_out/prof_rl.ncu-rep
 fi
