@@ -219,6 +219,14 @@ int enmf_gpu_dist_finalize(enmf_gpu_ctx* ctx);
 int enmf_gpu_dist_selftest(enmf_gpu_ctx* ctx, int world, int count, int epochs, int r, size_t full,
                            const double* in, double* red, double* sc, double* rep_w, double* rep_t);
 
+/* hals_solve (nnls.hpp:154-176) of an r x n problem sharded by columns over `world` ranks that all
+ * run on THIS GPU in one cooperative launch (64 < r <= 128): the sharded engine's sweep path — the
+ * synchronous grid decision with the per-sweep cross-rank gain exchange — with every rank
+ * co-resident.  h: r x n result; sweeps: world entries, identical on every rank. */
+int enmf_gpu_hals_solve_vranks(enmf_gpu_ctx* ctx, const double* gram, const double* cross, const double* h0,
+                               size_t r, size_t n, int world, uint64_t max_sweeps, double stall_fraction,
+                               double* h, int32_t* sweeps);
+
 /* ---- public kernels the reference's tests call (host pointers) --------------
  * They run in the context's kernel precision (default ENMF_PRECISION_FP64). */
 int enmf_gpu_set_precision(enmf_gpu_ctx* ctx, int precision);

@@ -67,7 +67,7 @@ EXPORTS = [
     "enmf_gpu_active_set_solve", "enmf_gpu_begin", "enmf_gpu_step", "enmf_gpu_step_profiled",
     "enmf_gpu_sync", "enmf_gpu_end", "enmf_gpu_stream", "enmf_gpu_digit_levels",
     "enmf_gpu_dist_shard", "enmf_gpu_dist_alloc", "enmf_gpu_dist_init", "enmf_gpu_load_dense_sharded",
-    "enmf_gpu_dist_finalize", "enmf_gpu_dist_selftest", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
+    "enmf_gpu_dist_finalize", "enmf_gpu_dist_selftest", "enmf_gpu_hals_solve_vranks", "enmf_gpu_load_csr", "enmf_gpu_last_error_line",
     "enmf_gpu_optimal_beta_linesearch", "enmf_gpu_optimal_beta_linesearch_csr",
     "enmf_gpu_batch_eligible", "enmf_gpu_run_batch_dense",
     # data formats and generators (csrc/io.cpp)
@@ -142,6 +142,8 @@ def load() -> C.CDLL:
     L.enmf_gpu_dist_init.argtypes = [vp, C.c_void_p]
     L.enmf_gpu_load_dense_sharded.argtypes = [vp, dp, dp, C.c_int]
     L.enmf_gpu_dist_finalize.argtypes = [vp]
+    L.enmf_gpu_hals_solve_vranks.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p, sz, sz, C.c_int, C.c_uint64,
+                                             C.c_double, C.c_void_p, C.c_void_p]
     L.enmf_gpu_dist_selftest.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, sz, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
     L.enmf_gpu_last_error_line.restype = sz

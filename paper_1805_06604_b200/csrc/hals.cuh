@@ -49,6 +49,11 @@ struct Args {
   const dist::View* dv;     // multi-GPU: all-reduce the sweep gain across ranks (nullable)
   const double* Gf;         // sweep_ws: Gram in A-fragment order (ws_prep)
   double* H2;               // sweep_tm: r×N scratch (row stride ld) for odd sweeps (speculative stall decision)
+  // virtual ranks (sweep_tm_vr, one cooperative launch over several ranks' column shards — the
+  // on-device check of the sharded sweep path, enmf_gpu_hals_solve_vranks): rank v's arguments
+  // and the CTAs per rank
+  const Args* vargs;
+  int vblocks;
 };
 
 ENMF_DEV void set_cond(const Args& a, unsigned v) {
@@ -365,20 +370,23 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
 // (nnls.hpp:172-173).  Single GPU: every CTA forms the same fixed-order total once all
 // partials are in and decides itself; sharded: the last CTA exchanges the gain with the other
 // ranks and publishes the decision.  Returns 1 to continue (same value in every thread).
-ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& first_total, double* red) {
+// bid / nblk: this CTA's index and the CTA count of its grid (of its virtual rank's share of the
+// grid in sweep_tm_vr).
+ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& first_total, double* red,
+                           unsigned bid = blockIdx.x, unsigned nblk = gridDim.x) {
   __shared__ int s_dec;
   const double bg = block_reduce_sum_any(__dadd_rn(gain, gain), red);   // gains are accumulated halved
   const int bnf = __syncthreads_or(nf);
-  const unsigned target = (unsigned)(sw + 1) * gridDim.x;
+  const unsigned target = (unsigned)(sw + 1) * nblk;
   // partials double-buffered by sweep parity: a CTA that has already decided sweep sw and
   // runs ahead writes its sweep sw+1 partial into the other half, never into the one a slower
   // CTA may still be summing (it can only come back to this half after every CTA has arrived
   // at sweep sw+1, i.e. after every CTA finished reading sweep sw's partials)
-  double* part = a.part + (sw & 1) * gridDim.x;
-  int* part_nf = a.part_nf + (sw & 1) * gridDim.x;
+  double* part = a.part + (sw & 1) * nblk;
+  int* part_nf = a.part_nf + (sw & 1) * nblk;
   if (threadIdx.x == 0) {
-    part[blockIdx.x] = bg;
-    part_nf[blockIdx.x] = bnf;
+    part[bid] = bg;
+    part_nf[bid] = bnf;
     __threadfence();
     const unsigned prev = atomicAdd(&a.ctl->arrive, 1u);
     s_dec = prev == target - 1 ? 1 : 0;      // this CTA arrived last (used when sharded)
@@ -393,7 +401,7 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
     __syncthreads();
     double v = 0.0;
     int f = 0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    for (int b = threadIdx.x; b < (int)nblk; b += blockDim.x) {
       v = __dadd_rn(v, __ldcg(part + b));
       f |= __ldcg(part_nf + b);
     }
@@ -402,7 +410,7 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
     if (sw == 0) first_total = total;
     const bool stop = (sw + 1 >= a.max_sweeps) ||
                       (total <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
-    if (blockIdx.x == 0 && threadIdx.x == 0) finish_sweep(a, total, f);   // bookkeeping (same rule)
+    if (bid == 0 && threadIdx.x == 0) finish_sweep(a, total, f);   // bookkeeping (same rule)
     __syncthreads();
     return stop ? 0 : 1;
   }
@@ -411,7 +419,7 @@ ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& f
     __threadfence();
     double v = 0.0;
     int f = 0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    for (int b = threadIdx.x; b < (int)nblk; b += blockDim.x) {
       v = __dadd_rn(v, __ldcg(part + b));
       f |= __ldcg(part_nf + b);
     }

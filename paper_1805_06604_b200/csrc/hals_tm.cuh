@@ -266,18 +266,18 @@ ENMF_DEV int tm_producer_round_nt(int nt, uint32_t tq, double* Ss, const double2
 // its sweep-s gain partial, then forms the total in a fixed order (lane l sums CTAs l, l+32, ...,
 // then a fixed xor tree), so every CTA reaches the identical decision; CTA 0 also does the
 // solve's bookkeeping (sweep count, first/last gain, sticky non-finite flag, NaN guard).
-ENMF_DEV int tm_decide(const Args& a, int s, double& first_total) {
+ENMF_DEV int tm_decide(const Args& a, int s, double& first_total, unsigned bid, unsigned nblk) {
   const int lane = threadIdx.x & 31;
-  const unsigned target = (unsigned)(s + 1) * gridDim.x;
+  const unsigned target = (unsigned)(s + 1) * nblk;
   unsigned e;
   do {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
   } while (e < target);
-  const double* part = a.part + (s & 1) * gridDim.x;
-  const int* part_nf = a.part_nf + (s & 1) * gridDim.x;
+  const double* part = a.part + (s & 1) * nblk;
+  const int* part_nf = a.part_nf + (s & 1) * nblk;
   double v = 0.0;
   int f = 0;
-  for (int b = lane; b < (int)gridDim.x; b += 32) {
+  for (int b = lane; b < (int)nblk; b += 32) {
     v = __dadd_rn(v, __ldcg(part + b));
     f |= __ldcg(part_nf + b);
   }
@@ -286,7 +286,7 @@ ENMF_DEV int tm_decide(const Args& a, int s, double& first_total) {
   f = __any_sync(0xffffffffu, f) ? 1 : 0;
   if (s == 0) first_total = v;
   const bool stop = (s + 1 >= a.max_sweeps) || (v <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
-  if (blockIdx.x == 0 && lane == 0) finish_sweep(a, v, f);
+  if (bid == 0 && lane == 0) finish_sweep(a, v, f);
   return stop ? 1 : 0;
 }
 
@@ -309,8 +309,10 @@ ENMF_DEV void tm_stage(uint32_t tg, const double* src, long ld, long col, int nc
   }
 }
 
+// bid / nblk: this CTA's index and the CTA count of its grid (sweep_tm), or of its virtual rank's
+// share of the grid (sweep_tm_vr)
 template <int RMAX>
-__global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
+ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsigned nblk) {
   static_assert(RMAX == 128, "two 32-column groups of RMAX rows fill a TMEM lane quarter");
   constexpr int NB = RMAX / 8;
   constexpr int KS = RMAX / 4;
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   const uint32_t tq = tmem_base + ((uint32_t)(32 * pair) << 16);   // this pair's lane quarter
 
   const int idS = 1 + pair, idH = 5 + pair, idP = 9 + pair;
-  const long P = (long)gridDim.x * 4, q = (long)blockIdx.x * 4 + pair;
+  const long P = (long)nblk * 4, q = (long)bid * 4 + pair;
   const long tq0 = q * ntiles / P, cnt = (q + 1) * ntiles / P - tq0;
   const int rounds = (int)((cnt + 7) / 8);
   const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
   for (int sw = 0;; ++sw) {
     double* const hout = (spec && (sw & 1)) ? a.H2 : a.H;
     if (spec && sw > 0 && warp == 4) {
-      const int d = tm_decide(a, sw - 1, first_total);
+      const int d = tm_decide(a, sw - 1, first_total, bid, nblk);
       if (lane == 0) {
         s_dec[(sw - 1) & 1] = d;
         if (d) *(volatile int*)&s_abort = 1;  // stop on sw-1: the rest of sweep sw is discarded
@@ -554,8 +556,8 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         const double g = __dadd_rn(__dadd_rn(s_wg[sw & 1][0], s_wg[sw & 1][1]),
                                    __dadd_rn(s_wg[sw & 1][2], s_wg[sw & 1][3]));
         const int f = s_wnf[sw & 1][0] | s_wnf[sw & 1][1] | s_wnf[sw & 1][2] | s_wnf[sw & 1][3];
-        a.part[(sw & 1) * gridDim.x + blockIdx.x] = g;
-        a.part_nf[(sw & 1) * gridDim.x + blockIdx.x] = f;
+        a.part[(sw & 1) * nblk + bid] = g;
+        a.part_nf[(sw & 1) * nblk + bid] = f;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&a.ctl->arrive) : "memory");
       }
       pf.mark(4);
@@ -564,7 +566,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
         break;
       }
       if (last) {                            // max_sweeps reached: no speculation past the cap
-        if (blockIdx.x == 0 && warp == 4) tm_decide(a, sw, first_total);   // bookkeeping only
+        if (bid == 0 && warp == 4) tm_decide(a, sw, first_total, bid, nblk);   // bookkeeping only
         result_sweep = sw;
         break;
       }
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
     // next sweep's fragment loads by the fences around grid_decision's block barriers) ----
     tc::fence_before();
     pf.mark(6);
-    const int cont = grid_decision(a, gain, nf, sw, first_total, red);
+    const int cont = grid_decision(a, gain, nf, sw, first_total, red, bid, nblk);
     tc::fence_after();
     pf.mark(4);
     if (!cont) {
@@ -589,9 +591,9 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
     src = a.H;
   }
 #ifdef ENMF_SWEEP_PROF
-  if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && lane == 0)
+  if ((bid == 0 || bid == nblk / 2) && lane == 0)
     printf("sweep_tm prof cta %d warp %d sweeps %d cycles/sweep: %lld %lld %lld %lld | decision %lld | stage %lld | "
-           "end %lld\n", blockIdx.x, warp, result_sweep + 1, pf.t[0] / (result_sweep + 1), pf.t[1] / (result_sweep + 1),
+           "end %lld\n", bid, warp, result_sweep + 1, pf.t[0] / (result_sweep + 1), pf.t[1] / (result_sweep + 1),
            pf.t[2] / (result_sweep + 1), pf.t[3] / (result_sweep + 1), pf.t[4] / (result_sweep + 1),
            pf.t[5] / (result_sweep + 1), pf.t[6] / (result_sweep + 1));
 #endif
@@ -608,6 +610,23 @@ __global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
     tc::fence_after();
     tc::tmem_dealloc<512>(tmem_base);
   }
+}
+
+
+template <int RMAX>
+__global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
+  tm_body<RMAX>(a, ntiles, blockIdx.x, gridDim.x);
+}
+
+// Several ranks' column shards in ONE cooperative launch: CTAs [v·vblocks, (v+1)·vblocks) run rank
+// v's solve (its own C / H shard, control block, partial buffers and dist::View), so the sharded
+// path — the synchronous grid decision with the cross-rank gain exchange (grid_decision, a.dv) —
+// executes with every rank co-resident on one GPU (enmf_gpu_hals_solve_vranks, tests/test_gpu_dist.py).
+template <int RMAX>
+__global__ void __launch_bounds__(256, 1) sweep_tm_vr(Args a0) {
+  const unsigned v = blockIdx.x / (unsigned)a0.vblocks;
+  const Args a = a0.vargs[v];
+  tm_body<RMAX>(a, ((long)a.N + 7) / 8, blockIdx.x - v * (unsigned)a0.vblocks, (unsigned)a0.vblocks);
 }
 
 }  // namespace hals

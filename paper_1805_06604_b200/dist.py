@@ -76,6 +76,21 @@ def exchange_selftest(ctx: Context, world: int, contributions: np.ndarray, epoch
     return red, sc, rep_w, rep_t
 
 
+def hals_solve_vranks(ctx: Context, gram, cross, h0, world: int, max_sweeps: int, stall_fraction: float = 0.01):
+    """hals_solve sharded by columns over `world` ranks that all run on ONE GPU in one cooperative
+    launch (enmf_gpu_hals_solve_vranks, 64 < r <= 128): the sharded engine's sweep path with its
+    per-sweep cross-rank gain exchange.  Returns (H, [sweeps of every rank])."""
+    gram, cross, h0 = _f64(gram, "gram"), _f64(cross, "cross"), _f64(h0, "h0")
+    r, n = h0.shape
+    if cross.shape != (r, n) or gram.shape != (r, r):
+        raise ValueError("hals_solve_vranks: shape mismatch")
+    h = np.empty_like(h0)
+    sw = (C.c_int32 * world)()
+    _check(ctx._lib.enmf_gpu_hals_solve_vranks(ctx._h, _p(gram), _p(cross), _p(h0), r, n, world, int(max_sweeps),
+                                               float(stall_fraction), _p(h), sw))
+    return h, [int(v) for v in sw]
+
+
 class ShardedContext(Context):
     """An enmf_gpu_ctx in sharded mode (rank `rank` of `world`)."""
 

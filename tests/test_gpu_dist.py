@@ -48,3 +48,22 @@ def test_exchange_primitives_world_n_on_one_gpu(ctx, world):
             want[:, off:off + cnt] = (1000.0 * e + 10.0 * p) + 1e-3 * np.arange(r * cnt).reshape(r, cnt)
         for p in range(world):
             assert np.array_equal(rep[p], want), (world, which, p)
+
+
+@pytest.mark.parametrize("world,r,n", [(2, 128, 3000), (4, 100, 2222), (3, 72, 1000), (8, 128, 4099)])
+def test_sharded_hals_sweeps_world_n_on_one_gpu(ctx, world, r, n):
+    """The sharded sweep path of the headline kernel (hals::sweep_tm with grid_decision's cross-rank
+    gain exchange, dist::allreduce_gain) with 2-8 ranks co-resident in one cooperative launch
+    (sweep_tm_vr): every rank stops after the same sweep, which is the single-GPU solve's, and the
+    column shards put together are the single-GPU H bit for bit (columns are independent within a
+    sweep, nnls.hpp:111-136; only the stall rule couples them)."""
+    rng = np.random.default_rng(world * 1000 + r)
+    w = rng.random((300, r))
+    g = w.T @ w
+    c = w.T @ rng.random((300, n))
+    h0 = rng.random((r, n))
+    for max_sweeps, stall in ((200, 0.01), (7, 1e-300)):
+        h1, s1 = ctx.hals_solve(g, c, h0, max_sweeps, stall)
+        hv, sv = D.hals_solve_vranks(ctx, g, c, h0, world, max_sweeps, stall)
+        assert sv == [s1] * world, (sv, s1)
+        assert np.array_equal(hv, h1)
