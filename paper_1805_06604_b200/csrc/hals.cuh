@@ -49,7 +49,7 @@ struct Args {
   const dist::View* dv;     // multi-GPU: all-reduce the sweep gain across ranks (nullable)
   const double* Gf;         // sweep_ws: Gram in A-fragment order (ws_prep)
   double* H2;               // sweep_tm: r×N scratch (row stride ld) for odd sweeps (speculative stall decision)
-  // virtual ranks (sweep_tm_vr, one cooperative launch over several ranks' column shards — the
+  // virtual ranks (sweep_tm<128, true>, one cooperative launch over several ranks' column shards — the
   // on-device check of the sharded sweep path, enmf_gpu_hals_solve_vranks): rank v's arguments
   // and the CTAs per rank
   const Args* vargs;
@@ -371,7 +371,7 @@ ENMF_DEV void ws_producer_round(const double* Hs, double* Ss, const double2* gf,
 // partials are in and decides itself; sharded: the last CTA exchanges the gain with the other
 // ranks and publishes the decision.  Returns 1 to continue (same value in every thread).
 // bid / nblk: this CTA's index and the CTA count of its grid (of its virtual rank's share of the
-// grid in sweep_tm_vr).
+// grid in the virtual-rank sweep_tm).
 ENMF_DEV int grid_decision(const Args& a, double gain, int nf, int sw, double& first_total, double* red,
                            unsigned bid = blockIdx.x, unsigned nblk = gridDim.x) {
   __shared__ int s_dec;

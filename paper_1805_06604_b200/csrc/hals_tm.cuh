@@ -309,10 +309,31 @@ ENMF_DEV void tm_stage(uint32_t tg, const double* src, long ld, long col, int nc
   }
 }
 
-// bid / nblk: this CTA's index and the CTA count of its grid (sweep_tm), or of its virtual rank's
-// share of the grid (sweep_tm_vr)
-template <int RMAX>
-ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsigned nblk) {
+// VR (virtual ranks): several ranks' column shards in ONE cooperative launch — CTAs
+// [v·vblocks, (v+1)·vblocks) run rank v's solve (its own C / H shard, control block, partial
+// buffers and dist::View, a0.vargs[v]), so the sharded path — the synchronous grid decision with
+// the cross-rank gain exchange (grid_decision, a.dv) — executes with every rank co-resident on one
+// GPU (enmf_gpu_hals_solve_vranks, tests/test_gpu_dist.py).  bid / nblk: this CTA's index and the
+// CTA count of its grid, or of its virtual rank's share of the grid.
+// (read at the point of use: in the plain kernel they are blockIdx.x / gridDim.x and must not
+// occupy registers across the product loops, which run at the register limit)
+template <bool VR>
+ENMF_DEV unsigned tm_bid(const Args& a0) {
+  if constexpr (VR) return blockIdx.x % (unsigned)a0.vblocks;
+  else return blockIdx.x;
+}
+template <bool VR>
+ENMF_DEV unsigned tm_nblk(const Args& a0) {
+  if constexpr (VR) return (unsigned)a0.vblocks;
+  else return gridDim.x;
+}
+
+template <int RMAX, bool VR = false>
+__global__ void __launch_bounds__(256, 1) sweep_tm(const Args a0, long ntiles) {
+  const Args& a = VR ? a0.vargs[blockIdx.x / (unsigned)(VR ? a0.vblocks : 1)] : a0;
+  if (VR) ntiles = ((long)a.N + 7) / 8;
+#define TM_BID tm_bid<VR>(a0)
+#define TM_NBLK tm_nblk<VR>(a0)
   static_assert(RMAX == 128, "two 32-column groups of RMAX rows fill a TMEM lane quarter");
   constexpr int NB = RMAX / 8;
   constexpr int KS = RMAX / 4;
@@ -357,7 +378,7 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
   const uint32_t tq = tmem_base + ((uint32_t)(32 * pair) << 16);   // this pair's lane quarter
 
   const int idS = 1 + pair, idH = 5 + pair, idP = 9 + pair;
-  const long P = (long)nblk * 4, q = (long)bid * 4 + pair;
+  const long P = (long)TM_NBLK * 4, q = (long)TM_BID * 4 + pair;
   const long tq0 = q * ntiles / P, cnt = (q + 1) * ntiles / P - tq0;
   const int rounds = (int)((cnt + 7) / 8);
   const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
@@ -385,7 +406,7 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
   for (int sw = 0;; ++sw) {
     double* const hout = (spec && (sw & 1)) ? a.H2 : a.H;
     if (spec && sw > 0 && warp == 4) {
-      const int d = tm_decide(a, sw - 1, first_total, bid, nblk);
+      const int d = tm_decide(a, sw - 1, first_total, TM_BID, TM_NBLK);
       if (lane == 0) {
         s_dec[(sw - 1) & 1] = d;
         if (d) *(volatile int*)&s_abort = 1;  // stop on sw-1: the rest of sweep sw is discarded
@@ -556,8 +577,8 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
         const double g = __dadd_rn(__dadd_rn(s_wg[sw & 1][0], s_wg[sw & 1][1]),
                                    __dadd_rn(s_wg[sw & 1][2], s_wg[sw & 1][3]));
         const int f = s_wnf[sw & 1][0] | s_wnf[sw & 1][1] | s_wnf[sw & 1][2] | s_wnf[sw & 1][3];
-        a.part[(sw & 1) * nblk + bid] = g;
-        a.part_nf[(sw & 1) * nblk + bid] = f;
+        a.part[(sw & 1) * TM_NBLK + TM_BID] = g;
+        a.part_nf[(sw & 1) * TM_NBLK + TM_BID] = f;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&a.ctl->arrive) : "memory");
       }
       pf.mark(4);
@@ -566,7 +587,7 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
         break;
       }
       if (last) {                            // max_sweeps reached: no speculation past the cap
-        if (bid == 0 && warp == 4) tm_decide(a, sw, first_total, bid, nblk);   // bookkeeping only
+        if (TM_BID == 0 && warp == 4) tm_decide(a, sw, first_total, TM_BID, TM_NBLK);   // bookkeeping only
         result_sweep = sw;
         break;
       }
@@ -579,7 +600,7 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
     // next sweep's fragment loads by the fences around grid_decision's block barriers) ----
     tc::fence_before();
     pf.mark(6);
-    const int cont = grid_decision(a, gain, nf, sw, first_total, red, bid, nblk);
+    const int cont = grid_decision(a, gain, nf, sw, first_total, red, TM_BID, TM_NBLK);
     tc::fence_after();
     pf.mark(4);
     if (!cont) {
@@ -591,9 +612,9 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
     src = a.H;
   }
 #ifdef ENMF_SWEEP_PROF
-  if ((bid == 0 || bid == nblk / 2) && lane == 0)
+  if ((TM_BID == 0 || TM_BID == TM_NBLK / 2) && lane == 0)
     printf("sweep_tm prof cta %d warp %d sweeps %d cycles/sweep: %lld %lld %lld %lld | decision %lld | stage %lld | "
-           "end %lld\n", bid, warp, result_sweep + 1, pf.t[0] / (result_sweep + 1), pf.t[1] / (result_sweep + 1),
+           "end %lld\n", TM_BID, warp, result_sweep + 1, pf.t[0] / (result_sweep + 1), pf.t[1] / (result_sweep + 1),
            pf.t[2] / (result_sweep + 1), pf.t[3] / (result_sweep + 1), pf.t[4] / (result_sweep + 1),
            pf.t[5] / (result_sweep + 1), pf.t[6] / (result_sweep + 1));
 #endif
@@ -613,20 +634,7 @@ ENMF_DEV void tm_body(const Args& a, long ntiles, const unsigned bid, const unsi
 }
 
 
-template <int RMAX>
-__global__ void __launch_bounds__(256, 1) sweep_tm(Args a, long ntiles) {
-  tm_body<RMAX>(a, ntiles, blockIdx.x, gridDim.x);
-}
-
-// Several ranks' column shards in ONE cooperative launch: CTAs [v·vblocks, (v+1)·vblocks) run rank
-// v's solve (its own C / H shard, control block, partial buffers and dist::View), so the sharded
-// path — the synchronous grid decision with the cross-rank gain exchange (grid_decision, a.dv) —
-// executes with every rank co-resident on one GPU (enmf_gpu_hals_solve_vranks, tests/test_gpu_dist.py).
-template <int RMAX>
-__global__ void __launch_bounds__(256, 1) sweep_tm_vr(Args a0) {
-  const unsigned v = blockIdx.x / (unsigned)a0.vblocks;
-  const Args a = a0.vargs[v];
-  tm_body<RMAX>(a, ((long)a.N + 7) / 8, blockIdx.x - v * (unsigned)a0.vblocks, (unsigned)a0.vblocks);
-}
+#undef TM_BID
+#undef TM_NBLK
 
 }  // namespace hals

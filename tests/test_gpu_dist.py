@@ -54,7 +54,7 @@ def test_exchange_primitives_world_n_on_one_gpu(ctx, world):
 def test_sharded_hals_sweeps_world_n_on_one_gpu(ctx, world, r, n):
     """The sharded sweep path of the headline kernel (hals::sweep_tm with grid_decision's cross-rank
     gain exchange, dist::allreduce_gain) with 2-8 ranks co-resident in one cooperative launch
-    (sweep_tm_vr): every rank stops after the same sweep, which is the single-GPU solve's, and the
+    (sweep_tm<128, true>): every rank stops after the same sweep, which is the single-GPU solve's, and the
     column shards put together are the single-GPU H bit for bit (columns are independent within a
     sweep, nnls.hpp:111-136; only the stall rule couples them)."""
     rng = np.random.default_rng(world * 1000 + r)
