@@ -3,9 +3,11 @@
 //
 // Same blocked Gauss-Seidel scheme as sweep_ws (hals.cuh): per SM sub-partition a warp
 // PAIR — a product warp forming S_b = G[b-rows, :]·H on the FP64 tensor pipe (DMMA.8x8x4)
-// and a row warp finishing the 8 rows of block b one column per lane — strictly
-// alternating, because scalar FP64 starves next to a DMMA stream on the same
-// sub-partition (profiles/r01_xsmsp_probe.txt).  What changes is where H lives:
+// and a row warp finishing the 8 rows of block b — handing blocks back and forth, the
+// products one block ahead of the row solves (tm_producer_round; scalar FP64 starves next
+// to a DMMA stream on the same sub-partition, profiles/r02_share_probe.txt, so only the
+// row pass that can hide under the next pair's products runs next to them).  What changes
+// is where H lives:
 //
 //   * H is kept in TMEM, not shared memory.  Each sub-partition owns its 32-lane quarter
 //     of the 128 × 512 × 32-bit tensor memory (64 KB): lane = column, two 32-column
