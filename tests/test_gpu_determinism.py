@@ -46,6 +46,21 @@ def test_repeated_runs_bitwise(ctx, shape, alg, reps):
         _same(first, ctx.run(x, w0, h0, cfg, E.TimingMode.none))
 
 
+@pytest.mark.parametrize("shape", [(700, 3000, 100), (4096, 4096, 128)])
+def test_tf32_variant_repeated_runs_bitwise(ctx, shape):
+    """The TF32 variant's tcgen05 kernels — the right-looking sweeps with the residual in tensor
+    memory (hals_rl.cuh: TMEM stores → TS-form MMA → mbarrier → TMEM loads, two column groups per
+    CTA on their own barriers) and, at 4096², the kind::tf32 cross-product GEMM — reproduce their
+    records and factors bit for bit."""
+    x, w0, h0 = _problem(*shape, seed=sum(shape) + 1)
+    cfg = _cfg("e-ahals-hp3", 8)
+    cfg.precision = E.Precision.tf32
+    first = ctx.run(x, w0, h0, cfg, E.TimingMode.none)
+    assert first.column("inner_h_count")[1:].min() >= 1
+    for _ in range(5):
+        _same(first, ctx.run(x, w0, h0, cfg, E.TimingMode.none))
+
+
 def test_concurrent_streams_bitwise(ctx):
     """The same problems run alone and as a batch on 4 concurrent streams (persistent sweep
     kernels sharing the SMs with other graphs' kernels): identical results."""
