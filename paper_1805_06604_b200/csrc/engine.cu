@@ -545,7 +545,7 @@ void launch_sweep_tf32(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   CU(cudaLaunchKernelEx(&lc, hals::sweep_tf32<R_>, a, ntiles));
 }
 
-// TF32 variant, 64 < r <= 128: right-looking sweeps with the residual in tensor memory and
+// TF32 variant, r <= 128: right-looking sweeps with the residual in tensor memory and
 // tcgen05 rank-8 updates (hals_rl.cuh) when every CTA's columns fit its two 128-column tiles;
 // ENMF_TF32_SWEEP=mma keeps the mma.sync left-looking kernel (A/B)
 bool sweep_rl_fits(const enmf_gpu_ctx* c, const hals::Args& a) {
@@ -553,7 +553,9 @@ bool sweep_rl_fits(const enmf_gpu_ctx* c, const hals::Args& a) {
     const char* e = std::getenv("ENMF_TF32_SWEEP");
     return e && std::strcmp(e, "mma") == 0;
   }();
-  return !off && a.r > 64 && a.r <= 128 && (long)a.N <= 256L * c->sms;
+  // (below ~256 columns the per-solve staging outweighs the faster sweeps: 200×200 r = 20 runs 11%
+  // faster on the mma.sync kernel, 10304×400 r = 40 23% slower, tools/tf32_small.py)
+  return !off && a.r <= 128 && a.N >= 256 && (long)a.N <= 256L * c->sms;
 }
 
 void launch_sweep_rl(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
@@ -637,9 +639,9 @@ void hals_body(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a, int prec) {
   }
   const int v = hals_variant();
   if (prec == PREC_TF32 && (v == 54 || v == 55)) {  // TF32 variant: block products on the TF32 tensor cores
-    if (r <= 32) launch_sweep_tf32<32>(c, s, a);
+    if (sweep_rl_fits(c, a)) launch_sweep_rl(c, s, a);
+    else if (r <= 32) launch_sweep_tf32<32>(c, s, a);
     else if (r <= 64) launch_sweep_tf32<64>(c, s, a);
-    else if (sweep_rl_fits(c, a)) launch_sweep_rl(c, s, a);
     else launch_sweep_tf32<128>(c, s, a);
   } else if (v == 1) {
 #define SW(S_, T_)                                                                          \

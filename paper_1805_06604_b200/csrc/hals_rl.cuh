@@ -1,4 +1,4 @@
-// hals_rl.cuh — HALS sweeps of the TF32 variant (ENMF_PRECISION_TF32, 64 < r <= 128) on the
+// hals_rl.cuh — HALS sweeps of the TF32 variant (ENMF_PRECISION_TF32, r <= 128) on the
 // tcgen05 tensor cores: RIGHT-LOOKING blocked Gauss-Seidel with the residual in tensor memory
 // (nnls.hpp:111-176; the variant's contract is the final relative error within 1e-4 of FP64).
 //
@@ -22,8 +22,9 @@
 // own mbarrier, named barrier and issuing thread, so one group's MMA round trip overlaps the
 // other's row pass.  H itself (the iterate, FP32) sits in shared memory in the A-operand layout
 // (used as the SS-form A of the first product, then as plain storage).  The kernel is resident
-// only: the launcher uses it when every CTA's columns fit its two tiles (N <= 256·grid) and
-// falls back to sweep_tf32 otherwise.  Grid-wide stall decision: grid_decision (hals.cuh).
+// only: the launcher uses it when every CTA's columns fit its two tiles (N <= 256·grid; and
+// N >= 256, below which the per-solve staging outweighs it) and falls back to sweep_tf32
+// otherwise.  Rows past r are padding (zero Gram rows, unit diagonal); only ⌈r/8⌉ blocks run.  Grid-wide stall decision: grid_decision (hals.cuh).
 #pragma once
 
 #include "hals.cuh"
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   const int tile = warp >> 2, quarter = warp & 3;
   const int mloc = 32 * quarter + lane;                    // this thread's column within its tile
   const int r = a.r;
+  const int nbr = (r + 7) >> 3;                            // row blocks in use (r <= 128)
 
   // ---- per-solve staging: Gram B tiles (TF32, round to nearest) and row-pass constants
 #pragma unroll 1
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
       if (issuer) {
         tc::fence_after();
 #pragma unroll 1
-        for (int s = 0; s < NB; ++s)
+        for (int s = 0; s < nbr; ++s)
           tc::mma_tf32(dR, dA0 + (uint64_t)((s * 256) >> 4), dB0 + (uint64_t)((s * 4096) >> 4), IDESC, 1u);
         tc::commit(mb);
       }
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
     int hmax = 0;
     if (active) {
 #pragma unroll 1
-      for (int b = 0; b < NB; ++b) {
+      for (int b = 0; b < nbr; ++b) {
         // everything that does not need the residual first: constants and the block's old rows
         float gc[44];
 #pragma unroll

@@ -1,7 +1,7 @@
 """GPU tier: the TF32 variant's HALS sweeps at kernel level (enmf_gpu_hals_solve in TF32 precision)
 against the FP64 sweeps of the same problem — the tcgen05 right-looking kernel (hals_rl.cuh:
-residual in tensor memory, rank-8 kind::tf32 updates) for 64 < r <= 128 with every CTA's columns
-resident, the mma.sync kernel (sweep_tf32.cuh) otherwise.  TF32 is a reduced-precision variant
+residual in tensor memory, rank-8 kind::tf32 updates) for r <= 128 with 256 <= N and every CTA's
+columns resident, the mma.sync kernel (sweep_tf32.cuh) otherwise.  TF32 is a reduced-precision variant
 (north_star: final relative error within 1e-4), so the check is on the NNLS objective
 f(H) = ½⟨H, G·H⟩ − ⟨C, H⟩ the sweeps minimise (nnls.hpp:111-176), not on H entry by entry."""
 import numpy as np
@@ -20,9 +20,11 @@ def _objective(g, c, h):
     (128, 5000, 30),     # 34 columns per CTA: tile 0 only
     (128, 29600, 12),    # 200 columns per CTA: both tiles
     (100, 300, 30),      # ragged r, few CTAs
-    (72, 777, 30),       # r just past the mma.sync kernel's range, ragged N
+    (72, 777, 30),       # ragged r and N
     (128, 40000, 6),     # more than 256 columns per CTA: falls back to the mma.sync kernel
-    (64, 900, 20),       # r <= 64: mma.sync kernel
+    (64, 900, 20),       # 8 row blocks of 16
+    (20, 3000, 20),      # 3 row blocks
+    (40, 200, 20),       # fewer than 256 columns: mma.sync kernel
 ])
 def test_tf32_sweeps_reach_the_fp64_objective(r, n, sweeps):
     ctx = E.Context(0)
