@@ -568,7 +568,7 @@ void launch_sweep_rl(enmf_gpu_ctx* c, cudaStream_t s, const hals::Args& a) {
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(256);
+  lc.blockDim = dim3(288);   // eight compute warps + the decision warp
   lc.dynamicSmemBytes = hals::rl_smem_bytes();
   lc.stream = s;
   cudaLaunchAttribute at[1];

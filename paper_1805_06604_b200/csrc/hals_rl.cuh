@@ -24,7 +24,9 @@
 // (used as the SS-form A of the first product, then as plain storage).  The kernel is resident
 // only: the launcher uses it when every CTA's columns fit its two tiles (N <= 256·grid; and
 // N >= 256, below which the per-solve staging outweighs it) and falls back to sweep_tf32
-// otherwise.  Rows past r are padding (zero Gram rows, unit diagonal); only ⌈r/8⌉ blocks run.  Grid-wide stall decision: grid_decision (hals.cuh).
+// otherwise.  Rows past r are padding (zero Gram rows, unit diagonal); only ⌈r/8⌉ blocks run.
+// Stall decision: speculative on one GPU (a ninth warp decides sweep s while the compute warps run
+// s+1, see the sweep loop); grid_decision (hals.cuh) when sharded.  Grid-wide stall decision: grid_decision (hals.cuh).
 #pragma once
 
 #include "hals.cuh"
@@ -74,7 +76,7 @@ ENMF_DEV void rl_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32
 }
 
 template <int RMAX>
-__global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
+__global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
   static_assert(RMAX == 128, "two 128 × 128 residual tiles");
   constexpr int NB = RMAX / 8;
   if (sweep_skipped(a)) return;
@@ -87,14 +89,15 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   __shared__ double red[256 + 33];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = warp >> 2, quarter = warp & 3;
+  const bool helper = warp == 8;                           // ninth warp: the stall decision (speculative path)
+  const int tile = (warp >> 2) & 1, quarter = warp & 3;
   const int mloc = 32 * quarter + lane;                    // this thread's column within its tile
   const int r = a.r;
   const int nbr = (r + 7) >> 3;                            // row blocks in use (r <= 128)
 
   // ---- per-solve staging: Gram B tiles (TF32, round to nearest) and row-pass constants
 #pragma unroll 1
-  for (int e0 = threadIdx.x; e0 < NB * 128 * 8; e0 += 256 * 8) {
+  for (int e0 = threadIdx.x; e0 < NB * 128 * 8 && !helper; e0 += 256 * 8) {
     float v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {                          // 8 loads in flight
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
       *reinterpret_cast<float*>(Gb + rl_b_off(row >> 3, n, row & 7)) = tf32_round(v[u]);
     }
   }
-  for (int e = threadIdx.x; e < NB * 48; e += 256) {
+  for (int e = threadIdx.x; e < NB * 48 && !helper; e += 256) {
     const int b = e / 48, j = e % 48;
     double v = 0.0;
     if (j < 28) {
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   const long c0 = (long)blockIdx.x * a.N / gridDim.x, c1 = (long)(blockIdx.x + 1) * a.N / gridDim.x;
   const int cnt = (int)(c1 - c0);
   const int tcols = tile == 0 ? min(cnt, 128) : max(cnt - 128, 0);   // columns of this thread's tile
-  const bool active = tcols > 0;                           // (warp-uniform, group-uniform)
+  const bool active = !helper && tcols > 0;                // (warp-uniform, group-uniform)
   const bool valid = mloc < tcols;
   const long col = c0 + tile * 128 + mloc;
   const uint32_t tR = tmem_base + (uint32_t)(tile * 128) + ((uint32_t)(32 * quarter) << 16);   // residual tile
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, 128);
   const uint64_t dB0 = tc::desc_noswz(tc::smem_u32(Gb), 128, 256);
   const uint64_t dA0 = tc::desc_noswz(tc::smem_u32(Ht), 128, 4096);
-  const bool issuer = (threadIdx.x & 127) == 0;
+  const bool issuer = !helper && (threadIdx.x & 127) == 0;
   const int bar_id = 1 + tile;
   const double* src = (a.ctl->sweeps == 0) ? a.Hin : a.H;
   const double* hsrc = src + (valid ? col : 0);
@@ -203,10 +206,55 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
     __syncwarp();
   }
 
+  // Speculative stall decision (single GPU, as in sweep_tm): the grid-wide decision costs 3.2 µs
+  // per sweep when every CTA waits for it (profiles/r02_sweep_rl_scan.txt), so sweep s only hands
+  // its gain partial to the CTA's ninth warp and the eight compute warps go on with sweep s+1.
+  // The ninth warp publishes the partial, waits for every CTA's, forms the fixed-order total and
+  // posts a "stop" in shared memory, which each column group picks up at its next step barrier
+  // (and everybody at the end-of-sweep barrier, where the ninth warp arrives only once sweep s is
+  // decided).  A "stop" on s discards s+1: every block's old rows are saved before they are
+  // overwritten — blocks 0..14 in the 240 TMEM columns left over, block 15 in registers — so the
+  // blocks already redone are restored and the others still hold sweep s.  Sharded solves keep the
+  // synchronous grid_decision (its cross-GPU exchange).
+  const bool spec = a.dv == nullptr;
+  const uint32_t tN = tmem_base + 272u + (uint32_t)(tile * 120) + ((uint32_t)(32 * quarter) << 16);   // saved rows of blocks 0..14
+  __shared__ float s_wg[2][8];
+  __shared__ int s_wnf[2][8];
+  __shared__ int s_stop_at;                 // sweep decided to be the last (-1: none yet)
+  __shared__ int g_stop[2][2];              // [column group][step parity]: the group's uniform view of "stop"
+  if (threadIdx.x == 0) s_stop_at = -1;
+  __syncthreads();
+  int restore_upto = 0;                     // blocks [0, restore_upto) come back from the saved rows
+  float xlast[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   double first_total = 0.0;
+  auto arrived = [&]() {
+    unsigned e;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(e) : "l"(&a.ctl->arrive) : "memory");
+    return e;
+  };
+  // (ninth warp) decision on sweep s once every CTA has published it; CTA 0 does the bookkeeping
+  auto decide = [&](int s) {
+    while (arrived() < (unsigned)(s + 1) * gridDim.x) __nanosleep(100);
+    const double* part = a.part + (s & 1) * gridDim.x;
+    const int* part_nf = a.part_nf + (s & 1) * gridDim.x;
+    double v = 0.0;
+    int f = 0;
+    for (int bb = lane; bb < (int)gridDim.x; bb += 32) {
+      v = __dadd_rn(v, __ldcg(part + bb));
+      f |= __ldcg(part_nf + bb);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    f = __any_sync(0xffffffffu, f) ? 1 : 0;
+    if (s == 0) first_total = v;
+    const bool stop = (s + 1 >= a.max_sweeps) || (v <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
+    if (blockIdx.x == 0 && lane == 0) finish_sweep(a, v, f);
+    if (stop && lane == 0) *(volatile int*)&s_stop_at = s;
+  };
   for (int sw = 0;; ++sw) {
     float gain = 0.f;
     int hmax = 0;
+    bool stopped = false;
     if (active) {
 #pragma unroll 1
       for (int b = 0; b < nbr; ++b) {
@@ -246,21 +294,92 @@ __global__ void __launch_bounds__(256, 1) sweep_rl(Args a) {
           hmax = max(hmax, __float_as_int(h));
         }
         rl_st8(tS, dv);
+        if (spec) {                                        // the rows this step overwrites
+          if (b < 15) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) rv[k] = __float_as_uint(x[k]);
+            rl_st8(tN + 8 * b, rv);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xlast[k] = x[k];
+          }
+        }
         *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b)) = make_float4(hn[0], hn[1], hn[2], hn[3]);
         *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b + 4)) = make_float4(hn[4], hn[5], hn[6], hn[7]);
         rl_wait_st();
         tc::fence_before();
+        if (spec && issuer && sw > 0) g_stop[tile][b & 1] = *(volatile int*)&s_stop_at == sw - 1;
         rl_bar(bar_id);
         if (issuer) {
           tc::fence_after();
           rl_mma_ts(dR, dS, dB0 + (uint64_t)((b * 4096) >> 4), IDESC);
           tc::commit(mb);
         }
+        if (spec && sw > 0 && *(volatile int*)&g_stop[tile][b & 1]) {   // sweep sw is discarded
+          restore_upto = b + 1;
+          stopped = true;
+          break;
+        }
       }
     }
     const int nf = hmax >= 0x7F800000 ? 1 : 0;
-    const int cont = grid_decision(a, (double)gain, nf, sw, first_total, red);
-    if (!cont) break;
+    if (!spec) {
+      const int cont = grid_decision(a, (double)gain, nf, sw, first_total, red);
+      if (!cont) break;
+      continue;
+    }
+    // ---- speculative end of sweep `sw`
+    if (!helper) {
+      float g = gain + gain;                               // gains are accumulated halved
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g += __shfl_xor_sync(0xffffffffu, g, off);
+      const int f = __any_sync(0xffffffffu, nf) ? 1 : 0;
+      if (lane == 0) {
+        s_wg[sw & 1][warp] = g;
+        s_wnf[sw & 1][warp] = f;
+      }
+    }
+    __syncthreads();                                       // (the ninth warp arrives once sweep sw-1 is decided)
+    if (sw > 0 && *(volatile int*)&s_stop_at == sw - 1) {  // sweep sw-1 was the last: sweep sw is discarded
+      if (!stopped) restore_upto = active ? nbr : 0;
+      break;
+    }
+    const bool last = sw + 1 >= a.max_sweeps;              // the cap: no speculation past it
+    if (helper) {
+      if (lane == 0) {                                     // this CTA's sweep-sw partial (fixed order over the warps)
+        double g = 0.0;
+        int f = 0;
+        for (int w = 0; w < 8; ++w) {
+          g = __dadd_rn(g, (double)s_wg[sw & 1][w]);
+          f |= s_wnf[sw & 1][w];
+        }
+        a.part[(sw & 1) * gridDim.x + blockIdx.x] = g;
+        a.part_nf[(sw & 1) * gridDim.x + blockIdx.x] = f;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&a.ctl->arrive) : "memory");
+      }
+      __syncwarp();
+      if (!last || blockIdx.x == 0) decide(sw);            // (at the cap: CTA 0 only, for the bookkeeping)
+    }
+    if (last) break;
+  }
+  // a discarded speculative sweep: the blocks it had already redone come back from the saved rows
+  if (active && restore_upto > 0) {
+#pragma unroll 1
+    for (int b = 0; b < restore_upto; ++b) {
+      float o[8];
+      if (b < 15) {
+        uint32_t rv[8];
+        rl_ld8(tN + 8 * b, rv);
+        rl_wait_ld8(rv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = __uint_as_float(rv[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = xlast[k];
+      }
+      *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b)) = make_float4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<float4*>(Ht + rl_a_off(mloc, 8 * b + 4)) = make_float4(o[4], o[5], o[6], o[7]);
+    }
   }
   // the result: this CTA's columns of H (rows < r)
   if (active && valid)
