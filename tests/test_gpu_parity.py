@@ -346,6 +346,39 @@ def test_sharded_engine_world1_matches_single(ctx, port, alg, shape):
     assert np.max(np.abs(h - single.factors.h)) <= 1e-6 * np.max(np.abs(single.factors.h))
 
 
+def test_sharded_engine_world1_tf32_sweeps(ctx, port):
+    """TF32 precision on the sharded engine: the cross products stay FP64 there, the sweeps run on
+    the tcgen05 right-looking kernel with the SYNCHRONOUS grid decision (the sharded path's
+    cross-rank gain exchange; the kernel's ninth warp only joins the barriers).  The run must be
+    finite, repeatable bit for bit, and end within 1e-4 of the FP64 relative error."""
+    from paper_1805_06604_b200.dist import ShardedContext
+    m, n, r = 900, 1100, 100
+    x = port.gen_config(2, m, n, r, 5)
+    w0, h0 = port.random_init(m, n, r, 6)
+    ref = ctx.run(x, w0, h0, _cfg("e-ahals-hp3", 15), E.TimingMode.none)
+    cfg = _cfg("e-ahals-hp3", 15, E.Precision.tf32)
+    runs = []
+    for _ in range(2):
+        sc = ShardedContext(0, 0, 1, m, n, r, lambda b: [b])
+        try:
+            sc.load_sharded(*sc.shard_x(x))
+            sc.begin(w0, h0, cfg)
+            sc.step(cfg.max_outer_iterations)
+            recs = sc.sync()
+            w = np.empty((m, r))
+            h = np.empty((r, n))
+            sc.end(w.ctypes.data, h.ctypes.data)
+        finally:
+            sc.finalize()
+        runs.append((np.array([it.error for it in recs]), w, h))
+    e, w, h = runs[0]
+    assert np.all(np.isfinite(w)) and np.all(np.isfinite(h)) and w.min() >= 0 and h.min() >= 0
+    assert np.array_equal(e, runs[1][0]) and np.array_equal(w, runs[1][1]) and np.array_equal(h, runs[1][2])
+    nx = np.linalg.norm(x)
+    direct = np.linalg.norm(x - w @ h) / nx
+    assert abs(direct - ref.final_relative_error()) <= 1e-4, (direct, ref.final_relative_error())
+
+
 # ------------------------------------------------------------ CSR (SURVEY §8(f) 1)
 def _csr_inputs(golden):
     inp = golden.load("csr_inputs")
