@@ -211,8 +211,7 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
   // its gain partial to the CTA's ninth warp and the eight compute warps go on with sweep s+1.
   // The ninth warp publishes the partial, waits for every CTA's, forms the fixed-order total and
   // posts a "stop" in shared memory, which each column group picks up at its next step barrier
-  // (and everybody at the end-of-sweep barrier, where the ninth warp arrives only once sweep s is
-  // decided).  A "stop" on s discards s+1: every block's old rows are saved before they are
+  // (and everybody at the end of the next sweep, before which sweep s must be decided).  A "stop" on s discards s+1: every block's old rows are saved before they are
   // overwritten — blocks 0..14 in the 240 TMEM columns left over, block 15 in registers — so the
   // blocks already redone are restored and the others still hold sweep s.  Sharded solves keep the
   // synchronous grid_decision (its cross-GPU exchange).
@@ -221,8 +220,12 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
   __shared__ float s_wg[2][8];
   __shared__ int s_wnf[2][8];
   __shared__ int s_stop_at;                 // sweep decided to be the last (-1: none yet)
+  __shared__ int s_decided;                 // last sweep whose decision is in
   __shared__ int g_stop[2][2];              // [column group][step parity]: the group's uniform view of "stop"
-  if (threadIdx.x == 0) s_stop_at = -1;
+  if (threadIdx.x == 0) {
+    s_stop_at = -1;
+    s_decided = -1;
+  }
   __syncthreads();
   int restore_upto = 0;                     // blocks [0, restore_upto) come back from the saved rows
   float xlast[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -249,7 +252,11 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
     if (s == 0) first_total = v;
     const bool stop = (s + 1 >= a.max_sweeps) || (v <= __dmul_rn(a.stall, first_total < 0.0 ? 0.0 : first_total));
     if (blockIdx.x == 0 && lane == 0) finish_sweep(a, v, f);
-    if (stop && lane == 0) *(volatile int*)&s_stop_at = s;
+    if (lane == 0) {
+      if (stop) *(volatile int*)&s_stop_at = s;
+      __threadfence_block();
+      *(volatile int*)&s_decided = s;
+    }
   };
   for (int sw = 0;; ++sw) {
     float gain = 0.f;
@@ -328,7 +335,11 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
       if (!cont) break;
       continue;
     }
-    // ---- speculative end of sweep `sw`
+    // ---- speculative end of sweep `sw`: the compute warps hand their gain partials to the ninth
+    // warp without waiting for anybody (they only ARRIVE at the barrier it syncs on, ids 3 / 4 by
+    // sweep parity), so the two column groups drift independently; they go on once sweep sw-1 is
+    // decided, which it normally has been for most of a sweep
+    const bool last = sw + 1 >= a.max_sweeps;              // the cap: no speculation past it
     if (!helper) {
       float g = gain + gain;                               // gains are accumulated halved
 #pragma unroll
@@ -338,14 +349,20 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
         s_wg[sw & 1][warp] = g;
         s_wnf[sw & 1][warp] = f;
       }
-    }
-    __syncthreads();                                       // (the ninth warp arrives once sweep sw-1 is decided)
-    if (sw > 0 && *(volatile int*)&s_stop_at == sw - 1) {  // sweep sw-1 was the last: sweep sw is discarded
-      if (!stopped) restore_upto = active ? nbr : 0;
-      break;
-    }
-    const bool last = sw + 1 >= a.max_sweeps;              // the cap: no speculation past it
-    if (helper) {
+      __syncwarp();
+      asm volatile("bar.arrive %0, 288;\n" ::"r"(3 + (sw & 1)) : "memory");
+      if (sw > 0) {
+        while (*(volatile int*)&s_decided < sw - 1) {
+        }
+        if (*(volatile int*)&s_stop_at == sw - 1) {        // sweep sw-1 was the last: sweep sw is discarded
+          if (!stopped) restore_upto = active ? nbr : 0;
+          break;
+        }
+      }
+      if (last) break;
+    } else {
+      asm volatile("bar.sync %0, 288;\n" ::"r"(3 + (sw & 1)) : "memory");
+      if (sw > 0 && *(volatile int*)&s_stop_at == sw - 1) break;
       if (lane == 0) {                                     // this CTA's sweep-sw partial (fixed order over the warps)
         double g = 0.0;
         int f = 0;
@@ -359,8 +376,8 @@ __global__ void __launch_bounds__(288, 1) sweep_rl(Args a) {
       }
       __syncwarp();
       if (!last || blockIdx.x == 0) decide(sw);            // (at the cap: CTA 0 only, for the bookkeeping)
+      if (last) break;
     }
-    if (last) break;
   }
   // a discarded speculative sweep: the blocks it had already redone come back from the saved rows
   if (active && restore_upto > 0) {
