@@ -53,10 +53,10 @@ UNIT = "outer_iters/s"
 FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.txt)
 FP64_PEAK_SRC = "measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry)"
 # DRAM bytes per HALS sweep inside sweep_tm: ncu --set full of one 16-sweep launch at C5 size,
-# dram__bytes_read.sum + dram__bytes_write.sum = 80.91 + 396.68 MB (profiles/r02_sweep_tm_lookahead_ncu.txt):
+# dram__bytes_read.sum + dram__bytes_write.sum = 79.85 + 395.90 MB (profiles/r02_sweep_tm_lookahead_ncu.txt):
 # mostly the rows written back each sweep (H ping-pongs between two buffers for the speculative
 # stall decision), C and H reads stay L2-resident
-SWEEP_DRAM_BYTES = (80.908032e6 + 396.680192e6) / 16
+SWEEP_DRAM_BYTES = (79.853056e6 + 395.901952e6) / 16
 # tcgen05 kind::i8 floor: 8192 MAC/cycle/SM (M=128 N≥128 MMAs at 100% in profiles/r02_umma_rate.txt)
 INT8_PEAK_TOPS = 2 * 8192 * 148 * 1.965e9 / 1e12
 INT8_PEAK_SRC = ("tcgen05 kind::i8 MMA floor measured on this pool's B200 (M=128, N>=128: 8192 MAC/cycle/SM, "
